@@ -1,0 +1,197 @@
+/*
+ * kunserve_b200.h -- C ABI of the B200 data plane for KunServe's
+ * parameter-centric overload path (arXiv 2412.18169).
+ *
+ * The reference (pkg/src/dropsim, pure Python) has no FFI: its "device"
+ * is a segment table and a link model.  Each entry point below is the
+ * device implementation behind one reference call site; the citation on
+ * every declaration names the reference function whose semantics it
+ * implements (file:line under /root/reference/pkg/src/dropsim/).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch / CUDA runtime types.
+ *     Streams are passed as `uintptr_t` (a cudaStream_t / CUstream value).
+ *   - status: 0 = ok, 1 = expected refusal (out of pages, restore cannot
+ *     vacate), < 0 = error.  kb_last_error() returns the thread-local text.
+ *     The Python shim maps refusals to the reference's False returns and
+ *     errors to ValueError/RuntimeError with the same text.
+ *   - single driver thread (reference SPEC.md:100); device work is async on
+ *     the caller's stream unless the function says it synchronizes.
+ *
+ * Device layout
+ *   weight VA : num_layers x slab_bytes, layer l at l*slab_bytes; one
+ *               physical VMM handle (cuMemCreate) mapped per held layer.
+ *   KV VA     : [slack pages | residual | dropped slab 0 | dropped slab 1 ...]
+ *               page p at kv_base + p*page_bytes; a page holds one layer of
+ *               `block_tokens` tokens of one request:
+ *               [K|V][n_kv_heads][block_tokens][head_dim] bf16.
+ *   metadata  : page bitmap (1 = live), owner[page] (reverse map),
+ *               block_table[slot][layer][max_pages_per_seq] (int32, -1 empty),
+ *               npages[slot][layer].
+ */
+#ifndef KUNSERVE_B200_H
+#define KUNSERVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KB_OK 0
+#define KB_REFUSED 1
+#define KB_EINVAL (-1)
+#define KB_ECUDA (-2)
+#define KB_ESTATE (-3)
+
+typedef struct kb_pool kb_pool; /* opaque: one instance's HBM on one GPU */
+
+typedef struct kb_model_desc {
+    int32_t num_layers;      /* ModelSpec.num_layers (ref core.py:50-68) */
+    int32_t n_kv_heads;
+    int32_t head_dim;        /* 128 for every BASELINE model */
+    int32_t block_tokens;    /* tokens per page */
+    int64_t slab_bytes;      /* ModelSpec.bytes_per_layer, 2 MiB multiple */
+    int64_t page_bytes;      /* block_tokens * 2 * n_kv_heads * head_dim * 2 */
+} kb_model_desc;
+
+typedef struct kb_pool_info {
+    int64_t extent_pages;    /* mapped KV pages (slack + residual + dropped) */
+    int64_t live_pages;
+    int64_t slack_pages;
+    int64_t max_pages;       /* KV VA capacity in pages */
+    int32_t layers_mapped;   /* layers whose slab is mapped at the weight VA */
+    int32_t device;
+    uint64_t weight_base;    /* device VA of layer 0's slab */
+    uint64_t kv_base;        /* device VA of page 0 */
+    uint64_t block_table;    /* device pointer, int32 [max_slots][L][max_pages_per_seq] */
+    uint64_t npages;         /* device pointer, int32 [max_slots][L] */
+    int32_t max_slots;
+    int32_t max_pages_per_seq;
+} kb_pool_info;
+
+/* One block-table growth request: every layer in [layer_lo, layer_hi) of
+ * `slot` gains `add_pages` pages (lowest free page ids first, assigned in
+ * request order, then layer order, then page order). */
+typedef struct kb_grow {
+    int32_t slot;
+    int32_t layer_lo;
+    int32_t layer_hi;
+    int32_t add_pages;
+} kb_grow;
+
+/* One KV move: flattened page range [flat_lo, flat_hi) of the layer range
+ * [layer_lo, layer_hi) of a request, flat = (layer - layer_lo) * npages + i,
+ * from src_slot in the source pool to dst_slot in the destination pool. */
+typedef struct kb_move {
+    int32_t src_slot;
+    int32_t dst_slot;
+    int32_t layer_lo;
+    int32_t layer_hi;
+    int32_t npages;
+    int32_t flat_lo;
+    int32_t flat_hi;
+    int32_t _pad;
+} kb_move;
+
+/* ---- context / errors ------------------------------------------------- */
+const char* kb_last_error(void);
+int kb_version(void);
+/* Initialise the CUDA primary context of `device` and enable peer access
+ * to the listed peers (NVSwitch: every pair).  Idempotent. */
+int kb_init(int32_t device, const int32_t* peers, int32_t n_peers);
+int kb_vmm_granularity(int32_t device, int64_t* out_bytes);
+
+/* ---- N1: VMM slab pool ------------------------------------------------ */
+/* build_instance (memory.py:132-144): one cuMemCreate slab per layer mapped
+ * into the weight VA, residual budget (hbm_bytes - param_bytes, rounded up
+ * to the granularity) plus `slack_pages` of fragmentation headroom at the
+ * head of the KV VA.  Refuses (KB_EINVAL) when hbm_bytes <= param_bytes. */
+int kb_pool_create(int32_t device, const kb_model_desc* model, int64_t hbm_bytes,
+                   int32_t max_slots, int32_t max_pages_per_seq, int32_t slack_pages,
+                   const int32_t* peers, int32_t n_peers, kb_pool** out);
+int kb_pool_destroy(kb_pool* pool);
+int kb_pool_query(kb_pool* pool, kb_pool_info* out);
+
+/* drop_layers (memory.py:147-172) + the caller's remap charge
+ * (engine.py:796-807): for each layer in [lo, hi) unmap its slab from the
+ * weight VA and map it at the KV VA tail; the new pages are free.
+ * Synchronizes the device first (no in-flight reader of the weights).
+ * remap_ns receives the host wall time of the unmap/map/access calls. */
+int kb_drop_layers(kb_pool* pool, int32_t lo, int32_t hi, int64_t* remap_ns);
+
+/* restore_layers (memory.py:175-197): vacate the last (hi-lo) slabs of the
+ * KV VA -- live pages there move to the lowest free pages below the new
+ * extent (device compaction kernel, block tables rewritten on device) --
+ * then unmap those slabs and map them under the weight VA of [lo, hi).
+ * Returns KB_REFUSED (nothing changed) if the live pages cannot fit.
+ * moved_pages / remap_ns report the compaction size and remap time. */
+int kb_restore_begin(kb_pool* pool, int32_t lo, int32_t hi, uintptr_t stream,
+                     int64_t* moved_pages, int64_t* remap_ns);
+/* complete_restore (memory.py:200-212): bookkeeping only; validates that
+ * [lo, hi) is mapped at the weight VA awaiting the pull. */
+int kb_restore_complete(kb_pool* pool, int32_t lo, int32_t hi);
+/* device pointer of layer `layer`'s slab in the weight VA (0 if unmapped) */
+uint64_t kb_weight_ptr(kb_pool* pool, int32_t layer);
+
+/* ---- N2: paged KV block tables (KVAllocator, memory.py:70-129) ---------- */
+/* Grow block tables on device: the kernel takes the K lowest free page ids
+ * below the extent (K = sum of (layer_hi-layer_lo)*add_pages) and appends
+ * them.  KB_REFUSED if fewer than K pages are free (nothing changed). */
+int kb_pages_grow(kb_pool* pool, const kb_grow* reqs, int32_t n, uintptr_t stream);
+/* Release every page of layers [lo, hi) of each listed slot (free / shrink
+ * of a request's allocation on this member, and the source side of an
+ * exchange once its last chunk lands). */
+int kb_pages_release(kb_pool* pool, const int32_t* slots, int32_t n, int32_t lo,
+                     int32_t hi, uintptr_t stream);
+/* Host copies of device state, for parity checks (synchronizing). */
+int kb_read_block_table(kb_pool* pool, int32_t slot, int32_t layer, int32_t* out,
+                        int32_t cap, int32_t* n_out);
+int kb_read_bitmap(kb_pool* pool, uint32_t* out, int64_t n_words);
+int kb_read_owner(kb_pool* pool, int32_t* out, int64_t n);
+int64_t kb_pages_per_layer_count(kb_pool* pool, int32_t slot, int32_t layer);
+
+/* ---- N4/N5/N7: NVLink peer copy kernels --------------------------------- */
+/* KV exchange / consolidation (exchange.py:146-205, engine.py:690-726,
+ * 1211-1239): copy whole pages named by the two pools' block tables. */
+int kb_copy_pages(kb_pool* dst, kb_pool* src, const kb_move* moves, int32_t n,
+                  uintptr_t stream);
+/* Parameter restore / fetch (exchange.py:208-249): bytes [byte_lo, byte_hi)
+ * of the weight range of layers [lo, hi) from src's weight VA to dst's. */
+int kb_copy_slabs(kb_pool* dst, kb_pool* src, int32_t lo, int32_t hi, int64_t byte_lo,
+                  int64_t byte_hi, uintptr_t stream);
+/* HOST replica source (exchange.py:18, 224-233): pinned host -> weight VA. */
+int kb_copy_slabs_from_host(kb_pool* dst, const void* host_src, int32_t lo, int32_t hi,
+                            int64_t byte_lo, int64_t byte_hi, uintptr_t stream);
+/* Activation hand-off between pipeline stages (engine.py:428-448) and any
+ * other flat device-to-device (peer) copy: 16-byte vector kernel. */
+int kb_copy_bytes(uint64_t dst, uint64_t src, int64_t nbytes, uintptr_t stream);
+
+/* ---- N8: paged attention over the pool --------------------------------- */
+/* Write the new tokens' K/V into their pages.  k, v: [ntok][n_kv_heads][head_dim]
+ * bf16; token t belongs to slot slots[t] at position pos[t]; its page must
+ * already be in the block table. */
+int kb_kv_append(kb_pool* pool, int32_t layer, uint64_t k, uint64_t v,
+                 uint64_t slots, uint64_t pos, int32_t ntok, uintptr_t stream);
+/* Decode: q [nseq][n_q_heads][head_dim] bf16, one query token per sequence
+ * attending to ctx_lens[i] cached tokens of slot slots[i] (including its
+ * own, already appended).  out [nseq][n_q_heads][head_dim] bf16.
+ * workspace: kb_decode_workspace_bytes() bytes of device scratch. */
+int64_t kb_decode_workspace_bytes(int32_t nseq, int32_t n_q_heads, int32_t max_splits);
+int kb_paged_decode(kb_pool* pool, int32_t layer, int32_t n_q_heads, uint64_t q,
+                    uint64_t slots, uint64_t ctx_lens, int32_t nseq, int32_t max_ctx,
+                    float scale, uint64_t out, uint64_t workspace, int32_t max_splits,
+                    uintptr_t stream);
+/* Chunked prefill: for sequence i, q rows [q_off[i], q_off[i]+q_len[i]) are
+ * positions [prefix[i], prefix[i]+q_len[i]) of slot slots[i]; they attend
+ * causally over pages [0, prefix[i]+q_len[i]) (the chunk's K/V must be
+ * appended first).  q/out: [total_q][n_q_heads][head_dim] bf16. */
+int kb_paged_prefill(kb_pool* pool, int32_t layer, int32_t n_q_heads, uint64_t q,
+                     uint64_t slots, uint64_t q_off, uint64_t q_len, uint64_t prefix,
+                     int32_t nseq, int32_t max_q_len, float scale, uint64_t out,
+                     uintptr_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KUNSERVE_B200_H */

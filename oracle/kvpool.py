@@ -1,0 +1,178 @@
+"""ORACLE -- CPU restatement of the device KV pool.  TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+--impl reference leg may import this module, and only as the checker or the
+CPU baseline -- never as the product path.
+
+What it restates.  The reference (pkg/src/dropsim/memory.py) is
+token-granular and position-free: its KVAllocator counts tokens against
+`kvcache_virtual_extent`, `drop_layers` grows the extent by whole layer
+blocks (memory.py:147-172) and `restore_layers` reserves bytes before the
+extent shrinks (memory.py:175-197, 116-124).  The device adds pages and
+block tables underneath; this module restates that device layer with the
+same deterministic rules as csrc/kb_pool.cu, so block tables, owners and
+moved bytes can be compared bit for bit:
+  * grow: the K lowest free page ids below the extent, assigned in request
+    order, then layer order, then page order;
+  * release: every page of (slot, layer in [lo, hi)) goes back to the pool;
+  * drop: the KV extent grows by one slab (slab_bytes / page_bytes pages)
+    per dropped layer, appended at the tail (the tail-mapping described at
+    PAPER.md:1240-1270, "mapping the tail of the KVCache memory");
+  * restore: live pages in the vacated tail move, in ascending order, to the
+    lowest free pages below the new extent (compaction), then the extent
+    shrinks by one slab per restored layer.
+Page contents are optional numpy byte arrays (small configs only) so copies
+and appends can be checked byte for byte.
+
+Parity pinning: the token-level counters this layer sits under are pinned
+against the reference's own outputs (tests/golden/memory_ops.json, produced
+by tests/golden/make_golden.py from pkg/src/dropsim); page ids and page
+bytes have no reference counterpart ("Page/block-table
+layout ... parity unpinned" at the reference level) and are pinned by the
+rules above, which tests/test_oracle.py checks against brute-force.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+
+@dataclass
+class OraclePool:
+    num_layers: int
+    slab_bytes: int
+    page_bytes: int
+    head_pages: int            # slack + residual pages mapped at creation
+    max_slots: int
+    max_pages_per_seq: int
+    track_bytes: bool = False
+    extent: int = field(init=False)
+    live: np.ndarray = field(init=False)
+    owner: dict = field(init=False)
+    bt: dict = field(init=False)       # (slot, layer) -> list of page ids
+    data: Optional[np.ndarray] = field(init=False, default=None)
+
+    def __post_init__(self):
+        assert self.slab_bytes % self.page_bytes == 0
+        self.slab_pages = self.slab_bytes // self.page_bytes
+        self.extent = self.head_pages
+        self.max_pages = self.head_pages + self.num_layers * self.slab_pages
+        self.live = np.zeros(self.max_pages, dtype=bool)
+        self.owner = {}
+        self.bt = {}
+        if self.track_bytes:
+            self.data = np.zeros((self.max_pages, self.page_bytes), dtype=np.uint8)
+
+    # cell id exactly as the device encodes owner[] (csrc/kb_pool.cu grow_kernel)
+    def cell(self, slot: int, layer: int, idx: int) -> int:
+        return (slot * self.num_layers + layer) * self.max_pages_per_seq + idx
+
+    def npages(self, slot: int, layer: int) -> int:
+        return len(self.bt.get((slot, layer), ()))
+
+    @property
+    def live_pages(self) -> int:
+        return int(self.live.sum())
+
+    def grow(self, reqs) -> bool:
+        need = sum((hi - lo) * add for _, lo, hi, add in reqs)
+        free = np.flatnonzero(~self.live[:self.extent])
+        if need > len(free):
+            return False
+        k = 0
+        for slot, lo, hi, add in reqs:
+            for layer in range(lo, hi):
+                row = self.bt.setdefault((slot, layer), [])
+                for _ in range(add):
+                    page = int(free[k])
+                    k += 1
+                    self.owner[page] = self.cell(slot, layer, len(row))
+                    row.append(page)
+                    self.live[page] = True
+        return True
+
+    def release(self, slots, lo: int, hi: int) -> None:
+        for slot in slots:
+            for layer in range(lo, hi):
+                for page in self.bt.pop((slot, layer), []):
+                    self.live[page] = False
+                    self.owner.pop(page, None)
+
+    def drop(self, n_layers: int) -> None:
+        self.extent += n_layers * self.slab_pages
+
+    def restore(self, n_layers: int) -> int:
+        """Vacate the last n slabs; returns pages moved, or -1 if refused."""
+        new_extent = self.extent - n_layers * self.slab_pages
+        src = np.flatnonzero(self.live[new_extent:self.extent]) + new_extent
+        dst = np.flatnonzero(~self.live[:new_extent])[:len(src)]
+        if len(dst) < len(src):
+            return -1
+        for s, d in zip(src.tolist(), dst.tolist()):
+            cell = self.owner.pop(s)
+            slot_layer, idx = divmod(cell, self.max_pages_per_seq)
+            slot, layer = divmod(slot_layer, self.num_layers)
+            self.bt[(slot, layer)][idx] = d
+            self.owner[d] = cell
+            self.live[s] = False
+            self.live[d] = True
+            if self.data is not None:
+                self.data[d] = self.data[s]
+        self.extent = new_extent
+        return len(src)
+
+    # ---- data plane (byte-exact) ----------------------------------------
+
+    def page_view(self, page: int) -> np.ndarray:
+        return self.data[page]
+
+
+def copy_pages(dst: OraclePool, src: OraclePool, moves) -> int:
+    """Byte copy of the flattened page ranges (csrc/kb_copy.cu copy_pages_kernel).
+    Returns bytes moved."""
+    moved = 0
+    for s_slot, d_slot, lo, hi, npages, flo, fhi in moves:
+        for flat in range(flo, fhi):
+            layer = lo + flat // npages
+            idx = flat % npages
+            sp = src.bt[(s_slot, layer)][idx]
+            dp = dst.bt[(d_slot, layer)][idx]
+            dst.data[dp] = src.data[sp]
+            moved += src.page_bytes
+    return moved
+
+
+def kv_append(pool: OraclePool, layer: int, k: np.ndarray, v: np.ndarray, slots, pos,
+              n_kv_heads: int, block_tokens: int, head_dim: int = 128) -> None:
+    """Scatter K/V rows into pages laid out [K|V][kv_head][token][head_dim]
+    (csrc/kb_append.cu).  k, v: uint16 (bf16 bits) [ntok, n_kv_heads, head_dim]."""
+    row_bytes = head_dim * 2
+    half = pool.page_bytes // 2
+    for t in range(k.shape[0]):
+        page = pool.bt[(int(slots[t]), layer)][int(pos[t]) // block_tokens]
+        r = int(pos[t]) % block_tokens
+        buf = pool.data[page]
+        for h in range(n_kv_heads):
+            off = (h * block_tokens + r) * row_bytes
+            buf[off:off + row_bytes] = k[t, h].view(np.uint8)
+            buf[half + off:half + off + row_bytes] = v[t, h].view(np.uint8)
+
+
+def gather_kv(pool: OraclePool, slot: int, layer: int, ctx: int, n_kv_heads: int,
+              block_tokens: int, head_dim: int = 128):
+    """K, V of the first ctx tokens as uint16 arrays [ctx, n_kv_heads, head_dim]."""
+    half = pool.page_bytes // 2
+    k = np.zeros((ctx, n_kv_heads, head_dim), dtype=np.uint16)
+    v = np.zeros_like(k)
+    row = pool.bt[(slot, layer)]
+    for t in range(ctx):
+        page = pool.data[row[t // block_tokens]]
+        r = t % block_tokens
+        for h in range(n_kv_heads):
+            off = (h * block_tokens + r) * head_dim * 2
+            k[t, h] = page[off:off + head_dim * 2].view(np.uint16)
+            v[t, h] = page[half + off:half + off + head_dim * 2].view(np.uint16)
+    return k, v

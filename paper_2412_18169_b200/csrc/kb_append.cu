@@ -1,0 +1,54 @@
+// KV append: scatter the new tokens' K/V rows into their pages.
+//
+// Page layout (one layer, one request, block_tokens tokens):
+//   [K|V][n_kv_heads][block_tokens][head_dim] bf16
+// so one kv head's K (or V) for a page is a contiguous block_tokens x 256 B
+// tile: the unit the attention kernels stage through TMA.
+// The page is found through the pool's block table ON DEVICE:
+//   page = bt[slot][layer][pos / block_tokens], row = pos % block_tokens.
+#include "kb_common.cuh"
+
+namespace kb {
+
+// one warp per (token, kv head): lanes 0-15 move K, lanes 16-31 move V,
+// 16 bytes each (head_dim 128 bf16 = 256 B per row).
+__global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __restrict__ bt,
+                                 const int4* __restrict__ k, const int4* __restrict__ v,
+                                 const int32_t* __restrict__ slots, const int32_t* __restrict__ pos,
+                                 int ntok, int Hkv, int B, int L, int maxp, int layer,
+                                 int64_t page_bytes) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ntok * Hkv) return;
+  const int t = warp / Hkv, h = warp % Hkv;
+  const int slot = slots[t], p = pos[t];
+  const int32_t page = bt[((int64_t)slot * L + layer) * maxp + p / B];
+  const int row = p % B;
+  const int which = lane >> 4;  // 0 = K, 1 = V
+  const int4* src = (which ? v : k) + ((int64_t)t * Hkv + h) * 16 + (lane & 15);
+  const int64_t half = page_bytes / 2;
+  int4* dst = reinterpret_cast<int4*>(kv + (int64_t)page * page_bytes + which * half +
+                                      ((int64_t)h * B + row) * 256) + (lane & 15);
+  *dst = *src;
+}
+
+}  // namespace kb
+
+using namespace kb;
+
+extern "C" int kb_kv_append(kb_pool* p, int32_t layer, uint64_t k, uint64_t v, uint64_t slots,
+                            uint64_t pos, int32_t ntok, uintptr_t stream) {
+  if (!p) return fail(KB_EINVAL, "null pool");
+  if (p->m.head_dim != 128) return fail(KB_EINVAL, "head_dim must be 128");
+  if (layer < 0 || layer >= p->m.num_layers) return fail(KB_EINVAL, "bad layer");
+  if (ntok <= 0) return KB_OK;
+  KB_RT(cudaSetDevice(p->device));
+  const int64_t warps = (int64_t)ntok * p->m.n_kv_heads;
+  kv_append_kernel<<<(int)ceil_div(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<uint8_t*>(p->kva), p->d_bt, reinterpret_cast<const int4*>(k),
+      reinterpret_cast<const int4*>(v), reinterpret_cast<const int32_t*>(slots),
+      reinterpret_cast<const int32_t*>(pos), ntok, p->m.n_kv_heads, p->m.block_tokens,
+      p->m.num_layers, p->maxp, layer, p->m.page_bytes);
+  KB_LAUNCH_CHECK();
+  return KB_OK;
+}

@@ -1,0 +1,120 @@
+// Shared internals of the kunserve_b200 C-ABI library (sm_100a).
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/kunserve_b200.h"
+
+namespace kb {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+// CUDA driver entry points, resolved at run time through the runtime's
+// cudaGetDriverEntryPoint so the library has no link-time libcuda
+// dependency (it loads -- and exports its ABI -- on a host without a GPU).
+struct Driver {
+  PFN_cuMemCreate MemCreate = nullptr;
+  PFN_cuMemRelease MemRelease = nullptr;
+  PFN_cuMemMap MemMap = nullptr;
+  PFN_cuMemUnmap MemUnmap = nullptr;
+  PFN_cuMemSetAccess MemSetAccess = nullptr;
+  PFN_cuMemAddressReserve MemAddressReserve = nullptr;
+  PFN_cuMemAddressFree MemAddressFree = nullptr;
+  PFN_cuMemGetAllocationGranularity MemGetAllocationGranularity = nullptr;
+  PFN_cuTensorMapEncodeTiled TensorMapEncodeTiled = nullptr;
+  PFN_cuGetErrorString GetErrorString = nullptr;
+  bool ready = false;
+};
+Driver& drv();
+int ensure_driver();
+
+#define KB_CU(call)                                                           \
+  do {                                                                        \
+    CUresult _r = (call);                                                     \
+    if (_r != CUDA_SUCCESS) {                                                 \
+      const char* _s = nullptr;                                               \
+      if (::kb::drv().GetErrorString) ::kb::drv().GetErrorString(_r, &_s);     \
+      return ::kb::fail(KB_ECUDA, std::string(#call) + ": " + (_s ? _s : "?")); \
+    }                                                                         \
+  } while (0)
+
+#define KB_RT(call)                                                           \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      return ::kb::fail(KB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    }                                                                         \
+  } while (0)
+
+#define KB_LAUNCH_CHECK()                                                     \
+  do {                                                                        \
+    cudaError_t _e = cudaGetLastError();                                      \
+    if (_e != cudaSuccess) {                                                  \
+      return ::kb::fail(KB_ECUDA, std::string("launch: ") + cudaGetErrorString(_e)); \
+    }                                                                         \
+  } while (0)
+
+struct KvSeg {
+  CUmemGenericAllocationHandle h;
+  int64_t bytes;
+  bool slab;  // a dropped layer slab (restorable) vs the head segment
+};
+
+}  // namespace kb
+
+struct kb_pool {
+  int device = 0;
+  kb_model_desc m{};
+  int64_t hbm_bytes = 0;
+  int64_t gran = 0;
+  std::vector<int> access;  // devices granted RW on every mapping (self first)
+
+  CUdeviceptr wva = 0;
+  size_t wva_size = 0;
+  CUdeviceptr kva = 0;
+  size_t kva_size = 0;
+  std::vector<CUmemGenericAllocationHandle> layer_handle;  // 0 = unmapped
+  std::vector<uint8_t> awaiting_restore;                   // mapped, pull pending
+  std::vector<kb::KvSeg> kv_segs;
+  int64_t kv_mapped_bytes = 0;
+
+  int64_t extent_pages = 0;
+  int64_t slack_pages = 0;
+  int64_t max_pages = 0;
+  int64_t live_pages = 0;
+  int64_t n_words = 0;
+
+  int max_slots = 0;
+  int maxp = 0;  // max pages per (slot, layer)
+  uint32_t* d_bitmap = nullptr;
+  int32_t* d_owner = nullptr;
+  int32_t* d_bt = nullptr;
+  int32_t* d_np = nullptr;
+  std::vector<int32_t> h_np;  // host mirror of npages
+
+  // scratch: device buffer for request lists and compaction pairs
+  void* d_scratch = nullptr;
+  int64_t scratch_bytes = 0;
+  int32_t* h_pinned = nullptr;  // small pinned readback buffer
+  cudaStream_t own_stream = nullptr;
+  // TMA descriptor over the whole KV VA viewed as [rows][head_dim] bf16
+  // (row = one token of one kv head of K or V), box = [block_tokens][64].
+  alignas(64) CUtensorMap kv_tmap;
+};
+
+namespace kb {
+int ensure_scratch(kb_pool* p, int64_t bytes);
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+inline int grid_for(int64_t work, int per_block, int max_blocks) {
+  int64_t g = ceil_div(work, per_block);
+  if (g > max_blocks) g = max_blocks;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+}  // namespace kb

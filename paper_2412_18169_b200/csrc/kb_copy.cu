@@ -1,0 +1,210 @@
+// N4 / N5 / N7: SM-driven peer copy kernels.
+//
+//   kb_copy_pages   KV exchange and dissolve-time consolidation: the moves
+//                   are the device image of plan_exchange's tasks
+//                   (pkg/src/dropsim/exchange.py:146-205) executed at
+//                   engine.py:690-726 / 1211-1239.  Page addresses come from
+//                   the two pools' block tables ON DEVICE; the host never
+//                   sees page ids.
+//   kb_copy_slabs   parameter restore / merge-time fetch: the device image of
+//                   plan_restore_transfers (exchange.py:208-249) used at
+//                   engine.py:762-783 and 1127-1141.
+//   kb_copy_bytes   activation hand-off between pipeline stages
+//                   (engine.py:428-448).
+// Source and destination may live on different GPUs: pools map every slab
+// with cuMemSetAccess for all peers, so a plain ld.global/st.global on the
+// peer VA travels over NVLink.  All kernels move 16-byte vectors with 8
+// loads in flight per thread and a grid of 148 x k blocks.
+#include "kb_common.cuh"
+
+namespace kb {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 8;
+constexpr int64_t kPiece = 32768;  // bytes of one page handled by one block pass
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Copy `nvec` int4 from s to d with the whole block, kUnroll loads in flight.
+__device__ __forceinline__ void block_copy(int4* __restrict__ d, const int4* __restrict__ s,
+                                           int64_t nvec) {
+  for (int64_t v0 = threadIdx.x; v0 < nvec; v0 += (int64_t)kThreads * kUnroll) {
+    int4 r[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      int64_t v = v0 + (int64_t)u * kThreads;
+      if (v < nvec) r[u] = ld_stream(s + v);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      int64_t v = v0 + (int64_t)u * kThreads;
+      if (v < nvec) st_stream(d + v, r[u]);
+    }
+  }
+}
+
+struct PoolView {
+  const int32_t* bt;
+  uint8_t* kv;
+  int L;
+  int maxp;
+};
+
+__global__ void __launch_bounds__(kThreads)
+copy_pages_kernel(PoolView dst, PoolView src, const kb_move* __restrict__ moves,
+                  const int64_t* __restrict__ cum, int n, int64_t total_pages,
+                  int64_t page_bytes, int64_t pieces) {
+  const int64_t piece_bytes = page_bytes / pieces;
+  for (int64_t job = blockIdx.x; job < total_pages * pieces; job += gridDim.x) {
+    const int64_t pg = job / pieces, pc = job % pieces;
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (cum[mid] <= pg) lo = mid; else hi = mid - 1;
+    }
+    const kb_move mv = moves[lo];
+    const int64_t flat = mv.flat_lo + (pg - cum[lo]);
+    const int layer = mv.layer_lo + (int)(flat / mv.npages);
+    const int idx = (int)(flat % mv.npages);
+    const int32_t sp = src.bt[((int64_t)mv.src_slot * src.L + layer) * src.maxp + idx];
+    const int32_t dp = dst.bt[((int64_t)mv.dst_slot * dst.L + layer) * dst.maxp + idx];
+    const int4* s = reinterpret_cast<const int4*>(src.kv + (int64_t)sp * page_bytes + pc * piece_bytes);
+    int4* d = reinterpret_cast<int4*>(dst.kv + (int64_t)dp * page_bytes + pc * piece_bytes);
+    block_copy(d, s, piece_bytes / 16);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+copy_flat_kernel(int4* __restrict__ d, const int4* __restrict__ s, int64_t nvec) {
+  // grid-stride over 32 KiB pieces
+  const int64_t per = kPiece / 16;
+  const int64_t pieces = (nvec + per - 1) / per;
+  for (int64_t pc = blockIdx.x; pc < pieces; pc += gridDim.x) {
+    const int64_t beg = pc * per;
+    const int64_t cnt = nvec - beg < per ? nvec - beg : per;
+    block_copy(d + beg, s + beg, cnt);
+  }
+}
+
+__global__ void copy_tail_kernel(uint8_t* __restrict__ d, const uint8_t* __restrict__ s, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+
+static int launch_flat(uint64_t dst, uint64_t src, int64_t nbytes, cudaStream_t st) {
+  if (nbytes <= 0) return KB_OK;
+  const bool aligned = ((dst | src) & 15) == 0;
+  int64_t body = aligned ? (nbytes & ~(int64_t)15) : 0;
+  if (body) {
+    int64_t pieces = ceil_div(body / 16, kPiece / 16);
+    int grid = grid_for(pieces, 1, 148 * 8);
+    copy_flat_kernel<<<grid, kThreads, 0, st>>>(reinterpret_cast<int4*>(dst),
+                                                reinterpret_cast<const int4*>(src), body / 16);
+    KB_LAUNCH_CHECK();
+  }
+  if (nbytes > body) {
+    int64_t rest = nbytes - body;
+    copy_tail_kernel<<<grid_for(rest, 256, 1024), 256, 0, st>>>(
+        reinterpret_cast<uint8_t*>(dst + body), reinterpret_cast<const uint8_t*>(src + body), rest);
+    KB_LAUNCH_CHECK();
+  }
+  return KB_OK;
+}
+
+}  // namespace kb
+
+using namespace kb;
+
+extern "C" int kb_copy_pages(kb_pool* dst, kb_pool* src, const kb_move* moves, int32_t n,
+                             uintptr_t stream) {
+  if (!dst || !src) return fail(KB_EINVAL, "null pool");
+  if (n <= 0) return KB_OK;
+  if (dst->m.page_bytes != src->m.page_bytes || dst->m.num_layers != src->m.num_layers)
+    return fail(KB_EINVAL, "pools disagree on page geometry");
+  const int L = src->m.num_layers;
+  std::vector<int64_t> cum(n);
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    const kb_move& mv = moves[i];
+    if (mv.layer_lo < 0 || mv.layer_hi > L || mv.layer_hi <= mv.layer_lo || mv.npages < 0 ||
+        mv.flat_lo < 0 || mv.flat_hi < mv.flat_lo ||
+        mv.flat_hi > (mv.layer_hi - mv.layer_lo) * mv.npages)
+      return fail(KB_EINVAL, "bad move " + std::to_string(i));
+    for (int l = mv.layer_lo; l < mv.layer_hi; ++l) {
+      if (src->h_np[(int64_t)mv.src_slot * L + l] < mv.npages ||
+          dst->h_np[(int64_t)mv.dst_slot * L + l] < mv.npages)
+        return fail(KB_EINVAL, "move " + std::to_string(i) + " names pages that are not allocated");
+    }
+    cum[i] = total;
+    total += mv.flat_hi - mv.flat_lo;
+  }
+  if (total == 0) return KB_OK;
+  KB_RT(cudaSetDevice(src->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  // request list lives in the source pool's scratch; synchronous hand-off
+  const int64_t mv_bytes = round_up((int64_t)n * sizeof(kb_move), 256);
+  int rc = ensure_scratch(src, mv_bytes + (int64_t)n * 8);
+  if (rc) return rc;
+  kb_move* d_moves = reinterpret_cast<kb_move*>(src->d_scratch);
+  int64_t* d_cum = reinterpret_cast<int64_t*>((char*)src->d_scratch + mv_bytes);
+  KB_RT(cudaMemcpyAsync(d_moves, moves, n * sizeof(kb_move), cudaMemcpyHostToDevice, st));
+  KB_RT(cudaMemcpyAsync(d_cum, cum.data(), n * 8, cudaMemcpyHostToDevice, st));
+  const int64_t pieces = src->m.page_bytes > kPiece ? src->m.page_bytes / kPiece : 1;
+  PoolView dv{dst->d_bt, reinterpret_cast<uint8_t*>(dst->kva), L, dst->maxp};
+  PoolView sv{src->d_bt, reinterpret_cast<uint8_t*>(src->kva), L, src->maxp};
+  int grid = grid_for(total * pieces, 1, 148 * 8);
+  copy_pages_kernel<<<grid, kThreads, 0, st>>>(dv, sv, d_moves, d_cum, n, total,
+                                               src->m.page_bytes, pieces);
+  KB_LAUNCH_CHECK();
+  KB_RT(cudaStreamSynchronize(st));
+  return KB_OK;
+}
+
+extern "C" int kb_copy_slabs(kb_pool* dst, kb_pool* src, int32_t lo, int32_t hi, int64_t byte_lo,
+                             int64_t byte_hi, uintptr_t stream) {
+  if (!dst || !src) return fail(KB_EINVAL, "null pool");
+  if (dst->m.slab_bytes != src->m.slab_bytes) return fail(KB_EINVAL, "pools disagree on slab size");
+  const int64_t slab = src->m.slab_bytes;
+  if (hi <= lo || byte_lo < 0 || byte_hi < byte_lo || byte_hi > (int64_t)(hi - lo) * slab)
+    return fail(KB_EINVAL, "bad slab byte range");
+  for (int l = lo; l < hi; ++l) {
+    if (!src->layer_handle[l]) return fail(KB_ESTATE, "source does not hold layer " + std::to_string(l));
+    if (!dst->layer_handle[l]) return fail(KB_ESTATE, "destination layer " + std::to_string(l) + " is not mapped");
+  }
+  KB_RT(cudaSetDevice(dst->device));
+  uint64_t d = (uint64_t)dst->wva + (uint64_t)lo * slab + byte_lo;
+  uint64_t s = (uint64_t)src->wva + (uint64_t)lo * slab + byte_lo;
+  return launch_flat(d, s, byte_hi - byte_lo, (cudaStream_t)stream);
+}
+
+extern "C" int kb_copy_slabs_from_host(kb_pool* dst, const void* host_src, int32_t lo, int32_t hi,
+                                       int64_t byte_lo, int64_t byte_hi, uintptr_t stream) {
+  if (!dst || !host_src) return fail(KB_EINVAL, "null argument");
+  const int64_t slab = dst->m.slab_bytes;
+  if (hi <= lo || byte_lo < 0 || byte_hi < byte_lo || byte_hi > (int64_t)(hi - lo) * slab)
+    return fail(KB_EINVAL, "bad slab byte range");
+  for (int l = lo; l < hi; ++l)
+    if (!dst->layer_handle[l]) return fail(KB_ESTATE, "destination layer " + std::to_string(l) + " is not mapped");
+  KB_RT(cudaSetDevice(dst->device));
+  KB_RT(cudaMemcpyAsync(reinterpret_cast<void*>(dst->wva + (uint64_t)lo * slab + byte_lo),
+                        static_cast<const char*>(host_src) + byte_lo, byte_hi - byte_lo,
+                        cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return KB_OK;
+}
+
+extern "C" int kb_copy_bytes(uint64_t dst, uint64_t src, int64_t nbytes, uintptr_t stream) {
+  if (nbytes < 0) return fail(KB_EINVAL, "negative size");
+  return launch_flat(dst, src, nbytes, (cudaStream_t)stream);
+}

@@ -1,0 +1,727 @@
+// N1 + N2 + N3: VMM slab pool, device page allocator / block tables, and the
+// restore-time page compaction.
+//
+// Reference semantics followed (pkg/src/dropsim/):
+//   build_instance   memory.py:132-144   -> kb_pool_create
+//   drop_layers      memory.py:147-172   -> kb_drop_layers (unmap weight VA,
+//                                           map at KV VA tail)
+//   restore_layers   memory.py:175-197   -> kb_restore_begin (vacate tail by
+//                                           compaction, remap under weight VA)
+//   complete_restore memory.py:200-212   -> kb_restore_complete
+//   KVAllocator      memory.py:70-129    -> kb_pages_grow / kb_pages_release
+// The reference is token-granular and position-free; pages, block tables and
+// compaction are the device layer underneath.  Every
+// allocation choice is deterministic (lowest free page id first) so the CPU
+// restatement in oracle/kvpool.py reproduces block tables bit for bit.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <mutex>
+
+#include "kb_common.cuh"
+
+namespace kb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+Driver& drv() {
+  static Driver d;
+  return d;
+}
+
+int ensure_driver() {
+  Driver& d = drv();
+  if (d.ready) return KB_OK;
+  KB_RT(cudaFree(nullptr));
+  auto get = [](const char* name, void** fn) -> bool {
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+           q == cudaDriverEntryPointSuccess && *fn != nullptr;
+  };
+  bool ok = get("cuMemCreate", (void**)&d.MemCreate) && get("cuMemRelease", (void**)&d.MemRelease) &&
+            get("cuMemMap", (void**)&d.MemMap) && get("cuMemUnmap", (void**)&d.MemUnmap) &&
+            get("cuMemSetAccess", (void**)&d.MemSetAccess) &&
+            get("cuMemAddressReserve", (void**)&d.MemAddressReserve) &&
+            get("cuMemAddressFree", (void**)&d.MemAddressFree) &&
+            get("cuMemGetAllocationGranularity", (void**)&d.MemGetAllocationGranularity) &&
+            get("cuTensorMapEncodeTiled", (void**)&d.TensorMapEncodeTiled) &&
+            get("cuGetErrorString", (void**)&d.GetErrorString);
+  if (!ok) return fail(KB_ECUDA, "cannot resolve CUDA driver entry points");
+  d.ready = true;
+  return KB_OK;
+}
+
+int ensure_scratch(kb_pool* p, int64_t bytes) {
+  if (p->scratch_bytes >= bytes) return KB_OK;
+  if (p->d_scratch) cudaFree(p->d_scratch);
+  p->d_scratch = nullptr;
+  int64_t want = round_up(bytes < (1 << 20) ? (1 << 20) : bytes * 2, 256);
+  KB_RT(cudaMalloc(&p->d_scratch, want));
+  p->scratch_bytes = want;
+  return KB_OK;
+}
+
+// ---------------------------------------------------------------- kernels
+
+constexpr int kScanThreads = 1024;
+
+// Block-wide exclusive scan of one int per thread (1024 threads).
+__device__ __forceinline__ int block_exclusive_scan(int v, int* total, int* warp_sums) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = warp_sums[lane];
+    int s = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_sums[lane] = s - w;
+    if (lane == 31) *total = s;
+  }
+  __syncthreads();
+  int r = warp_sums[warp] + x - v;
+  __syncthreads();
+  return r;
+}
+
+// Enumerate, in ascending order, the set bits of (select ? live : free) pages
+// in [lo, hi) and hand the k-th one to emit(k, page) for k < limit.  Works
+// in tiles of kScanThreads * kWordsPerThread words; stops once `limit` pages
+// were emitted.  Returns the number found (<= limit) in *found.
+template <int kWordsPerThread, typename Emit>
+__device__ void scan_pages(const uint32_t* __restrict__ bitmap, int64_t lo, int64_t hi,
+                           bool want_live, int64_t limit, Emit emit, int64_t* found_out) {
+  __shared__ int warp_sums[32];
+  __shared__ int tile_total;
+  int64_t found = 0;
+  const int64_t w_lo = lo >> 5, w_hi = (hi + 31) >> 5;
+  const int64_t tile_words = (int64_t)kScanThreads * kWordsPerThread;
+  for (int64_t t0 = w_lo; t0 < w_hi && found < limit; t0 += tile_words) {
+    uint32_t bits[kWordsPerThread];
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kWordsPerThread; ++j) {
+      int64_t w = t0 + (int64_t)threadIdx.x * kWordsPerThread + j;
+      uint32_t b = 0;
+      if (w < w_hi) {
+        uint32_t raw = bitmap[w];
+        b = want_live ? raw : ~raw;
+        int64_t base = w << 5;
+        if (base < lo) b &= ~0u << (lo - base);           // drop pages < lo
+        if (base + 32 > hi) {                             // drop pages >= hi
+          int64_t keep = hi - base;
+          b &= keep <= 0 ? 0u : (keep >= 32 ? ~0u : ((1u << keep) - 1u));
+        }
+      }
+      bits[j] = b;
+      cnt += __popc(b);
+    }
+    int off = block_exclusive_scan(cnt, &tile_total, warp_sums);
+    int64_t k = found + off;
+#pragma unroll
+    for (int j = 0; j < kWordsPerThread; ++j) {
+      uint32_t b = bits[j];
+      int64_t base = (t0 + (int64_t)threadIdx.x * kWordsPerThread + j) << 5;
+      while (b && k < limit) {
+        int bit = __ffs(b) - 1;
+        b &= b - 1;
+        emit(k, base + bit);
+        ++k;
+      }
+    }
+    found += tile_total;
+    __syncthreads();
+  }
+  if (found_out) *found_out = found < limit ? found : limit;
+}
+
+// Grow: requests with exclusive prefix `cum` (pages per request); the k-th
+// lowest free page below `extent` goes to flattened slot k.
+__global__ void __launch_bounds__(kScanThreads)
+grow_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner, int32_t* __restrict__ bt,
+            int32_t* __restrict__ np, const kb_grow* __restrict__ reqs,
+            const int64_t* __restrict__ cum, int n, int64_t total, int64_t extent, int L,
+            int maxp, int32_t* __restrict__ status) {
+  auto emit = [&](int64_t k, int64_t page) {
+    int lo = 0, hi = n - 1;  // last request with cum <= k
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (cum[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    const kb_grow r = reqs[lo];
+    int64_t rem = k - cum[lo];
+    int layer = r.layer_lo + (int)(rem / r.add_pages);
+    int idx = np[(int64_t)r.slot * L + layer] + (int)(rem % r.add_pages);
+    int64_t cell = ((int64_t)r.slot * L + layer) * maxp + idx;
+    bt[cell] = (int32_t)page;
+    owner[page] = (int32_t)cell;
+    atomicOr(&bitmap[page >> 5], 1u << (page & 31));
+  };
+  int64_t found = 0;
+  scan_pages<4>(bitmap, 0, extent, false, total, emit, &found);
+  __syncthreads();
+  if (found < total) {
+    if (threadIdx.x == 0) status[0] = 1;
+    return;  // host checked capacity first; this is a consistency failure
+  }
+  // advance per-(slot, layer) page counts
+  for (int i = 0; i < n; ++i) {
+    const kb_grow r = reqs[i];
+    for (int l = r.layer_lo + threadIdx.x; l < r.layer_hi; l += blockDim.x)
+      np[(int64_t)r.slot * L + l] += r.add_pages;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) status[0] = 0;
+}
+
+// Release all pages of (slot, layer) for layers in [lo, hi): one block per pair.
+__global__ void release_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner,
+                               int32_t* __restrict__ bt, int32_t* __restrict__ np,
+                               const int32_t* __restrict__ slots, int lo, int hi, int L,
+                               int maxp) {
+  const int span = hi - lo;
+  const int slot = slots[blockIdx.x / span];
+  const int layer = lo + blockIdx.x % span;
+  int32_t* row = bt + ((int64_t)slot * L + layer) * maxp;
+  const int cnt = np[(int64_t)slot * L + layer];
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    int32_t page = row[i];
+    atomicAnd(&bitmap[page >> 5], ~(1u << (page & 31)));
+    owner[page] = -1;
+    row[i] = -1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) np[(int64_t)slot * L + layer] = 0;
+}
+
+// Compaction plan: live pages in [new_extent, extent) ascending -> src[],
+// the same number of lowest free pages below new_extent -> dst[].
+__global__ void __launch_bounds__(kScanThreads)
+compact_plan_kernel(const uint32_t* __restrict__ bitmap, int64_t new_extent, int64_t extent,
+                    int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t cap,
+                    int64_t* __restrict__ counts) {
+  int64_t m = 0;
+  scan_pages<4>(bitmap, new_extent, extent, true, cap,
+                [&](int64_t k, int64_t page) { src[k] = (int32_t)page; }, &m);
+  __syncthreads();
+  int64_t f = 0;
+  scan_pages<4>(bitmap, 0, new_extent, false, m,
+                [&](int64_t k, int64_t page) { dst[k] = (int32_t)page; }, &f);
+  if (threadIdx.x == 0) {
+    counts[0] = m;
+    counts[1] = f;
+  }
+}
+
+// Move page contents src[i] -> dst[i] within one pool (HBM read+write).
+// One block per 32 KiB piece of a page; 16-byte vector accesses, 8 in flight
+// per thread.
+constexpr int kPieceBytes = 32768;
+constexpr int kCopyThreads = 256;
+
+__global__ void __launch_bounds__(kCopyThreads)
+compact_copy_kernel(uint8_t* __restrict__ kv, const int32_t* __restrict__ src,
+                    const int32_t* __restrict__ dst, const int64_t* __restrict__ counts,
+                    int64_t page_bytes) {
+  const int64_t pieces = page_bytes / kPieceBytes > 0 ? page_bytes / kPieceBytes : 1;
+  const int64_t piece_bytes = page_bytes / pieces;
+  const int64_t m = counts[0];
+  for (int64_t job = blockIdx.x; job < m * pieces; job += gridDim.x) {
+    const int64_t i = job / pieces, pc = job % pieces;
+    const int4* s = reinterpret_cast<const int4*>(kv + (int64_t)src[i] * page_bytes + pc * piece_bytes);
+    int4* d = reinterpret_cast<int4*>(kv + (int64_t)dst[i] * page_bytes + pc * piece_bytes);
+    const int64_t nvec = piece_bytes / 16;
+    for (int64_t v0 = threadIdx.x; v0 < nvec; v0 += (int64_t)kCopyThreads * 8) {
+      int4 r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int64_t v = v0 + (int64_t)u * kCopyThreads;
+        if (v < nvec) r[u] = s[v];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int64_t v = v0 + (int64_t)u * kCopyThreads;
+        if (v < nvec) d[v] = r[u];
+      }
+    }
+  }
+}
+
+// Rewrite block tables / owners / bitmap for the moved pages.
+__global__ void compact_fixup_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner,
+                                     int32_t* __restrict__ bt, const int32_t* __restrict__ src,
+                                     const int32_t* __restrict__ dst,
+                                     const int64_t* __restrict__ counts) {
+  const int64_t m = counts[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = src[i], d = dst[i];
+    const int32_t cell = owner[s];
+    bt[cell] = d;
+    owner[d] = cell;
+    owner[s] = -1;
+    atomicOr(&bitmap[d >> 5], 1u << (d & 31));
+    atomicAnd(&bitmap[s >> 5], ~(1u << (s & 31)));
+  }
+}
+
+// ---------------------------------------------------------------- VMM helpers
+
+static int make_handle(int device, int64_t bytes, CUmemGenericAllocationHandle* out) {
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  KB_CU(drv().MemCreate(out, (size_t)bytes, &prop, 0));
+  return KB_OK;
+}
+
+static int map_at(kb_pool* p, CUdeviceptr va, int64_t bytes, CUmemGenericAllocationHandle h) {
+  KB_CU(drv().MemMap(va, (size_t)bytes, 0, h, 0));
+  std::vector<CUmemAccessDesc> acc(p->access.size());
+  for (size_t i = 0; i < p->access.size(); ++i) {
+    acc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc[i].location.id = p->access[i];
+    acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  }
+  KB_CU(drv().MemSetAccess(va, (size_t)bytes, acc.data(), acc.size()));
+  return KB_OK;
+}
+
+static int set_device(int device) {
+  KB_RT(cudaSetDevice(device));
+  KB_RT(cudaFree(nullptr));  // materialise the primary context
+  return ensure_driver();
+}
+
+static int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+}  // namespace kb
+
+using namespace kb;
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" const char* kb_last_error(void) { return g_err.c_str(); }
+extern "C" int kb_version(void) { return 1; }
+
+extern "C" int kb_init(int32_t device, const int32_t* peers, int32_t n_peers) {
+  int rc = set_device(device);
+  if (rc) return rc;
+  for (int i = 0; i < n_peers; ++i) {
+    if (peers[i] == device) continue;
+    int can = 0;
+    KB_RT(cudaDeviceCanAccessPeer(&can, device, peers[i]));
+    if (!can) return fail(KB_EINVAL, "device " + std::to_string(device) +
+                                         " cannot access peer " + std::to_string(peers[i]));
+    cudaError_t e = cudaDeviceEnablePeerAccess(peers[i], 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+      return fail(KB_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+  }
+  return KB_OK;
+}
+
+extern "C" int kb_vmm_granularity(int32_t device, int64_t* out_bytes) {
+  int rc = set_device(device);
+  if (rc) return rc;
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g = 0;
+  KB_CU(drv().MemGetAllocationGranularity(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  *out_bytes = (int64_t)g;
+  return KB_OK;
+}
+
+extern "C" int kb_pool_create(int32_t device, const kb_model_desc* model, int64_t hbm_bytes,
+                              int32_t max_slots, int32_t max_pages_per_seq, int32_t slack_pages,
+                              const int32_t* peers, int32_t n_peers, kb_pool** out) {
+  *out = nullptr;
+  const kb_model_desc m = *model;
+  const int64_t param = (int64_t)m.num_layers * m.slab_bytes;
+  if (m.num_layers < 1 || m.slab_bytes < 1 || m.page_bytes < 1 || m.block_tokens < 1)
+    return fail(KB_EINVAL, "model byte sizes must be positive");
+  if (m.page_bytes != (int64_t)m.block_tokens * 2 * m.n_kv_heads * m.head_dim * 2)
+    return fail(KB_EINVAL, "page_bytes != block_tokens * 2 * n_kv_heads * head_dim * 2");
+  if (hbm_bytes <= param)
+    return fail(KB_EINVAL, "HBM " + std::to_string(hbm_bytes) + " cannot hold one parameter copy");
+  int64_t gran = 0;
+  int rc = kb_vmm_granularity(device, &gran);
+  if (rc) return rc;
+  if (m.slab_bytes % gran) return fail(KB_EINVAL, "slab_bytes must be a multiple of the VMM granularity");
+  if (gran % m.page_bytes) return fail(KB_EINVAL, "page_bytes must divide the VMM granularity");
+  if (max_slots < 1 || max_pages_per_seq < 1 || slack_pages < 0)
+    return fail(KB_EINVAL, "bad slot / page limits");
+
+  kb_pool* p = new kb_pool();
+  p->device = device;
+  p->m = m;
+  p->hbm_bytes = hbm_bytes;
+  p->gran = gran;
+  p->access.push_back(device);
+  for (int i = 0; i < n_peers; ++i)
+    if (peers[i] != device) p->access.push_back(peers[i]);
+  p->max_slots = max_slots;
+  p->maxp = max_pages_per_seq;
+
+  auto bail = [&](int code) {
+    kb_pool_destroy(p);
+    return code;
+  };
+  // weight VA: one slab per layer
+  p->wva_size = (size_t)param;
+  CUresult r = drv().MemAddressReserve(&p->wva, p->wva_size, (size_t)gran, 0, 0);
+  if (r != CUDA_SUCCESS) return bail(fail(KB_ECUDA, "drv().MemAddressReserve(weights) failed"));
+  p->layer_handle.assign(m.num_layers, 0);
+  p->awaiting_restore.assign(m.num_layers, 0);
+  for (int l = 0; l < m.num_layers; ++l) {
+    CUmemGenericAllocationHandle h;
+    if ((rc = make_handle(device, m.slab_bytes, &h))) return bail(rc);
+    p->layer_handle[l] = h;
+    if ((rc = map_at(p, p->wva + (CUdeviceptr)l * m.slab_bytes, m.slab_bytes, h))) return bail(rc);
+  }
+  // KV VA: head segment (slack + residual) then room for every slab
+  const int64_t head = round_up((int64_t)slack_pages * m.page_bytes + (hbm_bytes - param), gran);
+  p->kva_size = (size_t)(head + param);
+  r = drv().MemAddressReserve(&p->kva, p->kva_size, (size_t)gran, 0, 0);
+  if (r != CUDA_SUCCESS) return bail(fail(KB_ECUDA, "drv().MemAddressReserve(kv) failed"));
+  {
+    CUmemGenericAllocationHandle h;
+    if ((rc = make_handle(device, head, &h))) return bail(rc);
+    p->kv_segs.push_back({h, head, false});
+    if ((rc = map_at(p, p->kva, head, h))) return bail(rc);
+    p->kv_mapped_bytes = head;
+  }
+  if (m.head_dim == 128 && (m.block_tokens == 64 || m.block_tokens == 128)) {
+    cuuint64_t dims[2] = {128, (cuuint64_t)(p->kva_size / 256)};
+    cuuint64_t strides[1] = {256};
+    cuuint32_t box[2] = {64, (cuuint32_t)m.block_tokens};
+    cuuint32_t estr[2] = {1, 1};
+    r = drv().TensorMapEncodeTiled(&p->kv_tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                               reinterpret_cast<void*>(p->kva), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return bail(fail(KB_ECUDA, "drv().TensorMapEncodeTiled(kv) failed"));
+  }
+  p->slack_pages = slack_pages;
+  p->extent_pages = head / m.page_bytes;
+  p->max_pages = (int64_t)p->kva_size / m.page_bytes;
+  if (p->max_pages >= (int64_t)1 << 31) return bail(fail(KB_EINVAL, "too many pages for int32 ids"));
+  p->n_words = ceil_div(p->max_pages, 32);
+  const int64_t cells = (int64_t)max_slots * m.num_layers;
+  if (cells * max_pages_per_seq >= (int64_t)1 << 31)
+    return bail(fail(KB_EINVAL, "block table too large for int32 cells"));
+  if (cudaMalloc(&p->d_bitmap, p->n_words * 4) != cudaSuccess ||
+      cudaMalloc(&p->d_owner, p->max_pages * 4) != cudaSuccess ||
+      cudaMalloc(&p->d_bt, cells * max_pages_per_seq * 4) != cudaSuccess ||
+      cudaMalloc(&p->d_np, cells * 4) != cudaSuccess)
+    return bail(fail(KB_ECUDA, "cudaMalloc(pool metadata) failed"));
+  cudaMemset(p->d_bitmap, 0, p->n_words * 4);
+  cudaMemset(p->d_owner, 0xff, p->max_pages * 4);
+  cudaMemset(p->d_bt, 0xff, cells * max_pages_per_seq * 4);
+  cudaMemset(p->d_np, 0, cells * 4);
+  p->h_np.assign(cells, 0);
+  if (cudaMallocHost(&p->h_pinned, 64) != cudaSuccess)
+    return bail(fail(KB_ECUDA, "cudaMallocHost failed"));
+  if (cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(KB_ECUDA, "cudaStreamCreate failed"));
+  if ((rc = ensure_scratch(p, 1 << 20))) return bail(rc);
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(KB_ECUDA, "pool init sync failed"));
+  *out = p;
+  return KB_OK;
+}
+
+extern "C" int kb_pool_destroy(kb_pool* p) {
+  if (!p) return KB_OK;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  for (int l = 0; l < (int)p->layer_handle.size(); ++l) {
+    if (p->layer_handle[l]) {
+      drv().MemUnmap(p->wva + (CUdeviceptr)l * p->m.slab_bytes, p->m.slab_bytes);
+      drv().MemRelease(p->layer_handle[l]);
+    }
+  }
+  int64_t off = 0;
+  for (auto& s : p->kv_segs) {
+    drv().MemUnmap(p->kva + off, s.bytes);
+    drv().MemRelease(s.h);
+    off += s.bytes;
+  }
+  if (p->wva) drv().MemAddressFree(p->wva, p->wva_size);
+  if (p->kva) drv().MemAddressFree(p->kva, p->kva_size);
+  if (p->d_bitmap) cudaFree(p->d_bitmap);
+  if (p->d_owner) cudaFree(p->d_owner);
+  if (p->d_bt) cudaFree(p->d_bt);
+  if (p->d_np) cudaFree(p->d_np);
+  if (p->d_scratch) cudaFree(p->d_scratch);
+  if (p->h_pinned) cudaFreeHost(p->h_pinned);
+  if (p->own_stream) cudaStreamDestroy(p->own_stream);
+  delete p;
+  return KB_OK;
+}
+
+extern "C" int kb_pool_query(kb_pool* p, kb_pool_info* o) {
+  if (!p || !o) return fail(KB_EINVAL, "null pool");
+  o->extent_pages = p->extent_pages;
+  o->live_pages = p->live_pages;
+  o->slack_pages = p->slack_pages;
+  o->max_pages = p->max_pages;
+  int mapped = 0;
+  for (auto h : p->layer_handle) mapped += h != 0;
+  o->layers_mapped = mapped;
+  o->device = p->device;
+  o->weight_base = (uint64_t)p->wva;
+  o->kv_base = (uint64_t)p->kva;
+  o->block_table = (uint64_t)p->d_bt;
+  o->npages = (uint64_t)p->d_np;
+  o->max_slots = p->max_slots;
+  o->max_pages_per_seq = p->maxp;
+  return KB_OK;
+}
+
+extern "C" uint64_t kb_weight_ptr(kb_pool* p, int32_t layer) {
+  if (!p || layer < 0 || layer >= p->m.num_layers || !p->layer_handle[layer]) return 0;
+  return (uint64_t)(p->wva + (CUdeviceptr)layer * p->m.slab_bytes);
+}
+
+extern "C" int kb_drop_layers(kb_pool* p, int32_t lo, int32_t hi, int64_t* remap_ns) {
+  if (!p) return fail(KB_EINVAL, "null pool");
+  if (hi <= lo) return fail(KB_EINVAL, "empty layer range");
+  for (int l = lo; l < hi; ++l) {
+    if (l < 0 || l >= p->m.num_layers) return fail(KB_EINVAL, "layer " + std::to_string(l) + " absent from segment table");
+    if (!p->layer_handle[l] || p->awaiting_restore[l])
+      return fail(KB_ESTATE, "layer " + std::to_string(l) + " absent on device pool");
+  }
+  KB_RT(cudaSetDevice(p->device));
+  const int64_t t0 = now_ns();
+  KB_RT(cudaDeviceSynchronize());  // no in-flight reader of these weights
+  const int64_t slab = p->m.slab_bytes;
+  for (int l = lo; l < hi; ++l) {
+    CUmemGenericAllocationHandle h = p->layer_handle[l];
+    KB_CU(drv().MemUnmap(p->wva + (CUdeviceptr)l * slab, slab));
+    p->layer_handle[l] = 0;
+    int rc = map_at(p, p->kva + p->kv_mapped_bytes, slab, h);
+    if (rc) return rc;
+    p->kv_segs.push_back({h, slab, true});
+    p->kv_mapped_bytes += slab;
+    p->extent_pages += slab / p->m.page_bytes;
+  }
+  if (remap_ns) *remap_ns = now_ns() - t0;
+  return KB_OK;
+}
+
+extern "C" int kb_restore_begin(kb_pool* p, int32_t lo, int32_t hi, uintptr_t stream,
+                                int64_t* moved_pages, int64_t* remap_ns) {
+  if (!p) return fail(KB_EINVAL, "null pool");
+  if (hi <= lo) return fail(KB_EINVAL, "empty layer range");
+  const int n = hi - lo;
+  for (int l = lo; l < hi; ++l) {
+    if (l < 0 || l >= p->m.num_layers) return fail(KB_EINVAL, "layer " + std::to_string(l) + " absent from segment table");
+    if (p->layer_handle[l]) return fail(KB_ESTATE, "layer " + std::to_string(l) + " already held on device pool");
+  }
+  int tail_slabs = 0;
+  for (int i = (int)p->kv_segs.size() - 1; i >= 0 && p->kv_segs[i].slab; --i) ++tail_slabs;
+  if (tail_slabs < n) return fail(KB_ESTATE, "KV tail holds fewer dropped slabs than the restore needs");
+  KB_RT(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t slab_pages = p->m.slab_bytes / p->m.page_bytes;
+  const int64_t new_extent = p->extent_pages - (int64_t)n * slab_pages;
+  const int64_t cap = (int64_t)n * slab_pages;
+  int rc = ensure_scratch(p, 2 * cap * 4 + 64);
+  if (rc) return rc;
+  int64_t* d_counts = reinterpret_cast<int64_t*>(p->d_scratch);
+  int32_t* d_src = reinterpret_cast<int32_t*>((char*)p->d_scratch + 64);
+  int32_t* d_dst = d_src + cap;
+  compact_plan_kernel<<<1, kScanThreads, 0, st>>>(p->d_bitmap, new_extent, p->extent_pages, d_src,
+                                                   d_dst, cap, d_counts);
+  KB_LAUNCH_CHECK();
+  int64_t counts[2];
+  KB_RT(cudaMemcpyAsync(counts, d_counts, 16, cudaMemcpyDeviceToHost, st));
+  KB_RT(cudaStreamSynchronize(st));
+  if (counts[1] < counts[0]) {
+    return fail(KB_REFUSED, "restore blocked: " + std::to_string(counts[0]) +
+                                " live tail pages but only " + std::to_string(counts[1]) +
+                                " free pages below the new extent");
+  }
+  if (counts[0] > 0) {
+    const int64_t pieces = p->m.page_bytes / kPieceBytes > 0 ? p->m.page_bytes / kPieceBytes : 1;
+    int grid = grid_for(counts[0] * pieces, 1, 148 * 16);
+    compact_copy_kernel<<<grid, kCopyThreads, 0, st>>>(reinterpret_cast<uint8_t*>(p->kva), d_src,
+                                                       d_dst, d_counts, p->m.page_bytes);
+    KB_LAUNCH_CHECK();
+    compact_fixup_kernel<<<grid_for(counts[0], 256, 1024), 256, 0, st>>>(p->d_bitmap, p->d_owner,
+                                                                          p->d_bt, d_src, d_dst,
+                                                                          d_counts);
+    KB_LAUNCH_CHECK();
+  }
+  const int64_t t0 = now_ns();
+  KB_RT(cudaDeviceSynchronize());
+  const int64_t slab = p->m.slab_bytes;
+  for (int k = 0; k < n; ++k) {
+    kb::KvSeg s = p->kv_segs.back();
+    p->kv_segs.pop_back();
+    p->kv_mapped_bytes -= s.bytes;
+    KB_CU(drv().MemUnmap(p->kva + p->kv_mapped_bytes, s.bytes));
+    p->extent_pages -= slab_pages;
+    rc = map_at(p, p->wva + (CUdeviceptr)(lo + k) * slab, slab, s.h);
+    if (rc) return rc;
+    p->layer_handle[lo + k] = s.h;
+    p->awaiting_restore[lo + k] = 1;
+  }
+  if (moved_pages) *moved_pages = counts[0];
+  if (remap_ns) *remap_ns = now_ns() - t0;
+  return KB_OK;
+}
+
+extern "C" int kb_restore_complete(kb_pool* p, int32_t lo, int32_t hi) {
+  if (!p) return fail(KB_EINVAL, "null pool");
+  for (int l = lo; l < hi; ++l) {
+    if (l < 0 || l >= p->m.num_layers || !p->layer_handle[l] || !p->awaiting_restore[l])
+      return fail(KB_ESTATE, "layer " + std::to_string(l) + " not awaiting restore");
+  }
+  for (int l = lo; l < hi; ++l) p->awaiting_restore[l] = 0;
+  return KB_OK;
+}
+
+extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr_t stream) {
+  if (!p) return fail(KB_EINVAL, "null pool");
+  if (n <= 0) return KB_OK;
+  const int L = p->m.num_layers;
+  std::vector<int64_t> cum(n);
+  int64_t total = 0;
+  std::vector<uint8_t> seen;  // duplicate (slot, layer) detection
+  for (int i = 0; i < n; ++i) {
+    const kb_grow& r = reqs[i];
+    if (r.slot < 0 || r.slot >= p->max_slots || r.layer_lo < 0 || r.layer_hi > L ||
+        r.layer_hi <= r.layer_lo || r.add_pages < 1)
+      return fail(KB_EINVAL, "bad grow request " + std::to_string(i));
+    for (int l = r.layer_lo; l < r.layer_hi; ++l) {
+      int64_t c = (int64_t)r.slot * L + l;
+      if (p->h_np[c] + r.add_pages > p->maxp)
+        return fail(KB_EINVAL, "slot " + std::to_string(r.slot) + " exceeds max_pages_per_seq");
+    }
+    cum[i] = total;
+    total += (int64_t)(r.layer_hi - r.layer_lo) * r.add_pages;
+  }
+  if (n > 1) {
+    std::vector<int64_t> cells;
+    for (int i = 0; i < n; ++i)
+      for (int l = reqs[i].layer_lo; l < reqs[i].layer_hi; ++l)
+        cells.push_back((int64_t)reqs[i].slot * L + l);
+    std::sort(cells.begin(), cells.end());
+    for (size_t i = 1; i < cells.size(); ++i)
+      if (cells[i] == cells[i - 1]) return fail(KB_EINVAL, "duplicate (slot, layer) in one grow batch");
+  }
+  if (total > p->extent_pages - p->live_pages)
+    return fail(KB_REFUSED, "out of KV pages: need " + std::to_string(total) + ", free " +
+                                std::to_string(p->extent_pages - p->live_pages));
+  KB_RT(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t req_bytes = round_up((int64_t)n * sizeof(kb_grow), 256);
+  int rc = ensure_scratch(p, req_bytes + (int64_t)n * 8 + 64);
+  if (rc) return rc;
+  char* base = (char*)p->d_scratch;
+  kb_grow* d_reqs = reinterpret_cast<kb_grow*>(base);
+  int64_t* d_cum = reinterpret_cast<int64_t*>(base + req_bytes);
+  int32_t* d_status = reinterpret_cast<int32_t*>(base + req_bytes + round_up((int64_t)n * 8, 64));
+  KB_RT(cudaMemcpyAsync(d_reqs, reqs, n * sizeof(kb_grow), cudaMemcpyHostToDevice, st));
+  KB_RT(cudaMemcpyAsync(d_cum, cum.data(), n * 8, cudaMemcpyHostToDevice, st));
+  grow_kernel<<<1, kScanThreads, 0, st>>>(p->d_bitmap, p->d_owner, p->d_bt, p->d_np, d_reqs, d_cum,
+                                          n, total, p->extent_pages, L, p->maxp, d_status);
+  KB_LAUNCH_CHECK();
+  for (int i = 0; i < n; ++i)
+    for (int l = reqs[i].layer_lo; l < reqs[i].layer_hi; ++l)
+      p->h_np[(int64_t)reqs[i].slot * L + l] += reqs[i].add_pages;
+  p->live_pages += total;
+  // the host-side scratch (reqs/cum) is reused by the next call: make sure
+  // this kernel consumed it before returning
+  KB_RT(cudaStreamSynchronize(st));
+  return KB_OK;
+}
+
+extern "C" int kb_pages_release(kb_pool* p, const int32_t* slots, int32_t n, int32_t lo,
+                                int32_t hi, uintptr_t stream) {
+  if (!p) return fail(KB_EINVAL, "null pool");
+  const int L = p->m.num_layers;
+  if (n <= 0 || hi <= lo) return KB_OK;
+  if (lo < 0 || hi > L) return fail(KB_EINVAL, "bad layer range");
+  int64_t freed = 0;
+  for (int i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= p->max_slots) return fail(KB_EINVAL, "bad slot");
+    for (int l = lo; l < hi; ++l) freed += p->h_np[(int64_t)slots[i] * L + l];
+  }
+  KB_RT(cudaSetDevice(p->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_scratch(p, (int64_t)n * 4);
+  if (rc) return rc;
+  int32_t* d_slots = reinterpret_cast<int32_t*>(p->d_scratch);
+  KB_RT(cudaMemcpyAsync(d_slots, slots, n * 4, cudaMemcpyHostToDevice, st));
+  release_kernel<<<n * (hi - lo), 128, 0, st>>>(p->d_bitmap, p->d_owner, p->d_bt, p->d_np, d_slots,
+                                                 lo, hi, L, p->maxp);
+  KB_LAUNCH_CHECK();
+  for (int i = 0; i < n; ++i)
+    for (int l = lo; l < hi; ++l) p->h_np[(int64_t)slots[i] * L + l] = 0;
+  p->live_pages -= freed;
+  KB_RT(cudaStreamSynchronize(st));
+  return KB_OK;
+}
+
+extern "C" int64_t kb_pages_per_layer_count(kb_pool* p, int32_t slot, int32_t layer) {
+  if (!p || slot < 0 || slot >= p->max_slots || layer < 0 || layer >= p->m.num_layers) return -1;
+  return p->h_np[(int64_t)slot * p->m.num_layers + layer];
+}
+
+extern "C" int kb_read_block_table(kb_pool* p, int32_t slot, int32_t layer, int32_t* out,
+                                   int32_t cap, int32_t* n_out) {
+  if (!p || slot < 0 || slot >= p->max_slots || layer < 0 || layer >= p->m.num_layers)
+    return fail(KB_EINVAL, "bad slot/layer");
+  KB_RT(cudaSetDevice(p->device));
+  KB_RT(cudaDeviceSynchronize());
+  int cnt = 0;
+  KB_RT(cudaMemcpy(&cnt, p->d_np + (int64_t)slot * p->m.num_layers + layer, 4, cudaMemcpyDeviceToHost));
+  if (cnt > cap) return fail(KB_EINVAL, "output buffer too small");
+  if (cnt)
+    KB_RT(cudaMemcpy(out, p->d_bt + ((int64_t)slot * p->m.num_layers + layer) * p->maxp,
+                     (size_t)cnt * 4, cudaMemcpyDeviceToHost));
+  *n_out = cnt;
+  return KB_OK;
+}
+
+extern "C" int kb_read_bitmap(kb_pool* p, uint32_t* out, int64_t n_words) {
+  if (!p || n_words > p->n_words) return fail(KB_EINVAL, "bad bitmap read");
+  KB_RT(cudaSetDevice(p->device));
+  KB_RT(cudaDeviceSynchronize());
+  KB_RT(cudaMemcpy(out, p->d_bitmap, (size_t)n_words * 4, cudaMemcpyDeviceToHost));
+  return KB_OK;
+}
+
+extern "C" int kb_read_owner(kb_pool* p, int32_t* out, int64_t n) {
+  if (!p || n > p->max_pages) return fail(KB_EINVAL, "bad owner read");
+  KB_RT(cudaSetDevice(p->device));
+  KB_RT(cudaDeviceSynchronize());
+  KB_RT(cudaMemcpy(out, p->d_owner, (size_t)n * 4, cudaMemcpyDeviceToHost));
+  return KB_OK;
+}

@@ -1,0 +1,354 @@
+"""ctypes binding of the C-ABI data plane (include/kunserve_b200.h -> _kb.so).
+
+This is the only path to the device: there is no host fallback.  Importing
+this module without a built `_kb.so` raises immediately, and every call
+checks the C status and re-raises the library's message.
+
+Objects:
+  Runtime     one GPU (CUDA primary context, peer access); creates pools.
+  DevicePool  one instance's HBM: VMM slab pool + paged KV pool + block
+              tables (the device side of memory.build_instance).
+Free functions wrap the copy / append / attention entry points; tensors are
+torch CUDA tensors passed by data_ptr (borrowed for the duration of the
+call; the caller keeps them alive until its stream is synchronized).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+from .core import ModelShape, ModelSpec
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_kb.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with "
+                      "`python -m paper_2412_18169_b200.build` (no CPU fallback exists)")
+_lib = C.CDLL(LIB_PATH)
+
+KB_OK, KB_REFUSED = 0, 1
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("n_kv_heads", C.c_int32),
+                ("head_dim", C.c_int32), ("block_tokens", C.c_int32),
+                ("slab_bytes", C.c_int64), ("page_bytes", C.c_int64)]
+
+
+class PoolInfo(C.Structure):
+    _fields_ = [("extent_pages", C.c_int64), ("live_pages", C.c_int64),
+                ("slack_pages", C.c_int64), ("max_pages", C.c_int64),
+                ("layers_mapped", C.c_int32), ("device", C.c_int32),
+                ("weight_base", C.c_uint64), ("kv_base", C.c_uint64),
+                ("block_table", C.c_uint64), ("npages", C.c_uint64),
+                ("max_slots", C.c_int32), ("max_pages_per_seq", C.c_int32)]
+
+
+class Grow(C.Structure):
+    _fields_ = [("slot", C.c_int32), ("layer_lo", C.c_int32), ("layer_hi", C.c_int32),
+                ("add_pages", C.c_int32)]
+
+
+class Move(C.Structure):
+    _fields_ = [("src_slot", C.c_int32), ("dst_slot", C.c_int32), ("layer_lo", C.c_int32),
+                ("layer_hi", C.c_int32), ("npages", C.c_int32), ("flat_lo", C.c_int32),
+                ("flat_hi", C.c_int32), ("_pad", C.c_int32)]
+
+
+_P = C.c_void_p
+_I32P = C.POINTER(C.c_int32)
+_I64P = C.POINTER(C.c_int64)
+_U = C.c_uint64
+_S = C.c_size_t  # uintptr_t stream
+
+_sigs = {
+    "kb_last_error": (C.c_char_p, []),
+    "kb_version": (C.c_int, []),
+    "kb_init": (C.c_int, [C.c_int32, _I32P, C.c_int32]),
+    "kb_vmm_granularity": (C.c_int, [C.c_int32, _I64P]),
+    "kb_pool_create": (C.c_int, [C.c_int32, C.POINTER(ModelDesc), C.c_int64, C.c_int32,
+                                 C.c_int32, C.c_int32, _I32P, C.c_int32, C.POINTER(_P)]),
+    "kb_pool_destroy": (C.c_int, [_P]),
+    "kb_pool_query": (C.c_int, [_P, C.POINTER(PoolInfo)]),
+    "kb_drop_layers": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P]),
+    "kb_restore_begin": (C.c_int, [_P, C.c_int32, C.c_int32, _S, _I64P, _I64P]),
+    "kb_restore_complete": (C.c_int, [_P, C.c_int32, C.c_int32]),
+    "kb_weight_ptr": (C.c_uint64, [_P, C.c_int32]),
+    "kb_pages_grow": (C.c_int, [_P, C.POINTER(Grow), C.c_int32, _S]),
+    "kb_pages_release": (C.c_int, [_P, _I32P, C.c_int32, C.c_int32, C.c_int32, _S]),
+    "kb_read_block_table": (C.c_int, [_P, C.c_int32, C.c_int32, _I32P, C.c_int32, _I32P]),
+    "kb_read_bitmap": (C.c_int, [_P, C.POINTER(C.c_uint32), C.c_int64]),
+    "kb_read_owner": (C.c_int, [_P, _I32P, C.c_int64]),
+    "kb_pages_per_layer_count": (C.c_int64, [_P, C.c_int32, C.c_int32]),
+    "kb_copy_pages": (C.c_int, [_P, _P, C.POINTER(Move), C.c_int32, _S]),
+    "kb_copy_slabs": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int64, C.c_int64, _S]),
+    "kb_copy_slabs_from_host": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int64,
+                                          C.c_int64, _S]),
+    "kb_copy_bytes": (C.c_int, [_U, _U, C.c_int64, _S]),
+    "kb_kv_append": (C.c_int, [_P, C.c_int32, _U, _U, _U, _U, C.c_int32, _S]),
+    "kb_decode_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
+    "kb_paged_decode": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, C.c_int32, C.c_int32,
+                                  C.c_float, _U, _U, C.c_int32, _S]),
+    "kb_paged_prefill": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, _U, _U, C.c_int32,
+                                   C.c_int32, C.c_float, _U, _S]),
+}
+for _name, (_res, _args) in _sigs.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+EXPORTED = tuple(_sigs)
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+class Refused(Exception):
+    """Expected refusal (KB_REFUSED): out of pages / restore cannot vacate."""
+
+
+def _check(rc: int) -> None:
+    if rc == KB_OK:
+        return
+    msg = _lib.kb_last_error().decode()
+    if rc == KB_REFUSED:
+        raise Refused(msg)
+    raise DeviceError(f"kb error {rc}: {msg}")
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _i32arr(vals: Sequence[int]):
+    arr = (C.c_int32 * max(1, len(vals)))(*vals)
+    return arr
+
+
+class _CudaBuf:
+    """Raw device range exposed to torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
+def device_bytes(ptr: int, nbytes: int):
+    """uint8 torch view of a device range owned by the library."""
+    import torch
+    return torch.as_tensor(_CudaBuf(ptr, nbytes), device="cuda")
+
+
+class Runtime:
+    """One GPU.  `peers` lists other devices every mapping must be accessible
+    from (NVSwitch: all of them)."""
+
+    def __init__(self, device: int = 0, peers: Sequence[int] = (), max_slots: int = 1024,
+                 max_pages_per_seq: int = 1024, slack_pages: Optional[int] = None):
+        self.device = device
+        self.peers = list(peers)
+        self.max_slots = max_slots
+        self.max_pages_per_seq = max_pages_per_seq
+        self.slack_pages = slack_pages
+        _check(_lib.kb_init(device, _i32arr(self.peers), len(self.peers)))
+
+    def granularity(self) -> int:
+        g = C.c_int64()
+        _check(_lib.kb_vmm_granularity(self.device, C.byref(g)))
+        return g.value
+
+    def create_pool(self, iid: int, model: ModelSpec, hbm_bytes: int,
+                    shape: Optional[ModelShape] = None) -> "DevicePool":
+        if shape is None:
+            raise ValueError("device-backed instances need a ModelShape (page geometry)")
+        return DevicePool(self, iid, model, hbm_bytes, shape)
+
+
+class DevicePool:
+    def __init__(self, rt: Runtime, iid: int, model: ModelSpec, hbm_bytes: int,
+                 shape: ModelShape):
+        if model.num_layers != shape.num_layers or \
+                model.kv_bytes_per_token != shape.kv_bytes_per_token:
+            raise ValueError("ModelSpec and ModelShape disagree")
+        self.rt = rt
+        self.iid = iid
+        self.model = model
+        self.shape = shape
+        self.desc = ModelDesc(model.num_layers, shape.n_kv_heads, shape.head_dim,
+                              shape.block_tokens, model.bytes_per_layer, shape.page_bytes)
+        self.slack_pages = rt.slack_pages if rt.slack_pages is not None \
+            else model.num_layers * 64
+        h = _P()
+        _check(_lib.kb_pool_create(rt.device, C.byref(self.desc), hbm_bytes, rt.max_slots,
+                                   rt.max_pages_per_seq, self.slack_pages,
+                                   _i32arr(rt.peers), len(rt.peers), C.byref(h)))
+        self.h = h
+        self.last_remap_ns = 0
+        self.last_moved_pages = 0
+
+    # -- lifecycle
+    def close(self) -> None:
+        if self.h:
+            _lib.kb_pool_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> PoolInfo:
+        out = PoolInfo()
+        _check(_lib.kb_pool_query(self.h, C.byref(out)))
+        return out
+
+    @property
+    def page_bytes(self) -> int:
+        return self.shape.page_bytes
+
+    @property
+    def slab_pages(self) -> int:
+        return self.model.bytes_per_layer // self.shape.page_bytes
+
+    # -- N1 / N3: drop and restore (memory.drop_layers / restore_layers)
+    def drop_layers(self, lo: int, hi: int) -> int:
+        ns = C.c_int64()
+        _check(_lib.kb_drop_layers(self.h, lo, hi, C.byref(ns)))
+        self.last_remap_ns = ns.value
+        return ns.value
+
+    def restore_begin(self, lo: int, hi: int, stream=None) -> int:
+        moved, ns = C.c_int64(), C.c_int64()
+        _check(_lib.kb_restore_begin(self.h, lo, hi, _stream(stream), C.byref(moved),
+                                     C.byref(ns)))
+        self.last_moved_pages = moved.value
+        self.last_remap_ns = ns.value
+        return moved.value
+
+    def restore_complete(self, lo: int, hi: int) -> None:
+        _check(_lib.kb_restore_complete(self.h, lo, hi))
+
+    def weight_ptr(self, layer: int) -> int:
+        return int(_lib.kb_weight_ptr(self.h, layer))
+
+    def weight_bytes(self, layer: int):
+        ptr = self.weight_ptr(layer)
+        if not ptr:
+            raise DeviceError(f"layer {layer} is not mapped on pool {self.iid}")
+        return device_bytes(ptr, self.model.bytes_per_layer)
+
+    def kv_bytes(self):
+        """uint8 view of the mapped KV extent (pages [0, extent))."""
+        inf = self.info()
+        return device_bytes(inf.kv_base, inf.extent_pages * self.page_bytes)
+
+    # -- N2: block tables
+    def grow(self, reqs: Sequence[tuple[int, int, int, int]], stream=None) -> bool:
+        """reqs: (slot, layer_lo, layer_hi, add_pages).  False = out of pages."""
+        if not reqs:
+            return True
+        arr = (Grow * len(reqs))(*[Grow(*r) for r in reqs])
+        try:
+            _check(_lib.kb_pages_grow(self.h, arr, len(reqs), _stream(stream)))
+        except Refused:
+            return False
+        return True
+
+    def release(self, slots: Sequence[int], lo: int, hi: int, stream=None) -> None:
+        if not slots:
+            return
+        _check(_lib.kb_pages_release(self.h, _i32arr(slots), len(slots), lo, hi,
+                                     _stream(stream)))
+
+    def npages(self, slot: int, layer: int) -> int:
+        return int(_lib.kb_pages_per_layer_count(self.h, slot, layer))
+
+    def block_table(self, slot: int, layer: int) -> list[int]:
+        cap = self.rt.max_pages_per_seq
+        buf = (C.c_int32 * cap)()
+        n = C.c_int32()
+        _check(_lib.kb_read_block_table(self.h, slot, layer, buf, cap, C.byref(n)))
+        return list(buf[:n.value])
+
+    def bitmap(self, n_pages: Optional[int] = None):
+        import numpy as np
+        n_pages = n_pages or self.info().extent_pages
+        words = (n_pages + 31) // 32
+        buf = (C.c_uint32 * words)()
+        _check(_lib.kb_read_bitmap(self.h, buf, words))
+        bits = np.unpackbits(np.frombuffer(bytes(buf), dtype=np.uint8), bitorder="little")
+        return bits[:n_pages].astype(bool)
+
+    def owners(self, n_pages: Optional[int] = None):
+        import numpy as np
+        n_pages = n_pages or self.info().extent_pages
+        buf = (C.c_int32 * n_pages)()
+        _check(_lib.kb_read_owner(self.h, buf, n_pages))
+        return np.frombuffer(bytes(buf), dtype=np.int32).copy()
+
+
+# -- N4 / N5 / N7 copies ------------------------------------------------------
+
+def copy_pages(dst: DevicePool, src: DevicePool,
+               moves: Sequence[tuple[int, int, int, int, int, int, int]], stream=None) -> None:
+    """moves: (src_slot, dst_slot, layer_lo, layer_hi, npages, flat_lo, flat_hi)."""
+    if not moves:
+        return
+    arr = (Move * len(moves))(*[Move(*m, 0) for m in moves])
+    _check(_lib.kb_copy_pages(dst.h, src.h, arr, len(moves), _stream(stream)))
+
+
+def copy_slabs(dst: DevicePool, src: DevicePool, lo: int, hi: int, byte_lo: int,
+               byte_hi: int, stream=None) -> None:
+    _check(_lib.kb_copy_slabs(dst.h, src.h, lo, hi, byte_lo, byte_hi, _stream(stream)))
+
+
+def copy_slabs_from_host(dst: DevicePool, host_ptr: int, lo: int, hi: int, byte_lo: int,
+                         byte_hi: int, stream=None) -> None:
+    _check(_lib.kb_copy_slabs_from_host(dst.h, C.c_void_p(host_ptr), lo, hi, byte_lo, byte_hi,
+                                        _stream(stream)))
+
+
+def copy_bytes(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:
+    _check(_lib.kb_copy_bytes(dst_ptr, src_ptr, nbytes, _stream(stream)))
+
+
+# -- N8 attention -------------------------------------------------------------
+
+def kv_append(pool: DevicePool, layer: int, k, v, slots, pos, stream=None) -> None:
+    """k, v: [ntok, n_kv_heads, 128] bf16; slots/pos: int32 [ntok] (device)."""
+    _check(_lib.kb_kv_append(pool.h, layer, k.data_ptr(), v.data_ptr(), slots.data_ptr(),
+                             pos.data_ptr(), k.shape[0], _stream(stream)))
+
+
+def decode_workspace_bytes(nseq: int, n_q_heads: int, max_splits: int) -> int:
+    return int(_lib.kb_decode_workspace_bytes(nseq, n_q_heads, max_splits))
+
+
+def paged_decode(pool: DevicePool, layer: int, q, slots, ctx_lens, max_ctx: int, out,
+                 workspace, scale: float, max_splits: int = 16, stream=None) -> None:
+    """q/out: [nseq, n_q_heads, 128] bf16; slots/ctx_lens int32 [nseq] (device)."""
+    _check(_lib.kb_paged_decode(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
+                                ctx_lens.data_ptr(), q.shape[0], max_ctx, scale,
+                                out.data_ptr(), workspace.data_ptr(), max_splits,
+                                _stream(stream)))
+
+
+def paged_prefill(pool: DevicePool, layer: int, q, slots, q_off, q_len, prefix, max_q_len: int,
+                  out, scale: float, stream=None) -> None:
+    """q/out: [total_q, n_q_heads, 128] bf16; per-sequence int32 vectors (device)."""
+    _check(_lib.kb_paged_prefill(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
+                                 q_off.data_ptr(), q_len.data_ptr(), prefix.data_ptr(),
+                                 slots.shape[0], max_q_len, scale, out.data_ptr(),
+                                 _stream(stream)))

@@ -1,0 +1,282 @@
+"""GPU parity: device pool, block tables, copies and attention vs the CPU oracle.
+
+Bit-exact for block tables, bitmaps, owners and every copied byte; attention
+within BASELINE.json's bf16 tolerance (max-abs <= 2e-2, mean-rel <= 1e-3)
+against the fp32 oracle rounded to bf16 (the kernels emit bf16).
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.attention import bf16_to_f32, check_close, decode_ref, f32_to_bf16, prefill_ref  # noqa: E402
+from oracle.kvpool import OraclePool  # noqa: E402
+
+from paper_2412_18169_b200.core import SHAPES, ModelShape  # noqa: E402
+
+TINY = SHAPES["tiny"]
+MIB = 1 << 20
+
+
+@pytest.fixture(scope="module")
+def rt():
+    from paper_2412_18169_b200 import build
+    build.build()
+    from paper_2412_18169_b200 import runtime
+    assert torch.cuda.is_available()
+    return runtime.Runtime(0, max_slots=16, max_pages_per_seq=256, slack_pages=128)
+
+
+def oracle_for(pool):
+    inf = pool.info()
+    return OraclePool(num_layers=pool.model.num_layers, slab_bytes=pool.model.bytes_per_layer,
+                      page_bytes=pool.page_bytes, head_pages=inf.extent_pages,
+                      max_slots=pool.rt.max_slots, max_pages_per_seq=pool.rt.max_pages_per_seq)
+
+
+def assert_same_state(pool, orc, slots):
+    inf = pool.info()
+    assert inf.extent_pages == orc.extent
+    assert inf.live_pages == orc.live_pages
+    bits = pool.bitmap(orc.extent)
+    assert (bits == orc.live[:orc.extent]).all()
+    owners = pool.owners(orc.extent)
+    want = np.full(orc.extent, -1, dtype=np.int32)
+    for pg, cell in orc.owner.items():
+        want[pg] = cell
+    assert (owners == want).all()
+    for s in slots:
+        for l in range(orc.num_layers):
+            assert pool.block_table(s, l) == orc.bt.get((s, l), []), (s, l)
+
+
+def test_pool_ops_match_oracle_bit_exact(rt):
+    from paper_2412_18169_b200 import runtime
+    model = TINY.spec()
+    pool = rt.create_pool(0, model, model.param_bytes + MIB, TINY)
+    orc = oracle_for(pool)
+    rng = random.Random(17)
+    slots = list(range(rt.max_slots))
+    dropped = 0
+    for step in range(300):
+        r = rng.random()
+        if r < 0.45:
+            reqs, used = [], set()
+            for _ in range(rng.randrange(1, 4)):
+                s = rng.choice(slots)
+                lo = rng.randrange(0, 2)
+                hi = rng.randrange(lo + 1, 3)
+                add = rng.randrange(1, 9)
+                cells = {(s, l) for l in range(lo, hi)}
+                if cells & used or any(orc.npages(s, l) + add > rt.max_pages_per_seq
+                                       for l in range(lo, hi)):
+                    continue
+                used |= cells
+                reqs.append((s, lo, hi, add))
+            ok_dev = pool.grow(reqs)
+            ok_orc = orc.grow(reqs)
+            assert ok_dev == ok_orc
+        elif r < 0.75:
+            s = rng.sample(slots, rng.randrange(1, 4))
+            lo = rng.randrange(0, 2)
+            hi = rng.randrange(lo + 1, 3)
+            pool.release(s, lo, hi)
+            orc.release(s, lo, hi)
+        elif r < 0.87 and dropped < 2:
+            pool.drop_layers(dropped, dropped + 1)
+            orc.drop(1)
+            dropped += 1
+        elif dropped > 0:
+            want = orc.restore(1)
+            if want < 0:
+                with pytest.raises(runtime.Refused):
+                    pool.restore_begin(dropped - 1, dropped)
+            else:
+                assert pool.restore_begin(dropped - 1, dropped) == want
+                pool.restore_complete(dropped - 1, dropped)
+                dropped -= 1
+        assert_same_state(pool, orc, slots)
+    pool.close()
+
+
+def device_gather(pool, slot, layer, ctx, hkv, B):
+    kv = pool.kv_bytes().cpu().numpy()
+    pb = pool.page_bytes
+    rows = pool.block_table(slot, layer)
+    k = np.zeros((ctx, hkv, 128), dtype=np.uint16)
+    v = np.zeros_like(k)
+    for t in range(ctx):
+        base = rows[t // B] * pb
+        for h in range(hkv):
+            off = base + (h * B + t % B) * 256
+            k[t, h] = kv[off:off + 256].view(np.uint16)
+            v[t, h] = kv[off + pb // 2:off + pb // 2 + 256].view(np.uint16)
+    return k, v
+
+
+def rand_bf16(shape, gen, scale=1.0):
+    return (torch.randn(shape, generator=gen) * scale).to(torch.bfloat16)
+
+
+def append(pool, layer, k, v, slot, start):
+    from paper_2412_18169_b200 import runtime
+    n = k.shape[0]
+    slots = torch.full((n,), slot, dtype=torch.int32, device="cuda")
+    pos = torch.arange(start, start + n, dtype=torch.int32, device="cuda")
+    runtime.kv_append(pool, layer, k.cuda(), v.cuda(), slots, pos)
+
+
+def test_append_exchange_compaction_bytes(rt):
+    from paper_2412_18169_b200 import runtime
+    model = TINY.spec()
+    a = rt.create_pool(0, model, model.param_bytes + MIB, TINY)
+    b = rt.create_pool(1, model, model.param_bytes + MIB, TINY)
+    gen = torch.Generator().manual_seed(3)
+    ctx = 300
+    pages = (ctx + 63) // 64
+    # filler request so the request of interest spills into a dropped slab
+    a.drop_layers(1, 2)
+    assert a.grow([(5, 0, 1, 190)])
+    assert a.grow([(2, 0, 1, pages)])
+    k = rand_bf16((ctx, 1, 128), gen)
+    v = rand_bf16((ctx, 1, 128), gen)
+    append(a, 0, k, v, 2, 0)
+    torch.cuda.synchronize()
+    kk, vv = device_gather(a, 2, 0, ctx, 1, 64)
+    assert (kk == k.view(torch.int16).numpy().view(np.uint16)).all()
+    assert (vv == v.view(torch.int16).numpy().view(np.uint16)).all()
+    assert max(a.block_table(2, 0)) >= 192  # lives in the dropped slab's pages
+    # exchange a -> b (two chunks), byte exact
+    assert b.grow([(7, 0, 1, pages)])
+    runtime.copy_pages(b, a, [(2, 7, 0, 1, pages, 0, 2), (2, 7, 0, 1, pages, 2, pages)])
+    torch.cuda.synchronize()
+    kb_, vb_ = device_gather(b, 7, 0, ctx, 1, 64)
+    assert (kb_ == kk).all() and (vb_ == vv).all()
+    # restore on a: the filler leaves, compaction moves request 2's tail pages
+    a.release([5], 0, 1)
+    moved = a.restore_begin(1, 2)
+    assert moved > 0
+    a.restore_complete(1, 2)
+    assert max(a.block_table(2, 0)) < 192
+    kc, vc = device_gather(a, 2, 0, ctx, 1, 64)
+    assert (kc == kk).all() and (vc == vv).all()
+    a.close()
+    b.close()
+
+
+def test_slab_restore_pull_bit_exact(rt):
+    from paper_2412_18169_b200 import runtime
+    model = TINY.spec()
+    a = rt.create_pool(0, model, model.param_bytes + MIB, TINY)
+    b = rt.create_pool(1, model, model.param_bytes + MIB, TINY)
+    wa = a.weight_bytes(1)
+    wa.copy_(torch.randint(0, 256, (model.bytes_per_layer,), dtype=torch.uint8, device="cuda"))
+    b.drop_layers(1, 2)
+    assert b.weight_ptr(1) == 0
+    b.restore_begin(1, 2)
+    half = model.bytes_per_layer // 2
+    runtime.copy_slabs(b, a, 1, 2, 0, half)           # two chunks, like plan_restore_transfers
+    runtime.copy_slabs(b, a, 1, 2, half, model.bytes_per_layer)
+    b.restore_complete(1, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(b.weight_bytes(1), a.weight_bytes(1))
+    # host replica source (exchange.HOST)
+    host = torch.randint(0, 256, (model.bytes_per_layer,), dtype=torch.uint8).pin_memory()
+    b.drop_layers(1, 2)
+    b.restore_begin(1, 2)
+    runtime.copy_slabs_from_host(b, host.data_ptr(), 1, 2, 0, model.bytes_per_layer)
+    torch.cuda.synchronize()
+    assert torch.equal(b.weight_bytes(1).cpu(), host)
+    a.close()
+    b.close()
+
+
+ATTN_SHAPES = [
+    ModelShape("g2", num_layers=2, hidden=256, n_q_heads=2, n_kv_heads=1, head_dim=128,
+               ffn=768, vocab=1024, block_tokens=64),
+    ModelShape("g4", num_layers=2, hidden=4096, n_q_heads=32, n_kv_heads=8, head_dim=128,
+               ffn=1024, vocab=1024, block_tokens=64),
+    ModelShape("g5", num_layers=2, hidden=5120, n_q_heads=40, n_kv_heads=8, head_dim=128,
+               ffn=1024, vocab=1024, block_tokens=64),
+]
+
+
+@pytest.mark.parametrize("shape", ATTN_SHAPES, ids=lambda s: s.name)
+def test_paged_decode_matches_oracle(rt, shape):
+    from paper_2412_18169_b200 import runtime
+    model = shape.spec()
+    pool = rt.create_pool(0, model, model.param_bytes + 64 * MIB, shape)
+    gen = torch.Generator().manual_seed(11)
+    ctxs = [1, 63, 64, 65, 127, 128, 129, 300, 1000, 2047]
+    hkv, hq, B = shape.n_kv_heads, shape.n_q_heads, shape.block_tokens
+    ks, vs = [], []
+    for i, c in enumerate(ctxs):
+        assert pool.grow([(i, 1, 2, (c + B - 1) // B)])
+        k = rand_bf16((c, hkv, 128), gen)
+        v = rand_bf16((c, hkv, 128), gen)
+        append(pool, 1, k, v, i, 0)
+        ks.append(k)
+        vs.append(v)
+    q = rand_bf16((len(ctxs), hq, 128), gen)
+    scale = 128 ** -0.5
+    slots = torch.arange(len(ctxs), dtype=torch.int32, device="cuda")
+    lens = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    out = torch.empty((len(ctxs), hq, 128), dtype=torch.bfloat16, device="cuda")
+    for max_splits in (1, 4, 16):
+        ws = torch.empty(runtime.decode_workspace_bytes(len(ctxs), hq, max_splits),
+                         dtype=torch.uint8, device="cuda")
+        runtime.paged_decode(pool, 1, q.cuda(), slots, lens, max(ctxs), out, ws, scale,
+                             max_splits=max_splits)
+        torch.cuda.synchronize()
+        got = out.float().cpu().numpy()
+        for i, c in enumerate(ctxs):
+            want = decode_ref(q[i].float().numpy(), ks[i].float().numpy(), vs[i].float().numpy(),
+                              scale)
+            want = bf16_to_f32(f32_to_bf16(want))
+            ma, mr = check_close(got[i], want)
+            assert ma <= 2e-2 and mr <= 1e-3, (shape.name, c, max_splits, ma, mr)
+    pool.close()
+
+
+@pytest.mark.parametrize("shape", ATTN_SHAPES[:2], ids=lambda s: s.name)
+def test_paged_prefill_matches_oracle(rt, shape):
+    from paper_2412_18169_b200 import runtime
+    model = shape.spec()
+    pool = rt.create_pool(0, model, model.param_bytes + 64 * MIB, shape)
+    gen = torch.Generator().manual_seed(12)
+    hkv, hq, B = shape.n_kv_heads, shape.n_q_heads, shape.block_tokens
+    # (prefix, chunk) pairs: cold prefill, chunk after a prefix, ragged tails
+    cases = [(0, 1), (0, 100), (0, 128), (0, 300), (64, 64), (200, 77), (1000, 129)]
+    qs, ks, vs, offs = [], [], [], []
+    off = 0
+    for i, (pre, c) in enumerate(cases):
+        n = pre + c
+        assert pool.grow([(i, 0, 1, (n + B - 1) // B)])
+        k = rand_bf16((n, hkv, 128), gen)
+        v = rand_bf16((n, hkv, 128), gen)
+        append(pool, 0, k, v, i, 0)
+        qs.append(rand_bf16((c, hq, 128), gen))
+        ks.append(k)
+        vs.append(v)
+        offs.append(off)
+        off += c
+    q = torch.cat(qs).cuda()
+    out = torch.zeros_like(q)
+    dev = lambda xs: torch.tensor(xs, dtype=torch.int32, device="cuda")  # noqa: E731
+    scale = 128 ** -0.5
+    runtime.paged_prefill(pool, 0, q, dev(list(range(len(cases)))), dev(offs),
+                          dev([c for _, c in cases]), dev([p for p, _ in cases]),
+                          max(c for _, c in cases), out, scale)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for i, (pre, c) in enumerate(cases):
+        want = prefill_ref(qs[i].float().numpy(), ks[i].float().numpy(), vs[i].float().numpy(),
+                           pre, scale)
+        want = bf16_to_f32(f32_to_bf16(want))
+        ma, mr = check_close(got[offs[i]:offs[i] + c], want)
+        assert ma <= 2e-2 and mr <= 1e-3, (shape.name, pre, c, ma, mr)
+    pool.close()
