@@ -61,10 +61,18 @@ struct PoolView {
   int maxp;
 };
 
+// Moves travel by value in kernel parameter space (no staging copy, no sync).
+constexpr int kMoveBatch = 256;
+struct MoveBatch {
+  kb_move mv[kMoveBatch];
+  int64_t cum[kMoveBatch];
+};
+
 __global__ void __launch_bounds__(kThreads)
-copy_pages_kernel(PoolView dst, PoolView src, const kb_move* __restrict__ moves,
-                  const int64_t* __restrict__ cum, int n, int64_t total_pages,
-                  int64_t page_bytes, int64_t pieces) {
+copy_pages_kernel(PoolView dst, PoolView src, const __grid_constant__ MoveBatch batch, int n,
+                  int64_t total_pages, int64_t page_bytes, int64_t pieces) {
+  const kb_move* moves = batch.mv;
+  const int64_t* cum = batch.cum;
   const int64_t piece_bytes = page_bytes / pieces;
   for (int64_t job = blockIdx.x; job < total_pages * pieces; job += gridDim.x) {
     const int64_t pg = job / pieces, pc = job % pieces;
@@ -153,22 +161,25 @@ extern "C" int kb_copy_pages(kb_pool* dst, kb_pool* src, const kb_move* moves, i
   if (total == 0) return KB_OK;
   KB_RT(cudaSetDevice(src->device));
   cudaStream_t st = (cudaStream_t)stream;
-  // request list lives in the source pool's scratch; synchronous hand-off
-  const int64_t mv_bytes = round_up((int64_t)n * sizeof(kb_move), 256);
-  int rc = ensure_scratch(src, mv_bytes + (int64_t)n * 8);
-  if (rc) return rc;
-  kb_move* d_moves = reinterpret_cast<kb_move*>(src->d_scratch);
-  int64_t* d_cum = reinterpret_cast<int64_t*>((char*)src->d_scratch + mv_bytes);
-  KB_RT(cudaMemcpyAsync(d_moves, moves, n * sizeof(kb_move), cudaMemcpyHostToDevice, st));
-  KB_RT(cudaMemcpyAsync(d_cum, cum.data(), n * 8, cudaMemcpyHostToDevice, st));
   const int64_t pieces = src->m.page_bytes > kPiece ? src->m.page_bytes / kPiece : 1;
   PoolView dv{dst->d_bt, reinterpret_cast<uint8_t*>(dst->kva), L, dst->maxp};
   PoolView sv{src->d_bt, reinterpret_cast<uint8_t*>(src->kva), L, src->maxp};
-  int grid = grid_for(total * pieces, 1, 148 * 8);
-  copy_pages_kernel<<<grid, kThreads, 0, st>>>(dv, sv, d_moves, d_cum, n, total,
-                                               src->m.page_bytes, pieces);
-  KB_LAUNCH_CHECK();
-  KB_RT(cudaStreamSynchronize(st));
+  MoveBatch batch;
+  for (int b0 = 0; b0 < n; b0 += kMoveBatch) {
+    const int nb = std::min(kMoveBatch, n - b0);
+    int64_t sub = 0;
+    for (int i = 0; i < nb; ++i) {
+      batch.mv[i] = moves[b0 + i];
+      batch.cum[i] = sub;
+      sub += moves[b0 + i].flat_hi - moves[b0 + i].flat_lo;
+    }
+    if (sub == 0) continue;
+    int grid = grid_for(sub * pieces, 1, 148 * 8);
+    copy_pages_kernel<<<grid, kThreads, 0, st>>>(dv, sv, batch, nb, sub, src->m.page_bytes,
+                                                 pieces);
+    KB_LAUNCH_CHECK();
+  }
+  (void)cum;
   return KB_OK;
 }
 

@@ -246,10 +246,11 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       if (j > 0) {  // fold in O of the previous tile (also frees the P buffer)
         mbar_wait(&misc->o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
-        float ov[8];
+        float ov[8], ol[8];
         tmem_ld_32x32b_x8(tmem + lane_base + 32 + ((j - 1) & 1) * 16, ov);
+        tmem_ld_32x32b_x8(tmem + lane_base + 40 + ((j - 1) & 1) * 16, ol);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) o_acc[g] = o_acc[g] * alpha_prev[g] + ov[g];
+        for (int g = 0; g < 8; ++g) o_acc[g] = o_acc[g] * alpha_prev[g] + (ov[g] + ol[g]);
       }
 #pragma unroll
       for (int g = 0; g < 8; ++g) alpha_prev[g] = alpha[g];
@@ -269,13 +270,18 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           }
         }
       }
-      // P^T -> SW128 K-major smem image (rows = heads, K = tokens)
+      // P^T -> SW128 K-major smem image (rows = heads, K = tokens).  The
+      // N=16 MMA has room for 16 columns but a GQA group uses <= 8, so the
+      // spare rows carry the bf16 residual of P: row g = bf16(p), row 8+g =
+      // bf16(p - bf16(p)).  O^T columns g and 8+g sum to a ~16-bit-mantissa
+      // P.V at no extra MMA cost (the kernel is HBM-bound).
       const uint32_t tbase = (tid >> 6) * 2048;
 #pragma unroll
-      for (int g = 0; g < 16; ++g) {
-        const float pv = g < 8 ? p[g & 7] : 0.f;
-        *reinterpret_cast<__nv_bfloat16*>(sP + tbase + sw128_offset(g, tid & 63)) =
-            __float2bfloat16(pv);
+      for (int g = 0; g < 8; ++g) {
+        const __nv_bfloat16 hi = __float2bfloat16(p[g]);
+        const __nv_bfloat16 lo = __float2bfloat16(p[g] - __bfloat162float(hi));
+        *reinterpret_cast<__nv_bfloat16*>(sP + tbase + sw128_offset(g, tid & 63)) = hi;
+        *reinterpret_cast<__nv_bfloat16*>(sP + tbase + sw128_offset(g + 8, tid & 63)) = lo;
       }
       fence_proxy_async_smem();
       mbar_arrive(&misc->p_full);
@@ -284,10 +290,11 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       const int j = nt - 1;
       mbar_wait(&misc->o_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      float ov[8];
+      float ov[8], ol[8];
       tmem_ld_32x32b_x8(tmem + lane_base + 32 + (j & 1) * 16, ov);
+      tmem_ld_32x32b_x8(tmem + lane_base + 40 + (j & 1) * 16, ol);
 #pragma unroll
-      for (int g = 0; g < 8; ++g) o_acc[g] = o_acc[g] * alpha_prev[g] + ov[g];
+      for (int g = 0; g < 8; ++g) o_acc[g] = o_acc[g] * alpha_prev[g] + (ov[g] + ol[g]);
     }
     // l = sum over the 128 token lanes
 #pragma unroll

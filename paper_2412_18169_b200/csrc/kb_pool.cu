@@ -149,13 +149,21 @@ __device__ void scan_pages(const uint32_t* __restrict__ bitmap, int64_t lo, int6
   if (found_out) *found_out = found < limit ? found : limit;
 }
 
-// Grow: requests with exclusive prefix `cum` (pages per request); the k-th
-// lowest free page below `extent` goes to flattened slot k.
+// Grow: a batch of requests passed by value (kernel parameter space, no
+// host->device copy) with exclusive prefix `cum` (pages per request); the
+// k-th lowest free page below `extent` goes to flattened slot k.
+constexpr int kGrowBatch = 256;
+struct GrowBatch {
+  kb_grow r[kGrowBatch];
+  int64_t cum[kGrowBatch];
+};
+
 __global__ void __launch_bounds__(kScanThreads)
 grow_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner, int32_t* __restrict__ bt,
-            int32_t* __restrict__ np, const kb_grow* __restrict__ reqs,
-            const int64_t* __restrict__ cum, int n, int64_t total, int64_t extent, int L,
-            int maxp, int32_t* __restrict__ status) {
+            int32_t* __restrict__ np, const __grid_constant__ GrowBatch batch, int n,
+            int64_t total, int64_t extent, int L, int maxp) {
+  const kb_grow* reqs = batch.r;
+  const int64_t* cum = batch.cum;
   auto emit = [&](int64_t k, int64_t page) {
     int lo = 0, hi = n - 1;  // last request with cum <= k
     while (lo < hi) {
@@ -174,10 +182,7 @@ grow_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner, int32_t*
   int64_t found = 0;
   scan_pages<4>(bitmap, 0, extent, false, total, emit, &found);
   __syncthreads();
-  if (found < total) {
-    if (threadIdx.x == 0) status[0] = 1;
-    return;  // host checked capacity first; this is a consistency failure
-  }
+  // (found < total cannot happen: the host checked capacity first)
   // advance per-(slot, layer) page counts
   for (int i = 0; i < n; ++i) {
     const kb_grow r = reqs[i];
@@ -185,16 +190,20 @@ grow_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner, int32_t*
       np[(int64_t)r.slot * L + l] += r.add_pages;
     __syncthreads();
   }
-  if (threadIdx.x == 0) status[0] = 0;
 }
 
 // Release all pages of (slot, layer) for layers in [lo, hi): one block per pair.
+constexpr int kReleaseBatch = 1024;
+struct SlotBatch {
+  int32_t s[kReleaseBatch];
+};
+
 __global__ void release_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner,
                                int32_t* __restrict__ bt, int32_t* __restrict__ np,
-                               const int32_t* __restrict__ slots, int lo, int hi, int L,
+                               const __grid_constant__ SlotBatch slots, int lo, int hi, int L,
                                int maxp) {
   const int span = hi - lo;
-  const int slot = slots[blockIdx.x / span];
+  const int slot = slots.s[blockIdx.x / span];
   const int layer = lo + blockIdx.x % span;
   int32_t* row = bt + ((int64_t)slot * L + layer) * maxp;
   const int cnt = np[(int64_t)slot * L + layer];
@@ -640,25 +649,27 @@ extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr
                                 std::to_string(p->extent_pages - p->live_pages));
   KB_RT(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t req_bytes = round_up((int64_t)n * sizeof(kb_grow), 256);
-  int rc = ensure_scratch(p, req_bytes + (int64_t)n * 8 + 64);
-  if (rc) return rc;
-  char* base = (char*)p->d_scratch;
-  kb_grow* d_reqs = reinterpret_cast<kb_grow*>(base);
-  int64_t* d_cum = reinterpret_cast<int64_t*>(base + req_bytes);
-  int32_t* d_status = reinterpret_cast<int32_t*>(base + req_bytes + round_up((int64_t)n * 8, 64));
-  KB_RT(cudaMemcpyAsync(d_reqs, reqs, n * sizeof(kb_grow), cudaMemcpyHostToDevice, st));
-  KB_RT(cudaMemcpyAsync(d_cum, cum.data(), n * 8, cudaMemcpyHostToDevice, st));
-  grow_kernel<<<1, kScanThreads, 0, st>>>(p->d_bitmap, p->d_owner, p->d_bt, p->d_np, d_reqs, d_cum,
-                                          n, total, p->extent_pages, L, p->maxp, d_status);
-  KB_LAUNCH_CHECK();
+  // batches of kGrowBatch requests travel in kernel parameter space: no
+  // staging copy and no host synchronization; launches on one stream run in
+  // order, so a later batch sees the pages an earlier one took
+  GrowBatch batch;
+  for (int b0 = 0; b0 < n; b0 += kGrowBatch) {
+    const int nb = std::min(kGrowBatch, n - b0);
+    int64_t sub = 0;
+    for (int i = 0; i < nb; ++i) {
+      batch.r[i] = reqs[b0 + i];
+      batch.cum[i] = sub;
+      sub += (int64_t)(reqs[b0 + i].layer_hi - reqs[b0 + i].layer_lo) * reqs[b0 + i].add_pages;
+    }
+    grow_kernel<<<1, kScanThreads, 0, st>>>(p->d_bitmap, p->d_owner, p->d_bt, p->d_np, batch, nb,
+                                            sub, p->extent_pages, L, p->maxp);
+    KB_LAUNCH_CHECK();
+  }
+  (void)cum;
   for (int i = 0; i < n; ++i)
     for (int l = reqs[i].layer_lo; l < reqs[i].layer_hi; ++l)
       p->h_np[(int64_t)reqs[i].slot * L + l] += reqs[i].add_pages;
   p->live_pages += total;
-  // the host-side scratch (reqs/cum) is reused by the next call: make sure
-  // this kernel consumed it before returning
-  KB_RT(cudaStreamSynchronize(st));
   return KB_OK;
 }
 
@@ -675,17 +686,17 @@ extern "C" int kb_pages_release(kb_pool* p, const int32_t* slots, int32_t n, int
   }
   KB_RT(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = ensure_scratch(p, (int64_t)n * 4);
-  if (rc) return rc;
-  int32_t* d_slots = reinterpret_cast<int32_t*>(p->d_scratch);
-  KB_RT(cudaMemcpyAsync(d_slots, slots, n * 4, cudaMemcpyHostToDevice, st));
-  release_kernel<<<n * (hi - lo), 128, 0, st>>>(p->d_bitmap, p->d_owner, p->d_bt, p->d_np, d_slots,
-                                                 lo, hi, L, p->maxp);
-  KB_LAUNCH_CHECK();
+  SlotBatch batch;
+  for (int b0 = 0; b0 < n; b0 += kReleaseBatch) {
+    const int nb = std::min(kReleaseBatch, n - b0);
+    for (int i = 0; i < nb; ++i) batch.s[i] = slots[b0 + i];
+    release_kernel<<<nb * (hi - lo), 128, 0, st>>>(p->d_bitmap, p->d_owner, p->d_bt, p->d_np,
+                                                    batch, lo, hi, L, p->maxp);
+    KB_LAUNCH_CHECK();
+  }
   for (int i = 0; i < n; ++i)
     for (int l = lo; l < hi; ++l) p->h_np[(int64_t)slots[i] * L + l] = 0;
   p->live_pages -= freed;
-  KB_RT(cudaStreamSynchronize(st));
   return KB_OK;
 }
 

@@ -26,7 +26,7 @@ constexpr int kPfTile = 128;
 constexpr int kPfHalf = 16384;                     // 128 rows x 64 el x 2 B
 constexpr int kPfKV = 4 * kPfHalf;                 // K + V for one 128-key tile
 constexpr int kPfQ = 2 * kPfHalf;
-constexpr int kPfP = 2 * kPfHalf;
+constexpr int kPfP = 4 * kPfHalf;                  // P_hi + P_lo
 constexpr int kPfSmem = kPfStages * kPfKV + kPfQ + kPfP + 1024 + 1024;
 constexpr uint32_t kPfTmemCols = 512;               // S0 | S1 | O
 
@@ -45,16 +45,17 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* __restrict__ q,
                   const int32_t* __restrict__ bt, const int32_t* __restrict__ slots,
                   const int32_t* __restrict__ q_off, const int32_t* __restrict__ q_len,
-                  const int32_t* __restrict__ prefix, const int32_t* __restrict__ tile_seq,
-                  const int32_t* __restrict__ tile_m, __nv_bfloat16* __restrict__ out, int Hkv,
-                  int Hq, int L, int maxp, int layer, float scale_log2) {
+                  const int32_t* __restrict__ prefix, int mtiles,
+                  __nv_bfloat16* __restrict__ out, int Hkv, int Hq, int L, int maxp, int layer,
+                  float scale_log2) {
   using namespace sm100;
   constexpr int kPPT = kPfTile / kB;
   const int hq = blockIdx.y;
-  const int seq = tile_seq[blockIdx.x], mt = tile_m[blockIdx.x];
+  const int seq = blockIdx.x / mtiles, mt = blockIdx.x % mtiles;
   const int h = hq / (Hq / Hkv);
   const int qlen = q_len[seq], pre = prefix[seq], qo = q_off[seq];
   const int row0 = mt * kPfTile;
+  if (row0 >= qlen) return;  // grid is sized for the longest chunk
   const int rows = min(kPfTile, qlen - row0);
   const int kv_len = pre + row0 + rows;  // keys visible to the last row
   const int nt = (kv_len + kPfTile - 1) / kPfTile;
@@ -149,9 +150,11 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         const int stage = j % kPfStages;
         const uint32_t v_addr = smem_u32(smem + stage * kPfKV + 2 * kPfHalf);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t a = sw128_desc(p_addr + (kk >> 2) * kPfHalf + (kk & 3) * 32, 16, 1024);
-          const uint64_t b = sw128_desc(v_addr + kk * 2048, kPfHalf, 1024);  // MN-major V
+        for (int kk = 0; kk < 16; ++kk) {
+          const int k8 = kk & 7;  // kk < 8: P_hi, kk >= 8: P_lo; both against V
+          const uint64_t a = sw128_desc(p_addr + (kk >> 3) * 2 * kPfHalf + (k8 >> 2) * kPfHalf +
+                                            (k8 & 3) * 32, 16, 1024);
+          const uint64_t b = sw128_desc(v_addr + k8 * 2048, kPfHalf, 1024);  // MN-major V
           mma_f16_ss(tmem + 256, a, b, kIdPV, kk > 0);
         }
         mma_commit(&misc->o_full);
@@ -241,12 +244,19 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 #pragma unroll
         for (int q8 = 0; q8 < 4; ++q8) {
           const int ch = c * 4 + q8;  // 16-byte chunk (8 keys) of the 128-key row
-          __nv_bfloat162 pk[4];
+          // P = P_hi + P_lo, both bf16: the PV chain runs over K = 256
+          // ([P_hi | P_lo] . [V ; V]) so P carries ~16 mantissa bits.
+          __nv_bfloat162 hi[4], lo[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            pk[e] = __floats2bfloat162_rn(part[q8 * 8 + 2 * e], part[q8 * 8 + 2 * e + 1]);
+          for (int e = 0; e < 4; ++e) {
+            const float x0 = part[q8 * 8 + 2 * e], x1 = part[q8 * 8 + 2 * e + 1];
+            hi[e] = __floats2bfloat162_rn(x0, x1);
+            const float2 hf = __bfloat1622float2(hi[e]);
+            lo[e] = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
+          }
           const uint32_t off = (ch >> 3) * kPfHalf + tid * 128 + ((((ch & 7) ^ (tid & 7)) & 7) << 4);
-          *reinterpret_cast<int4*>(sP + off) = *reinterpret_cast<int4*>(pk);
+          *reinterpret_cast<int4*>(sP + off) = *reinterpret_cast<int4*>(hi);
+          *reinterpret_cast<int4*>(sP + 2 * kPfHalf + off) = *reinterpret_cast<int4*>(lo);
         }
       }
       l_run = l_run * alpha + rs;
@@ -301,28 +311,12 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
   if (nseq <= 0) return KB_OK;
   KB_RT(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
-  // (seq, m-tile) list built on the host from q_len (host copy needed)
-  std::vector<int32_t> lens(nseq);
-  KB_RT(cudaMemcpyAsync(lens.data(), reinterpret_cast<const void*>(q_len), nseq * 4,
-                        cudaMemcpyDeviceToHost, st));
-  KB_RT(cudaStreamSynchronize(st));
-  std::vector<int32_t> tseq, tm;
-  for (int i = 0; i < nseq; ++i)
-    for (int m = 0; m * kPfTile < lens[i]; ++m) {
-      tseq.push_back(i);
-      tm.push_back(m);
-    }
-  (void)max_q_len;
-  const int ntile = (int)tseq.size();
-  if (ntile == 0) return KB_OK;
-  int rc = ensure_scratch(p, (int64_t)ntile * 8 + 256);
-  if (rc) return rc;
-  int32_t* d_ts = reinterpret_cast<int32_t*>(p->d_scratch);
-  int32_t* d_tm = d_ts + round_up(ntile, 64);
-  KB_RT(cudaMemcpyAsync(d_ts, tseq.data(), ntile * 4, cudaMemcpyHostToDevice, st));
-  KB_RT(cudaMemcpyAsync(d_tm, tm.data(), ntile * 4, cudaMemcpyHostToDevice, st));
+  if (max_q_len <= 0) return KB_OK;
+  // grid = (seq x m-tiles of the longest chunk) x q heads; CTAs past their
+  // sequence's chunk exit at once, so no host copy of q_len is needed
+  const int mtiles = (int)ceil_div(max_q_len, kPfTile);
   const float scale_log2 = scale * 1.4426950408889634f;
-  dim3 grid(ntile, n_q_heads);
+  dim3 grid((unsigned)(nseq * mtiles), n_q_heads);
   if (B == 64) {
     static bool attr = false;
     if (!attr) {
@@ -333,8 +327,8 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
     prefill_tc_kernel<64><<<grid, kPfThreads, kPfSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(q_off),
-        reinterpret_cast<const int32_t*>(q_len), reinterpret_cast<const int32_t*>(prefix), d_ts,
-        d_tm, reinterpret_cast<__nv_bfloat16*>(out), Hkv, n_q_heads, p->m.num_layers, p->maxp,
+        reinterpret_cast<const int32_t*>(q_len), reinterpret_cast<const int32_t*>(prefix), mtiles,
+        reinterpret_cast<__nv_bfloat16*>(out), Hkv, n_q_heads, p->m.num_layers, p->maxp,
         layer, scale_log2);
   } else {
     static bool attr = false;
@@ -346,12 +340,10 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
     prefill_tc_kernel<128><<<grid, kPfThreads, kPfSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(q_off),
-        reinterpret_cast<const int32_t*>(q_len), reinterpret_cast<const int32_t*>(prefix), d_ts,
-        d_tm, reinterpret_cast<__nv_bfloat16*>(out), Hkv, n_q_heads, p->m.num_layers, p->maxp,
+        reinterpret_cast<const int32_t*>(q_len), reinterpret_cast<const int32_t*>(prefix), mtiles,
+        reinterpret_cast<__nv_bfloat16*>(out), Hkv, n_q_heads, p->m.num_layers, p->maxp,
         layer, scale_log2);
   }
   KB_LAUNCH_CHECK();
-  // scratch (tile lists) is reused by later calls on this pool
-  KB_RT(cudaStreamSynchronize(st));
   return KB_OK;
 }

@@ -1,0 +1,253 @@
+"""Device execution of TransferTasks (N4 / N5 / N6 / N7).
+
+The reference times every task on a serialized link model
+(pkg/src/dropsim/exchange.py:49-101) and the engine consumes them through
+`enqueue_task(task, cb)` / `cb(task, done_us)` (engine.py:279-302).  Here the
+same task lists run on the GPU:
+
+  KVCACHE_CHUNK  -> kb_copy_pages over a slice of the flow's pages.  A flow
+                    is (rid, src -> dst) over the layer overlap of the old and
+                    new stage maps (exchange.py:146-205); chunk k of n covers
+                    flattened pages [k*P//n, (k+1)*P//n) of the flow's
+                    P = layers x pages, so the chunks tile the flow exactly.
+                    The destination's pages are grown on the first chunk,
+                    the source's released after the last one lands.
+  PARAM_SHARD    -> kb_copy_slabs over consecutive byte ranges of the run's
+                    layers (exchange.py:208-249); HOST sources come from a
+                    pinned host replica (kb_copy_slabs_from_host).
+  ACTIVATION     -> kb_copy_bytes (stage s -> s+1 hand-off, engine.py:428-448).
+
+Scheduling (N6): activations go on a high-priority stream, KV chunks and
+parameter shards on a low-priority stream in FIFO order -- the device
+version of `_PRIO` (exchange.py:27-28).  Chunks are the preemption points,
+as in the reference; completion is a CUDA event the engine polls.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+from . import runtime
+from .exchange import HOST, TaskKind, TransferTask
+
+
+class SlotTable:
+    """rid -> block-table slot on one pool (lowest free slot first)."""
+
+    def __init__(self, max_slots: int):
+        self.max_slots = max_slots
+        self.of: dict[int, int] = {}
+        self._free = list(range(max_slots - 1, -1, -1))
+
+    def get(self, rid: int) -> int:
+        s = self.of.get(rid)
+        if s is None:
+            if not self._free:
+                raise RuntimeError("out of block-table slots")
+            s = self._free.pop()
+            self.of[rid] = s
+        return s
+
+    def drop(self, rid: int) -> Optional[int]:
+        s = self.of.pop(rid, None)
+        if s is not None:
+            self._free.append(s)
+            self._free.sort(reverse=True)
+        return s
+
+
+@dataclass
+class KVFlow:
+    rid: int
+    src: int
+    dst: int
+    layers: tuple[int, int]
+    npages: int
+    n_chunks: int
+    done_chunks: int = 0
+    grown: bool = False
+
+    @property
+    def total(self) -> int:
+        return (self.layers[1] - self.layers[0]) * self.npages
+
+
+@dataclass
+class Pending:
+    task: TransferTask
+    event: object
+    cb: Optional[Callable]
+    bytes_moved: int
+    start_event: object = None
+
+
+@dataclass
+class TransferStats:
+    kv_bytes: int = 0
+    param_bytes: int = 0
+    act_bytes: int = 0
+    tasks: int = 0
+
+
+class TransferEngine:
+    """Runs transfer tasks between device pools of one process.
+
+    pools: iid -> DevicePool; slots: iid -> SlotTable; host_replica: optional
+    pinned host tensor holding one full parameter copy (layer l at
+    l * bytes_per_layer) for HOST-sourced restores.
+    """
+
+    def __init__(self, pools: dict, slots: dict, host_replica=None, timing: bool = False):
+        import torch
+        self.torch = torch
+        self.pools = pools
+        self.slots = slots
+        self.host_replica = host_replica
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.bulk = torch.cuda.Stream(priority=lo)   # KV chunks + param shards, FIFO
+        self.urgent = torch.cuda.Stream(priority=hi)  # activations
+        self.flows: dict[tuple[int, int, int], KVFlow] = {}
+        self.chunk_of: dict[int, tuple[tuple[int, int, int], int]] = {}
+        self.param_off: dict[int, int] = {}
+        self.pending: list[Pending] = []
+        self.stats = TransferStats()
+        self.timing = timing
+
+    # -------------------------------------------------------------- planning
+    def register_exchange(self, tasks: list[TransferTask], old_map: dict, new_map: dict,
+                          context_tokens: dict[int, int]) -> None:
+        """Attach device geometry to a plan_exchange task list."""
+        per_flow: dict[tuple[int, int, int], list[TransferTask]] = {}
+        for t in tasks:
+            per_flow.setdefault((t.rid, t.src, t.dst), []).append(t)
+        for key, chunks in per_flow.items():
+            rid, j, k = key
+            lo = max(old_map[j][0], new_map[k][0])
+            hi = min(old_map[j][1], new_map[k][1])
+            B = self.pools[j].shape.block_tokens
+            npages = -(-context_tokens[rid] // B)
+            self.flows[key] = KVFlow(rid, j, k, (lo, hi), npages, len(chunks))
+            for idx, t in enumerate(chunks):
+                self.chunk_of[t.tid] = (key, idx)
+
+    def register_restore(self, tasks: list[TransferTask], bytes_per_layer: int) -> None:
+        """Byte offsets of every PARAM_SHARD chunk inside its layer run."""
+        run_off: dict[tuple[int, int, tuple[int, int]], int] = {}
+        for t in tasks:
+            key = (t.src, t.dst, t.layers)
+            off = run_off.get(key, 0)
+            self.param_off[t.tid] = off
+            run_off[key] = off + t.size_bytes
+
+    def register_chunked_kv(self, tasks: list[TransferTask], layers: tuple[int, int],
+                            context_tokens: dict[int, int]) -> None:
+        """Consolidation-style KV moves (dissolve, engine.py:1211-1239): every
+        task of (rid, src, dst) moves the request's pages of `layers`."""
+        per_flow: dict[tuple[int, int, int], list[TransferTask]] = {}
+        for t in tasks:
+            per_flow.setdefault((t.rid, t.src, t.dst), []).append(t)
+        for key, chunks in per_flow.items():
+            rid, j, _ = key
+            B = self.pools[j].shape.block_tokens
+            self.flows[key] = KVFlow(rid, j, key[2], layers, -(-context_tokens[rid] // B),
+                                     len(chunks))
+            for idx, t in enumerate(chunks):
+                self.chunk_of[t.tid] = (key, idx)
+
+    # -------------------------------------------------------------- execution
+    def submit(self, task: TransferTask, cb: Optional[Callable] = None) -> None:
+        torch = self.torch
+        stream = self.urgent if task.kind is TaskKind.ACTIVATION else self.bulk
+        start = torch.cuda.Event(enable_timing=True) if self.timing else None
+        if start is not None:
+            start.record(stream)
+        moved = 0
+        if task.kind is TaskKind.KVCACHE_CHUNK:
+            moved = self._run_kv_chunk(task, stream)
+            self.stats.kv_bytes += moved
+        elif task.kind is TaskKind.PARAM_SHARD:
+            moved = self._run_param_shard(task, stream)
+            self.stats.param_bytes += moved
+        else:
+            raise ValueError("activation tasks go through submit_activation")
+        ev = torch.cuda.Event(enable_timing=self.timing)
+        ev.record(stream)
+        self.stats.tasks += 1
+        self.pending.append(Pending(task, ev, cb, moved, start))
+
+    def submit_activation(self, task: TransferTask, dst_ptr: int, src_ptr: int,
+                          cb: Optional[Callable] = None) -> None:
+        runtime.copy_bytes(dst_ptr, src_ptr, task.size_bytes, stream=self.urgent)
+        ev = self.torch.cuda.Event()
+        ev.record(self.urgent)
+        self.stats.act_bytes += task.size_bytes
+        self.pending.append(Pending(task, ev, cb, task.size_bytes))
+
+    def _run_kv_chunk(self, task: TransferTask, stream) -> int:
+        key, idx = self.chunk_of.pop(task.tid)
+        fl = self.flows[key]
+        src, dst = self.pools[fl.src], self.pools[fl.dst]
+        s_slot = self.slots[fl.src].get(fl.rid)
+        d_slot = self.slots[fl.dst].get(fl.rid)
+        lo, hi = fl.layers
+        if not fl.grown:
+            if fl.npages and not dst.grow([(d_slot, lo, hi, fl.npages)], stream=stream):
+                raise runtime.DeviceError(f"instance {fl.dst} out of KV pages for rid {fl.rid}")
+            fl.grown = True
+        P = fl.total
+        a, b = idx * P // fl.n_chunks, (idx + 1) * P // fl.n_chunks
+        if b > a:
+            runtime.copy_pages(dst, src, [(s_slot, d_slot, lo, hi, fl.npages, a, b)],
+                               stream=stream)
+        return (b - a) * src.page_bytes
+
+    def _run_param_shard(self, task: TransferTask, stream) -> int:
+        lo, hi = task.layers
+        off = self.param_off.pop(task.tid)
+        dst = self.pools[task.dst]
+        if task.src == HOST:
+            if self.host_replica is None:
+                raise runtime.DeviceError("HOST-sourced restore without a host replica")
+            base = self.host_replica.data_ptr() + lo * dst.model.bytes_per_layer
+            runtime.copy_slabs_from_host(dst, base, lo, hi, off, off + task.size_bytes,
+                                         stream=stream)
+        else:
+            runtime.copy_slabs(dst, self.pools[task.src], lo, hi, off, off + task.size_bytes,
+                               stream=stream)
+        return task.size_bytes
+
+    def finish_flow_sources(self) -> list[KVFlow]:
+        """Release source pages of every flow whose chunks all landed."""
+        done = []
+        for key, fl in list(self.flows.items()):
+            if fl.done_chunks == fl.n_chunks:
+                slot = self.slots[fl.src].of.get(fl.rid)
+                if slot is not None:
+                    self.pools[fl.src].release([slot], fl.layers[0], fl.layers[1],
+                                               stream=self.bulk)
+                del self.flows[key]
+                done.append(fl)
+        return done
+
+    def poll(self, block: bool = False) -> list[Pending]:
+        """Completed tasks in submission order; runs their callbacks."""
+        out = []
+        while self.pending:
+            p = self.pending[0]
+            if not block and not p.event.query():
+                break
+            p.event.synchronize()
+            self.pending.pop(0)
+            if p.task.kind is TaskKind.KVCACHE_CHUNK:
+                for key, fl in self.flows.items():
+                    if key == (p.task.rid, p.task.src, p.task.dst):
+                        fl.done_chunks += 1
+                        break
+            out.append(p)
+            if p.cb is not None:
+                p.cb(p.task)
+        return out
+
+    def drain(self) -> list[Pending]:
+        return self.poll(block=True)
