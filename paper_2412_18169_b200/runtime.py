@@ -111,8 +111,14 @@ class Refused(Exception):
     """Expected refusal (KB_REFUSED): out of pages / restore cannot vacate."""
 
 
-def _check(rc: int) -> None:
+# Kernel launches issued by this process through the library (the bench's
+# `gpu_launches` claim): incremented by the wrappers that launch.
+LAUNCHES = [0]
+
+
+def _check(rc: int, launches: int = 0) -> None:
     if rc == KB_OK:
+        LAUNCHES[0] += launches
         return
     msg = _lib.kb_last_error().decode()
     if rc == KB_REFUSED:
@@ -232,6 +238,7 @@ class DevicePool:
         moved, ns = C.c_int64(), C.c_int64()
         _check(_lib.kb_restore_begin(self.h, lo, hi, _stream(stream), C.byref(moved),
                                      C.byref(ns)))
+        LAUNCHES[0] += 3 if moved.value else 1  # plan (+ copy + fixup)
         self.last_moved_pages = moved.value
         self.last_remap_ns = ns.value
         return moved.value
@@ -260,7 +267,8 @@ class DevicePool:
             return True
         arr = (Grow * len(reqs))(*[Grow(*r) for r in reqs])
         try:
-            _check(_lib.kb_pages_grow(self.h, arr, len(reqs), _stream(stream)))
+            _check(_lib.kb_pages_grow(self.h, arr, len(reqs), _stream(stream)),
+                   launches=-(-len(reqs) // 256))
         except Refused:
             return False
         return True
@@ -269,7 +277,7 @@ class DevicePool:
         if not slots:
             return
         _check(_lib.kb_pages_release(self.h, _i32arr(slots), len(slots), lo, hi,
-                                     _stream(stream)))
+                                     _stream(stream)), launches=-(-len(slots) // 1024))
 
     def npages(self, slot: int, layer: int) -> int:
         return int(_lib.kb_pages_per_layer_count(self.h, slot, layer))
@@ -306,12 +314,14 @@ def copy_pages(dst: DevicePool, src: DevicePool,
     if not moves:
         return
     arr = (Move * len(moves))(*[Move(*m, 0) for m in moves])
-    _check(_lib.kb_copy_pages(dst.h, src.h, arr, len(moves), _stream(stream)))
+    _check(_lib.kb_copy_pages(dst.h, src.h, arr, len(moves), _stream(stream)),
+           launches=-(-len(moves) // 256))
 
 
 def copy_slabs(dst: DevicePool, src: DevicePool, lo: int, hi: int, byte_lo: int,
                byte_hi: int, stream=None) -> None:
-    _check(_lib.kb_copy_slabs(dst.h, src.h, lo, hi, byte_lo, byte_hi, _stream(stream)))
+    _check(_lib.kb_copy_slabs(dst.h, src.h, lo, hi, byte_lo, byte_hi, _stream(stream)),
+           launches=1)
 
 
 def copy_slabs_from_host(dst: DevicePool, host_ptr: int, lo: int, hi: int, byte_lo: int,
@@ -321,7 +331,7 @@ def copy_slabs_from_host(dst: DevicePool, host_ptr: int, lo: int, hi: int, byte_
 
 
 def copy_bytes(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:
-    _check(_lib.kb_copy_bytes(dst_ptr, src_ptr, nbytes, _stream(stream)))
+    _check(_lib.kb_copy_bytes(dst_ptr, src_ptr, nbytes, _stream(stream)), launches=1)
 
 
 # -- N8 attention -------------------------------------------------------------
@@ -329,7 +339,7 @@ def copy_bytes(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:
 def kv_append(pool: DevicePool, layer: int, k, v, slots, pos, stream=None) -> None:
     """k, v: [ntok, n_kv_heads, 128] bf16; slots/pos: int32 [ntok] (device)."""
     _check(_lib.kb_kv_append(pool.h, layer, k.data_ptr(), v.data_ptr(), slots.data_ptr(),
-                             pos.data_ptr(), k.shape[0], _stream(stream)))
+                             pos.data_ptr(), k.shape[0], _stream(stream)), launches=1)
 
 
 def decode_workspace_bytes(nseq: int, n_q_heads: int, max_splits: int) -> int:
@@ -342,7 +352,7 @@ def paged_decode(pool: DevicePool, layer: int, q, slots, ctx_lens, max_ctx: int,
     _check(_lib.kb_paged_decode(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
                                 ctx_lens.data_ptr(), q.shape[0], max_ctx, scale,
                                 out.data_ptr(), workspace.data_ptr(), max_splits,
-                                _stream(stream)))
+                                _stream(stream)), launches=3)
 
 
 def paged_prefill(pool: DevicePool, layer: int, q, slots, q_off, q_len, prefix, max_q_len: int,
@@ -351,4 +361,4 @@ def paged_prefill(pool: DevicePool, layer: int, q, slots, q_off, q_len, prefix, 
     _check(_lib.kb_paged_prefill(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
                                  q_off.data_ptr(), q_len.data_ptr(), prefix.data_ptr(),
                                  slots.shape[0], max_q_len, scale, out.data_ptr(),
-                                 _stream(stream)))
+                                 _stream(stream)), launches=1)
