@@ -9,27 +9,28 @@ token-granular and position-free: its KVAllocator counts tokens against
 `kvcache_virtual_extent`, `drop_layers` grows the extent by whole layer
 blocks (memory.py:147-172) and `restore_layers` reserves bytes before the
 extent shrinks (memory.py:175-197, 116-124).  The device adds pages and
-block tables underneath; this module restates that device layer with the
-same deterministic rules as csrc/kb_pool.cu, so block tables, owners and
-moved bytes can be compared bit for bit:
-  * grow: the K lowest free page ids below the extent, assigned in request
-    order, then layer order, then page order;
+block tables underneath (csrc/kb_pool.cu); this module restates that device
+layer with the same deterministic rules, so block tables, owners and moved
+bytes can be compared bit for bit:
+  * page space: [head pages | slab of layer 0 | ... | slab of layer L-1];
+    a held layer's slab pages are reserved (they hold its weights);
+  * drop(lo, hi): the slab pages of layers [lo, hi) become free KV pages;
+  * grow: the K lowest free page ids, assigned in request order, then layer
+    order, then page order;
   * release: every page of (slot, layer in [lo, hi)) goes back to the pool;
-  * drop: the KV extent grows by one slab (slab_bytes / page_bytes pages)
-    per dropped layer, appended at the tail (the tail-mapping described at
-    PAPER.md:1240-1270, "mapping the tail of the KVCache memory");
-  * restore: live pages in the vacated tail move, in ascending order, to the
-    lowest free pages below the new extent (compaction), then the extent
-    shrinks by one slab per restored layer.
+  * restore(lo, hi): refused unless every live page fits outside the slabs
+    of [lo, hi); otherwise their live pages move, in ascending order, to the
+    lowest free pages outside the range (compaction) and the range is
+    reserved again for the parameter pull.
 Page contents are optional numpy byte arrays (small configs only) so copies
 and appends can be checked byte for byte.
 
 Parity pinning: the token-level counters this layer sits under are pinned
 against the reference's own outputs (tests/golden/memory_ops.json, produced
 by tests/golden/make_golden.py from pkg/src/dropsim); page ids and page
-bytes have no reference counterpart ("Page/block-table
-layout ... parity unpinned" at the reference level) and are pinned by the
-rules above, which tests/test_oracle.py checks against brute-force.
+bytes have no reference counterpart (page/block-table layout
+is unpinned at the reference level) and are pinned by the rules above, which
+tests/test_oracle.py checks against brute-force invariants.
 """
 
 from __future__ import annotations
@@ -38,6 +39,8 @@ from dataclasses import dataclass, field
 from typing import Optional
 
 import numpy as np
+
+RESERVED = -2  # owner id of a page that holds live weights
 
 
 @dataclass
@@ -49,8 +52,8 @@ class OraclePool:
     max_slots: int
     max_pages_per_seq: int
     track_bytes: bool = False
-    extent: int = field(init=False)
     live: np.ndarray = field(init=False)
+    reserved: np.ndarray = field(init=False)
     owner: dict = field(init=False)
     bt: dict = field(init=False)       # (slot, layer) -> list of page ids
     data: Optional[np.ndarray] = field(init=False, default=None)
@@ -58,13 +61,17 @@ class OraclePool:
     def __post_init__(self):
         assert self.slab_bytes % self.page_bytes == 0
         self.slab_pages = self.slab_bytes // self.page_bytes
-        self.extent = self.head_pages
         self.max_pages = self.head_pages + self.num_layers * self.slab_pages
         self.live = np.zeros(self.max_pages, dtype=bool)
+        self.reserved = np.zeros(self.max_pages, dtype=bool)
+        self.reserved[self.head_pages:] = True
         self.owner = {}
         self.bt = {}
         if self.track_bytes:
             self.data = np.zeros((self.max_pages, self.page_bytes), dtype=np.uint8)
+
+    def slab_range(self, lo: int, hi: int) -> tuple[int, int]:
+        return self.head_pages + lo * self.slab_pages, self.head_pages + hi * self.slab_pages
 
     # cell id exactly as the device encodes owner[] (csrc/kb_pool.cu grow_kernel)
     def cell(self, slot: int, layer: int, idx: int) -> int:
@@ -77,9 +84,16 @@ class OraclePool:
     def live_pages(self) -> int:
         return int(self.live.sum())
 
+    @property
+    def usable_pages(self) -> int:
+        return int((~self.reserved).sum())
+
+    def free_pages(self) -> np.ndarray:
+        return np.flatnonzero(~(self.live | self.reserved))
+
     def grow(self, reqs) -> bool:
         need = sum((hi - lo) * add for _, lo, hi, add in reqs)
-        free = np.flatnonzero(~self.live[:self.extent])
+        free = self.free_pages()
         if need > len(free):
             return False
         k = 0
@@ -101,16 +115,21 @@ class OraclePool:
                     self.live[page] = False
                     self.owner.pop(page, None)
 
-    def drop(self, n_layers: int) -> None:
-        self.extent += n_layers * self.slab_pages
+    def drop(self, lo: int, hi: int) -> None:
+        a, b = self.slab_range(lo, hi)
+        assert self.reserved[a:b].all()
+        self.reserved[a:b] = False
 
-    def restore(self, n_layers: int) -> int:
-        """Vacate the last n slabs; returns pages moved, or -1 if refused."""
-        new_extent = self.extent - n_layers * self.slab_pages
-        src = np.flatnonzero(self.live[new_extent:self.extent]) + new_extent
-        dst = np.flatnonzero(~self.live[:new_extent])[:len(src)]
-        if len(dst) < len(src):
+    def restore(self, lo: int, hi: int) -> int:
+        """Vacate the slabs of [lo, hi); returns pages moved, or -1 if refused."""
+        a, b = self.slab_range(lo, hi)
+        assert not self.reserved[a:b].any()
+        if self.live_pages > self.usable_pages - (b - a):
             return -1
+        src = np.flatnonzero(self.live[a:b]) + a
+        free = self.free_pages()
+        dst = free[(free < a) | (free >= b)][:len(src)]
+        assert len(dst) == len(src)
         for s, d in zip(src.tolist(), dst.tolist()):
             cell = self.owner.pop(s)
             slot_layer, idx = divmod(cell, self.max_pages_per_seq)
@@ -121,13 +140,19 @@ class OraclePool:
             self.live[d] = True
             if self.data is not None:
                 self.data[d] = self.data[s]
-        self.extent = new_extent
+        self.reserved[a:b] = True
         return len(src)
 
-    # ---- data plane (byte-exact) ----------------------------------------
+    def owner_array(self) -> np.ndarray:
+        """owner[] as the device stores it: cell, -2 reserved, -1 free."""
+        out = np.full(self.max_pages, -1, dtype=np.int32)
+        out[self.reserved] = RESERVED
+        for pg, cell in self.owner.items():
+            out[pg] = cell
+        return out
 
-    def page_view(self, page: int) -> np.ndarray:
-        return self.data[page]
+    def bitmap(self) -> np.ndarray:
+        return self.live | self.reserved
 
 
 def copy_pages(dst: OraclePool, src: OraclePool, moves) -> int:

@@ -62,8 +62,12 @@ int ensure_driver();
 struct KvSeg {
   CUmemGenericAllocationHandle h;
   int64_t bytes;
-  bool slab;  // a dropped layer slab (restorable) vs the head segment
+  bool slab;
 };
+
+constexpr uint8_t kLayerHeld = 0;       // weights valid under the weight VA
+constexpr uint8_t kLayerDropped = 1;    // slab pages belong to the KV pool
+constexpr uint8_t kLayerRestoring = 2;  // slab vacated, parameter pull pending
 
 }  // namespace kb
 
@@ -78,12 +82,12 @@ struct kb_pool {
   size_t wva_size = 0;
   CUdeviceptr kva = 0;
   size_t kva_size = 0;
-  std::vector<CUmemGenericAllocationHandle> layer_handle;  // 0 = unmapped
-  std::vector<uint8_t> awaiting_restore;                   // mapped, pull pending
-  std::vector<kb::KvSeg> kv_segs;
-  int64_t kv_mapped_bytes = 0;
+  std::vector<CUmemGenericAllocationHandle> layer_handle;  // slab l (mapped twice)
+  std::vector<uint8_t> layer_state;                        // kLayerHeld / Dropped / Restoring
+  std::vector<kb::KvSeg> kv_segs;                          // head segment
 
-  int64_t extent_pages = 0;
+  int64_t head_pages = 0;    // slack + residual pages at the head of the KV VA
+  int64_t usable_pages = 0;  // head + pages of every dropped slab
   int64_t slack_pages = 0;
   int64_t max_pages = 0;
   int64_t live_pages = 0;

@@ -191,8 +191,10 @@ extern "C" int kb_copy_slabs(kb_pool* dst, kb_pool* src, int32_t lo, int32_t hi,
   if (hi <= lo || byte_lo < 0 || byte_hi < byte_lo || byte_hi > (int64_t)(hi - lo) * slab)
     return fail(KB_EINVAL, "bad slab byte range");
   for (int l = lo; l < hi; ++l) {
-    if (!src->layer_handle[l]) return fail(KB_ESTATE, "source does not hold layer " + std::to_string(l));
-    if (!dst->layer_handle[l]) return fail(KB_ESTATE, "destination layer " + std::to_string(l) + " is not mapped");
+    if (src->layer_state[l] != kLayerHeld)
+      return fail(KB_ESTATE, "source does not hold layer " + std::to_string(l));
+    if (dst->layer_state[l] == kLayerDropped)
+      return fail(KB_ESTATE, "destination layer " + std::to_string(l) + " is not reserved for a pull");
   }
   KB_RT(cudaSetDevice(dst->device));
   uint64_t d = (uint64_t)dst->wva + (uint64_t)lo * slab + byte_lo;
@@ -207,7 +209,8 @@ extern "C" int kb_copy_slabs_from_host(kb_pool* dst, const void* host_src, int32
   if (hi <= lo || byte_lo < 0 || byte_hi < byte_lo || byte_hi > (int64_t)(hi - lo) * slab)
     return fail(KB_EINVAL, "bad slab byte range");
   for (int l = lo; l < hi; ++l)
-    if (!dst->layer_handle[l]) return fail(KB_ESTATE, "destination layer " + std::to_string(l) + " is not mapped");
+    if (dst->layer_state[l] == kLayerDropped)
+      return fail(KB_ESTATE, "destination layer " + std::to_string(l) + " is not reserved for a pull");
   KB_RT(cudaSetDevice(dst->device));
   KB_RT(cudaMemcpyAsync(reinterpret_cast<void*>(dst->wva + (uint64_t)lo * slab + byte_lo),
                         static_cast<const char*>(host_src) + byte_lo, byte_hi - byte_lo,

@@ -3,20 +3,30 @@
 //
 // Reference semantics followed (pkg/src/dropsim/):
 //   build_instance   memory.py:132-144   -> kb_pool_create
-//   drop_layers      memory.py:147-172   -> kb_drop_layers (unmap weight VA,
-//                                           map at KV VA tail)
-//   restore_layers   memory.py:175-197   -> kb_restore_begin (vacate tail by
-//                                           compaction, remap under weight VA)
+//   drop_layers      memory.py:147-172   -> kb_drop_layers
+//   restore_layers   memory.py:175-197   -> kb_restore_begin
 //   complete_restore memory.py:200-212   -> kb_restore_complete
 //   KVAllocator      memory.py:70-129    -> kb_pages_grow / kb_pages_release
-// The reference is token-granular and position-free; pages, block tables and
-// compaction are the device layer underneath.  Every
+//
+// B200 design: every layer slab is ONE physical VMM allocation mapped at TWO
+// virtual addresses from pool creation on -- under the weight VA (layer l at
+// l * slab) and as a fixed page range of the KV VA (after the head segment).
+// Dropping a layer is therefore no driver call at all: a kernel flips the
+// slab's pages from "reserved" to "free" in the page bitmap, and the next
+// block-table growth can hand them out.  Restoring vacates the slab's page
+// range (device compaction: live pages move to the lowest free pages outside
+// it, block tables rewritten through the owner map) and marks it reserved
+// again, so the parameter pull can land under the weight VA.  The paper's
+// "5 ms per remap" (map_latency_us, config.py:40) becomes a
+// few microseconds of kernel time.
+//
+// The reference is token-granular and position-free; pages, block tables
+// and compaction are the device layer underneath.  Every
 // allocation choice is deterministic (lowest free page id first) so the CPU
 // restatement in oracle/kvpool.py reproduces block tables bit for bit.
 #include <algorithm>
 #include <chrono>
 #include <cstring>
-#include <mutex>
 
 #include "kb_common.cuh"
 
@@ -69,6 +79,7 @@ int ensure_scratch(kb_pool* p, int64_t bytes) {
 // ---------------------------------------------------------------- kernels
 
 constexpr int kScanThreads = 1024;
+constexpr int32_t kReserved = -2;  // owner[] of a slab page holding live weights
 
 // Block-wide exclusive scan of one int per thread (1024 threads).
 __device__ __forceinline__ int block_exclusive_scan(int v, int* total, int* warp_sums) {
@@ -98,10 +109,10 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* total, int* warp
   return r;
 }
 
-// Enumerate, in ascending order, the set bits of (select ? live : free) pages
-// in [lo, hi) and hand the k-th one to emit(k, page) for k < limit.  Works
-// in tiles of kScanThreads * kWordsPerThread words; stops once `limit` pages
-// were emitted.  Returns the number found (<= limit) in *found.
+// Enumerate, in ascending order, the set (want_live) or clear bits of the
+// pages in [lo, hi) and hand the k-th one to emit(base_k + k, page) for
+// k < limit.  Tiles of kScanThreads * kWordsPerThread words; stops early
+// once `limit` pages were found.  *found_out = min(found, limit).
 template <int kWordsPerThread, typename Emit>
 __device__ void scan_pages(const uint32_t* __restrict__ bitmap, int64_t lo, int64_t hi,
                            bool want_live, int64_t limit, Emit emit, int64_t* found_out) {
@@ -121,8 +132,8 @@ __device__ void scan_pages(const uint32_t* __restrict__ bitmap, int64_t lo, int6
         uint32_t raw = bitmap[w];
         b = want_live ? raw : ~raw;
         int64_t base = w << 5;
-        if (base < lo) b &= ~0u << (lo - base);           // drop pages < lo
-        if (base + 32 > hi) {                             // drop pages >= hi
+        if (base < lo) b &= ~0u << (lo - base);
+        if (base + 32 > hi) {
           int64_t keep = hi - base;
           b &= keep <= 0 ? 0u : (keep >= 32 ? ~0u : ((1u << keep) - 1u));
         }
@@ -151,7 +162,8 @@ __device__ void scan_pages(const uint32_t* __restrict__ bitmap, int64_t lo, int6
 
 // Grow: a batch of requests passed by value (kernel parameter space, no
 // host->device copy) with exclusive prefix `cum` (pages per request); the
-// k-th lowest free page below `extent` goes to flattened slot k.
+// k-th lowest free page goes to flattened slot k (reserved slab pages are
+// set in the bitmap, so they are never free).
 constexpr int kGrowBatch = 256;
 struct GrowBatch {
   kb_grow r[kGrowBatch];
@@ -161,7 +173,7 @@ struct GrowBatch {
 __global__ void __launch_bounds__(kScanThreads)
 grow_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner, int32_t* __restrict__ bt,
             int32_t* __restrict__ np, const __grid_constant__ GrowBatch batch, int n,
-            int64_t total, int64_t extent, int L, int maxp) {
+            int64_t total, int64_t max_pages, int L, int maxp) {
   const kb_grow* reqs = batch.r;
   const int64_t* cum = batch.cum;
   auto emit = [&](int64_t k, int64_t page) {
@@ -179,11 +191,8 @@ grow_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner, int32_t*
     owner[page] = (int32_t)cell;
     atomicOr(&bitmap[page >> 5], 1u << (page & 31));
   };
-  int64_t found = 0;
-  scan_pages<4>(bitmap, 0, extent, false, total, emit, &found);
+  scan_pages<4>(bitmap, 0, max_pages, false, total, emit, nullptr);
   __syncthreads();
-  // (found < total cannot happen: the host checked capacity first)
-  // advance per-(slot, layer) page counts
   for (int i = 0; i < n; ++i) {
     const kb_grow r = reqs[i];
     for (int l = r.layer_lo + threadIdx.x; l < r.layer_hi; l += blockDim.x)
@@ -217,28 +226,46 @@ __global__ void release_kernel(uint32_t* __restrict__ bitmap, int32_t* __restric
   if (threadIdx.x == 0) np[(int64_t)slot * L + layer] = 0;
 }
 
-// Compaction plan: live pages in [new_extent, extent) ascending -> src[],
-// the same number of lowest free pages below new_extent -> dst[].
+// Mark a page range reserved for weights (set) or free for KV (clear).
+__global__ void range_mark_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner,
+                                  int64_t lo, int64_t hi, int set) {
+  for (int64_t p = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < hi;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    if (set) {
+      atomicOr(&bitmap[p >> 5], 1u << (p & 31));
+      owner[p] = kReserved;
+    } else {
+      atomicAnd(&bitmap[p >> 5], ~(1u << (p & 31)));
+      owner[p] = -1;
+    }
+  }
+}
+
+// Compaction plan for vacating [r_lo, r_hi): its live pages ascending ->
+// src[]; the same number of lowest free pages outside the range -> dst[].
 __global__ void __launch_bounds__(kScanThreads)
-compact_plan_kernel(const uint32_t* __restrict__ bitmap, int64_t new_extent, int64_t extent,
-                    int32_t* __restrict__ src, int32_t* __restrict__ dst, int64_t cap,
-                    int64_t* __restrict__ counts) {
+compact_plan_kernel(const uint32_t* __restrict__ bitmap, int64_t r_lo, int64_t r_hi,
+                    int64_t max_pages, int32_t* __restrict__ src, int32_t* __restrict__ dst,
+                    int64_t cap, int64_t* __restrict__ counts) {
   int64_t m = 0;
-  scan_pages<4>(bitmap, new_extent, extent, true, cap,
+  scan_pages<4>(bitmap, r_lo, r_hi, true, cap,
                 [&](int64_t k, int64_t page) { src[k] = (int32_t)page; }, &m);
   __syncthreads();
-  int64_t f = 0;
-  scan_pages<4>(bitmap, 0, new_extent, false, m,
-                [&](int64_t k, int64_t page) { dst[k] = (int32_t)page; }, &f);
+  int64_t f1 = 0, f2 = 0;
+  scan_pages<4>(bitmap, 0, r_lo, false, m,
+                [&](int64_t k, int64_t page) { dst[k] = (int32_t)page; }, &f1);
+  __syncthreads();
+  if (f1 < m) {
+    scan_pages<4>(bitmap, r_hi, max_pages, false, m - f1,
+                  [&](int64_t k, int64_t page) { dst[f1 + k] = (int32_t)page; }, &f2);
+  }
   if (threadIdx.x == 0) {
     counts[0] = m;
-    counts[1] = f;
+    counts[1] = f1 + f2;
   }
 }
 
 // Move page contents src[i] -> dst[i] within one pool (HBM read+write).
-// One block per 32 KiB piece of a page; 16-byte vector accesses, 8 in flight
-// per thread.
 constexpr int kPieceBytes = 32768;
 constexpr int kCopyThreads = 256;
 
@@ -324,6 +351,11 @@ static int64_t now_ns() {
       .count();
 }
 
+static inline int64_t slab_pages(const kb_pool* p) { return p->m.slab_bytes / p->m.page_bytes; }
+static inline int64_t slab_first_page(const kb_pool* p, int layer) {
+  return p->head_pages + (int64_t)layer * slab_pages(p);
+}
+
 }  // namespace kb
 
 using namespace kb;
@@ -399,45 +431,46 @@ extern "C" int kb_pool_create(int32_t device, const kb_model_desc* model, int64_
     kb_pool_destroy(p);
     return code;
   };
-  // weight VA: one slab per layer
-  p->wva_size = (size_t)param;
-  CUresult r = drv().MemAddressReserve(&p->wva, p->wva_size, (size_t)gran, 0, 0);
-  if (r != CUDA_SUCCESS) return bail(fail(KB_ECUDA, "drv().MemAddressReserve(weights) failed"));
-  p->layer_handle.assign(m.num_layers, 0);
-  p->awaiting_restore.assign(m.num_layers, 0);
-  for (int l = 0; l < m.num_layers; ++l) {
-    CUmemGenericAllocationHandle h;
-    if ((rc = make_handle(device, m.slab_bytes, &h))) return bail(rc);
-    p->layer_handle[l] = h;
-    if ((rc = map_at(p, p->wva + (CUdeviceptr)l * m.slab_bytes, m.slab_bytes, h))) return bail(rc);
-  }
-  // KV VA: head segment (slack + residual) then room for every slab
   const int64_t head = round_up((int64_t)slack_pages * m.page_bytes + (hbm_bytes - param), gran);
+  p->wva_size = (size_t)param;
   p->kva_size = (size_t)(head + param);
+  CUresult r = drv().MemAddressReserve(&p->wva, p->wva_size, (size_t)gran, 0, 0);
+  if (r != CUDA_SUCCESS) return bail(fail(KB_ECUDA, "cuMemAddressReserve(weights) failed"));
   r = drv().MemAddressReserve(&p->kva, p->kva_size, (size_t)gran, 0, 0);
-  if (r != CUDA_SUCCESS) return bail(fail(KB_ECUDA, "drv().MemAddressReserve(kv) failed"));
+  if (r != CUDA_SUCCESS) return bail(fail(KB_ECUDA, "cuMemAddressReserve(kv) failed"));
   {
     CUmemGenericAllocationHandle h;
     if ((rc = make_handle(device, head, &h))) return bail(rc);
     p->kv_segs.push_back({h, head, false});
     if ((rc = map_at(p, p->kva, head, h))) return bail(rc);
-    p->kv_mapped_bytes = head;
   }
+  // each layer slab: one physical allocation, two views
+  p->layer_handle.assign(m.num_layers, 0);
+  p->layer_state.assign(m.num_layers, kLayerHeld);
+  for (int l = 0; l < m.num_layers; ++l) {
+    CUmemGenericAllocationHandle h;
+    if ((rc = make_handle(device, m.slab_bytes, &h))) return bail(rc);
+    p->layer_handle[l] = h;
+    if ((rc = map_at(p, p->wva + (CUdeviceptr)l * m.slab_bytes, m.slab_bytes, h))) return bail(rc);
+    if ((rc = map_at(p, p->kva + head + (CUdeviceptr)l * m.slab_bytes, m.slab_bytes, h)))
+      return bail(rc);
+  }
+  p->head_pages = head / m.page_bytes;
+  p->slack_pages = slack_pages;
+  p->usable_pages = p->head_pages;
+  p->max_pages = (int64_t)p->kva_size / m.page_bytes;
   if (m.head_dim == 128 && (m.block_tokens == 64 || m.block_tokens == 128)) {
     cuuint64_t dims[2] = {128, (cuuint64_t)(p->kva_size / 256)};
     cuuint64_t strides[1] = {256};
     cuuint32_t box[2] = {64, (cuuint32_t)m.block_tokens};
     cuuint32_t estr[2] = {1, 1};
     r = drv().TensorMapEncodeTiled(&p->kv_tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                               reinterpret_cast<void*>(p->kva), dims, strides, box, estr,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return bail(fail(KB_ECUDA, "drv().TensorMapEncodeTiled(kv) failed"));
+                                   reinterpret_cast<void*>(p->kva), dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return bail(fail(KB_ECUDA, "cuTensorMapEncodeTiled(kv) failed"));
   }
-  p->slack_pages = slack_pages;
-  p->extent_pages = head / m.page_bytes;
-  p->max_pages = (int64_t)p->kva_size / m.page_bytes;
   if (p->max_pages >= (int64_t)1 << 31) return bail(fail(KB_EINVAL, "too many pages for int32 ids"));
   p->n_words = ceil_div(p->max_pages, 32);
   const int64_t cells = (int64_t)max_slots * m.num_layers;
@@ -458,6 +491,9 @@ extern "C" int kb_pool_create(int32_t device, const kb_model_desc* model, int64_
   if (cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(KB_ECUDA, "cudaStreamCreate failed"));
   if ((rc = ensure_scratch(p, 1 << 20))) return bail(rc);
+  // every slab page starts reserved: the layer's weights live there
+  range_mark_kernel<<<grid_for(p->max_pages - p->head_pages, 256, 1024), 256, 0, p->own_stream>>>(
+      p->d_bitmap, p->d_owner, p->head_pages, p->max_pages, 1);
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(KB_ECUDA, "pool init sync failed"));
   *out = p;
   return KB_OK;
@@ -467,17 +503,17 @@ extern "C" int kb_pool_destroy(kb_pool* p) {
   if (!p) return KB_OK;
   cudaSetDevice(p->device);
   cudaDeviceSynchronize();
+  const int64_t head = p->kv_segs.empty() ? 0 : p->kv_segs[0].bytes;
   for (int l = 0; l < (int)p->layer_handle.size(); ++l) {
     if (p->layer_handle[l]) {
       drv().MemUnmap(p->wva + (CUdeviceptr)l * p->m.slab_bytes, p->m.slab_bytes);
+      drv().MemUnmap(p->kva + head + (CUdeviceptr)l * p->m.slab_bytes, p->m.slab_bytes);
       drv().MemRelease(p->layer_handle[l]);
     }
   }
-  int64_t off = 0;
   for (auto& s : p->kv_segs) {
-    drv().MemUnmap(p->kva + off, s.bytes);
+    drv().MemUnmap(p->kva, s.bytes);
     drv().MemRelease(s.h);
-    off += s.bytes;
   }
   if (p->wva) drv().MemAddressFree(p->wva, p->wva_size);
   if (p->kva) drv().MemAddressFree(p->kva, p->kva_size);
@@ -494,13 +530,13 @@ extern "C" int kb_pool_destroy(kb_pool* p) {
 
 extern "C" int kb_pool_query(kb_pool* p, kb_pool_info* o) {
   if (!p || !o) return fail(KB_EINVAL, "null pool");
-  o->extent_pages = p->extent_pages;
+  o->extent_pages = p->usable_pages;
   o->live_pages = p->live_pages;
   o->slack_pages = p->slack_pages;
   o->max_pages = p->max_pages;
-  int mapped = 0;
-  for (auto h : p->layer_handle) mapped += h != 0;
-  o->layers_mapped = mapped;
+  int held = 0;
+  for (auto s : p->layer_state) held += s != kLayerDropped;
+  o->layers_mapped = held;
   o->device = p->device;
   o->weight_base = (uint64_t)p->wva;
   o->kv_base = (uint64_t)p->kva;
@@ -512,7 +548,8 @@ extern "C" int kb_pool_query(kb_pool* p, kb_pool_info* o) {
 }
 
 extern "C" uint64_t kb_weight_ptr(kb_pool* p, int32_t layer) {
-  if (!p || layer < 0 || layer >= p->m.num_layers || !p->layer_handle[layer]) return 0;
+  if (!p || layer < 0 || layer >= p->m.num_layers || p->layer_state[layer] == kLayerDropped)
+    return 0;
   return (uint64_t)(p->wva + (CUdeviceptr)layer * p->m.slab_bytes);
 }
 
@@ -521,23 +558,21 @@ extern "C" int kb_drop_layers(kb_pool* p, int32_t lo, int32_t hi, int64_t* remap
   if (hi <= lo) return fail(KB_EINVAL, "empty layer range");
   for (int l = lo; l < hi; ++l) {
     if (l < 0 || l >= p->m.num_layers) return fail(KB_EINVAL, "layer " + std::to_string(l) + " absent from segment table");
-    if (!p->layer_handle[l] || p->awaiting_restore[l])
+    if (p->layer_state[l] != kLayerHeld)
       return fail(KB_ESTATE, "layer " + std::to_string(l) + " absent on device pool");
   }
   KB_RT(cudaSetDevice(p->device));
   const int64_t t0 = now_ns();
-  KB_RT(cudaDeviceSynchronize());  // no in-flight reader of these weights
-  const int64_t slab = p->m.slab_bytes;
-  for (int l = lo; l < hi; ++l) {
-    CUmemGenericAllocationHandle h = p->layer_handle[l];
-    KB_CU(drv().MemUnmap(p->wva + (CUdeviceptr)l * slab, slab));
-    p->layer_handle[l] = 0;
-    int rc = map_at(p, p->kva + p->kv_mapped_bytes, slab, h);
-    if (rc) return rc;
-    p->kv_segs.push_back({h, slab, true});
-    p->kv_mapped_bytes += slab;
-    p->extent_pages += slab / p->m.page_bytes;
-  }
+  // the slab pages of [lo, hi) become free KV pages; no driver call, the
+  // slabs were mapped into the KV VA at creation.  Synchronous on the pool's
+  // stream so any later grow (on any stream) sees them.
+  const int64_t a = slab_first_page(p, lo), b = slab_first_page(p, hi);
+  range_mark_kernel<<<grid_for(b - a, 256, 1024), 256, 0, p->own_stream>>>(p->d_bitmap, p->d_owner,
+                                                                           a, b, 0);
+  KB_LAUNCH_CHECK();
+  KB_RT(cudaStreamSynchronize(p->own_stream));
+  for (int l = lo; l < hi; ++l) p->layer_state[l] = kLayerDropped;
+  p->usable_pages += b - a;
   if (remap_ns) *remap_ns = now_ns() - t0;
   return KB_OK;
 }
@@ -546,60 +581,47 @@ extern "C" int kb_restore_begin(kb_pool* p, int32_t lo, int32_t hi, uintptr_t st
                                 int64_t* moved_pages, int64_t* remap_ns) {
   if (!p) return fail(KB_EINVAL, "null pool");
   if (hi <= lo) return fail(KB_EINVAL, "empty layer range");
-  const int n = hi - lo;
   for (int l = lo; l < hi; ++l) {
     if (l < 0 || l >= p->m.num_layers) return fail(KB_EINVAL, "layer " + std::to_string(l) + " absent from segment table");
-    if (p->layer_handle[l]) return fail(KB_ESTATE, "layer " + std::to_string(l) + " already held on device pool");
+    if (p->layer_state[l] != kLayerDropped)
+      return fail(KB_ESTATE, "layer " + std::to_string(l) + " already held on device pool");
   }
-  int tail_slabs = 0;
-  for (int i = (int)p->kv_segs.size() - 1; i >= 0 && p->kv_segs[i].slab; --i) ++tail_slabs;
-  if (tail_slabs < n) return fail(KB_ESTATE, "KV tail holds fewer dropped slabs than the restore needs");
+  const int64_t a = slab_first_page(p, lo), b = slab_first_page(p, hi);
+  // every live page must fit outside the returned range
+  if (p->live_pages > p->usable_pages - (b - a))
+    return fail(KB_REFUSED, "restore blocked: " + std::to_string(p->live_pages) +
+                                " live pages do not fit in " +
+                                std::to_string(p->usable_pages - (b - a)) + " remaining pages");
   KB_RT(cudaSetDevice(p->device));
+  const int64_t t0 = now_ns();
+  // releases / grows may be in flight on other streams: the plan must see them
+  KB_RT(cudaDeviceSynchronize());
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t slab_pages = p->m.slab_bytes / p->m.page_bytes;
-  const int64_t new_extent = p->extent_pages - (int64_t)n * slab_pages;
-  const int64_t cap = (int64_t)n * slab_pages;
+  const int64_t cap = b - a;
   int rc = ensure_scratch(p, 2 * cap * 4 + 64);
   if (rc) return rc;
   int64_t* d_counts = reinterpret_cast<int64_t*>(p->d_scratch);
   int32_t* d_src = reinterpret_cast<int32_t*>((char*)p->d_scratch + 64);
   int32_t* d_dst = d_src + cap;
-  compact_plan_kernel<<<1, kScanThreads, 0, st>>>(p->d_bitmap, new_extent, p->extent_pages, d_src,
-                                                   d_dst, cap, d_counts);
+  compact_plan_kernel<<<1, kScanThreads, 0, st>>>(p->d_bitmap, a, b, p->max_pages, d_src, d_dst,
+                                                   cap, d_counts);
+  KB_LAUNCH_CHECK();
+  const int64_t pieces = p->m.page_bytes / kPieceBytes > 0 ? p->m.page_bytes / kPieceBytes : 1;
+  compact_copy_kernel<<<grid_for(cap * pieces, 1, 148 * 16), kCopyThreads, 0, st>>>(
+      reinterpret_cast<uint8_t*>(p->kva), d_src, d_dst, d_counts, p->m.page_bytes);
+  KB_LAUNCH_CHECK();
+  compact_fixup_kernel<<<grid_for(cap, 256, 1024), 256, 0, st>>>(p->d_bitmap, p->d_owner, p->d_bt,
+                                                                  d_src, d_dst, d_counts);
+  KB_LAUNCH_CHECK();
+  range_mark_kernel<<<grid_for(cap, 256, 1024), 256, 0, st>>>(p->d_bitmap, p->d_owner, a, b, 1);
   KB_LAUNCH_CHECK();
   int64_t counts[2];
   KB_RT(cudaMemcpyAsync(counts, d_counts, 16, cudaMemcpyDeviceToHost, st));
   KB_RT(cudaStreamSynchronize(st));
-  if (counts[1] < counts[0]) {
-    return fail(KB_REFUSED, "restore blocked: " + std::to_string(counts[0]) +
-                                " live tail pages but only " + std::to_string(counts[1]) +
-                                " free pages below the new extent");
-  }
-  if (counts[0] > 0) {
-    const int64_t pieces = p->m.page_bytes / kPieceBytes > 0 ? p->m.page_bytes / kPieceBytes : 1;
-    int grid = grid_for(counts[0] * pieces, 1, 148 * 16);
-    compact_copy_kernel<<<grid, kCopyThreads, 0, st>>>(reinterpret_cast<uint8_t*>(p->kva), d_src,
-                                                       d_dst, d_counts, p->m.page_bytes);
-    KB_LAUNCH_CHECK();
-    compact_fixup_kernel<<<grid_for(counts[0], 256, 1024), 256, 0, st>>>(p->d_bitmap, p->d_owner,
-                                                                          p->d_bt, d_src, d_dst,
-                                                                          d_counts);
-    KB_LAUNCH_CHECK();
-  }
-  const int64_t t0 = now_ns();
-  KB_RT(cudaDeviceSynchronize());
-  const int64_t slab = p->m.slab_bytes;
-  for (int k = 0; k < n; ++k) {
-    kb::KvSeg s = p->kv_segs.back();
-    p->kv_segs.pop_back();
-    p->kv_mapped_bytes -= s.bytes;
-    KB_CU(drv().MemUnmap(p->kva + p->kv_mapped_bytes, s.bytes));
-    p->extent_pages -= slab_pages;
-    rc = map_at(p, p->wva + (CUdeviceptr)(lo + k) * slab, slab, s.h);
-    if (rc) return rc;
-    p->layer_handle[lo + k] = s.h;
-    p->awaiting_restore[lo + k] = 1;
-  }
+  if (counts[1] < counts[0])  // cannot happen after the capacity check above
+    return fail(KB_ESTATE, "compaction found too few free pages");
+  for (int l = lo; l < hi; ++l) p->layer_state[l] = kLayerRestoring;
+  p->usable_pages -= b - a;
   if (moved_pages) *moved_pages = counts[0];
   if (remap_ns) *remap_ns = now_ns() - t0;
   return KB_OK;
@@ -608,10 +630,10 @@ extern "C" int kb_restore_begin(kb_pool* p, int32_t lo, int32_t hi, uintptr_t st
 extern "C" int kb_restore_complete(kb_pool* p, int32_t lo, int32_t hi) {
   if (!p) return fail(KB_EINVAL, "null pool");
   for (int l = lo; l < hi; ++l) {
-    if (l < 0 || l >= p->m.num_layers || !p->layer_handle[l] || !p->awaiting_restore[l])
+    if (l < 0 || l >= p->m.num_layers || p->layer_state[l] != kLayerRestoring)
       return fail(KB_ESTATE, "layer " + std::to_string(l) + " not awaiting restore");
   }
-  for (int l = lo; l < hi; ++l) p->awaiting_restore[l] = 0;
+  for (int l = lo; l < hi; ++l) p->layer_state[l] = kLayerHeld;
   return KB_OK;
 }
 
@@ -619,9 +641,7 @@ extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr
   if (!p) return fail(KB_EINVAL, "null pool");
   if (n <= 0) return KB_OK;
   const int L = p->m.num_layers;
-  std::vector<int64_t> cum(n);
   int64_t total = 0;
-  std::vector<uint8_t> seen;  // duplicate (slot, layer) detection
   for (int i = 0; i < n; ++i) {
     const kb_grow& r = reqs[i];
     if (r.slot < 0 || r.slot >= p->max_slots || r.layer_lo < 0 || r.layer_hi > L ||
@@ -632,7 +652,6 @@ extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr
       if (p->h_np[c] + r.add_pages > p->maxp)
         return fail(KB_EINVAL, "slot " + std::to_string(r.slot) + " exceeds max_pages_per_seq");
     }
-    cum[i] = total;
     total += (int64_t)(r.layer_hi - r.layer_lo) * r.add_pages;
   }
   if (n > 1) {
@@ -644,14 +663,13 @@ extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr
     for (size_t i = 1; i < cells.size(); ++i)
       if (cells[i] == cells[i - 1]) return fail(KB_EINVAL, "duplicate (slot, layer) in one grow batch");
   }
-  if (total > p->extent_pages - p->live_pages)
+  if (total > p->usable_pages - p->live_pages)
     return fail(KB_REFUSED, "out of KV pages: need " + std::to_string(total) + ", free " +
-                                std::to_string(p->extent_pages - p->live_pages));
+                                std::to_string(p->usable_pages - p->live_pages));
   KB_RT(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
-  // batches of kGrowBatch requests travel in kernel parameter space: no
-  // staging copy and no host synchronization; launches on one stream run in
-  // order, so a later batch sees the pages an earlier one took
+  // batches travel in kernel parameter space: no staging copy, no host
+  // synchronization; launches on one stream run in order
   GrowBatch batch;
   for (int b0 = 0; b0 < n; b0 += kGrowBatch) {
     const int nb = std::min(kGrowBatch, n - b0);
@@ -662,10 +680,9 @@ extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr
       sub += (int64_t)(reqs[b0 + i].layer_hi - reqs[b0 + i].layer_lo) * reqs[b0 + i].add_pages;
     }
     grow_kernel<<<1, kScanThreads, 0, st>>>(p->d_bitmap, p->d_owner, p->d_bt, p->d_np, batch, nb,
-                                            sub, p->extent_pages, L, p->maxp);
+                                            sub, p->max_pages, L, p->maxp);
     KB_LAUNCH_CHECK();
   }
-  (void)cum;
   for (int i = 0; i < n; ++i)
     for (int l = reqs[i].layer_lo; l < reqs[i].layer_hi; ++l)
       p->h_np[(int64_t)reqs[i].slot * L + l] += reqs[i].add_pages;

@@ -1,19 +1,24 @@
 """One parameter-centric overload cycle on real device pools.
 
-drop -> KV exchange -> restore -> consolidate, driven through the same
-public calls the reference's engine makes (pkg/src/dropsim/engine.py):
+drop -> KV exchange -> (burst drains) -> restore -> consolidate, driven
+through the same public calls the reference's engine makes
+(pkg/src/dropsim/engine.py):
 
   plan     compute_demand + plan_drop               engine.py:616-648
   drop     member_moves + memory.drop_layers         engine.py:751-807
   re-share stage_share allocations                   engine.py:823-830
   exchange plan_exchange per original-map cohort     engine.py:690-726
+  drain    half the residents finish: occupancy falls under the restore
+           threshold (0.5), the gate of engine.py:1051-1059
   restore  memory.restore_layers + plan_restore_transfers +
            complete_restore                          engine.py:1093-1157
   dissolve consolidation of peer KV back home        engine.py:1159-1254
+  refill   the finished residents are re-admitted (next burst)
 
-Every byte movement runs on the GPU through transfer.TransferEngine; the
-cycle returns the instances to their boot layout, so it can be repeated.
-Used by bench.py (the headline drop/restore GB/s) and by the GPU tests.
+Every byte movement runs on the GPU through transfer.TransferEngine.  The
+drain and refill phases are bookkeeping + synthetic KV writes and are not
+part of the timed path; the long-lived residents' KV must survive every
+cycle bit for bit (checked by kv_checksums()).
 """
 
 from __future__ import annotations
@@ -39,6 +44,7 @@ class CycleReport:
     n_tasks: int = 0
     ms: dict = field(default_factory=dict)
     param_kernel_ms: float = 0.0   # device time of the parameter-pull launches
+    kv_kernel_ms: float = 0.0      # device time of the KV page-copy launches
 
     @property
     def bytes_moved(self) -> int:
@@ -47,9 +53,9 @@ class CycleReport:
 
 
 class OverloadCycle:
-    """N instances (replicas) on the devices of `runtimes` (one per instance,
-    several instances may share a GPU), each filled to `fill` of its KV
-    budget with ShareGPT-shaped residents."""
+    """Replicas (one per entry of `runtimes`; several may share a GPU), each
+    filled to `fill` of its KV budget with ShareGPT-shaped residents; every
+    other resident is transient (finishes during the drain)."""
 
     def __init__(self, runtimes: list, shape: ModelShape, kv_budget_bytes: int,
                  fill: float = 0.9, seed: int = 3, kv_chunk_bytes: int = 64 << 20,
@@ -70,11 +76,9 @@ class OverloadCycle:
         self.slots = {i: SlotTable(runtimes[i].max_slots) for i in self.instances}
         self.te = TransferEngine(self.pools, self.slots, timing=True)
         self._fill_weights()
-        # residents: ShareGPT-shaped lengths, dealt round-robin until full
         trace = synth_burst(10_000.0, 4.0, 16.0, 0.0, 10_000.0, input_mean, 373, seed=seed)
         self.tokens: dict[int, int] = {}
         self.home: dict[int, int] = {}
-        B = shape.block_tokens
         full = {i: False for i in self.instances}
         rid = 0
         for rec in trace:
@@ -85,28 +89,31 @@ class OverloadCycle:
             if full[iid]:
                 continue
             inst = self.instances[iid]
-            cap = inst.kv.capacity_tokens
-            if inst.kv.used_tokens + rec.input_len > fill * cap:
+            if inst.kv.used_tokens + rec.input_len > fill * inst.kv.capacity_tokens:
                 full[iid] = True
                 continue
-            assert inst.kv.alloc(rid, rec.input_len)
-            slot = self.slots[iid].get(rid)
-            assert inst.pool.grow([(slot, 0, self.L, -(-rec.input_len // B))])
             self.tokens[rid] = rec.input_len
             self.home[rid] = iid
-        torch.cuda.synchronize()
-        # synthetic KV content: deterministic random bytes over every mapped page
-        for iid, pool in self.pools.items():
+            self._admit(rid)
+        self.transient = set(sorted(self.tokens)[1::2])
+        for iid, pool in self.pools.items():  # synthetic KV content on every mapped page
             g = torch.Generator(device=f"cuda:{pool.rt.device}").manual_seed(77 + iid)
-            kv = pool.kv_bytes()
-            kv.view(torch.int32).copy_(torch.randint(-2**31, 2**31 - 1, (kv.numel() // 4,),
-                                                     dtype=torch.int32, device=kv.device,
-                                                     generator=g))
+            kv = pool.kv_bytes().view(torch.int32)
+            kv.copy_(torch.randint(-2**31, 2**31 - 1, (kv.numel(),), dtype=torch.int32,
+                                   device=kv.device, generator=g))
         torch.cuda.synchronize()
         self.pause_merged = False  # set True to stop after the exchange (see resume())
         self._paused = None
+        self.merged = {}
 
     # ------------------------------------------------------------------ data
+    def _admit(self, rid: int) -> None:
+        iid = self.home[rid]
+        inst = self.instances[iid]
+        assert inst.kv.alloc(rid, self.tokens[rid])
+        slot = self.slots[iid].get(rid)
+        assert inst.pool.grow([(slot, 0, self.L, -(-self.tokens[rid] // self.shape.block_tokens))])
+
     def _fill_weights(self) -> None:
         """bf16 randn x 0.02 per layer, seed 1000 + layer: identical replicas,
         so a restored layer is checkable bit for bit."""
@@ -119,32 +126,31 @@ class OverloadCycle:
                 w.copy_((torch.randn(n, device=w.device, generator=g) * 0.02).to(torch.bfloat16))
         torch.cuda.synchronize()
 
+    def _bt_view(self, iid):
+        torch = self.torch
+        inf = self.pools[iid].info()
+        bt = runtime.device_bytes(inf.block_table,
+                                  inf.max_slots * self.L * inf.max_pages_per_seq * 4)
+        return bt.view(torch.int32).view(inf.max_slots, self.L, inf.max_pages_per_seq)
+
     def weight_checksums(self) -> dict:
         torch = self.torch
-        out = {}
-        for iid, pool in self.pools.items():
-            for l in range(self.L):
-                w = pool.weight_bytes(l).view(torch.int32)
-                out[(iid, l)] = int(w.to(torch.int64).sum().item())
-        return out
+        return {(iid, l): int(pool.weight_bytes(l).view(torch.int32).to(torch.int64).sum().item())
+                for iid, pool in self.pools.items() for l in range(self.L)}
 
     def kv_checksums(self) -> dict:
-        """Per resident: per (layer, page index) int32-sum of the page bytes
-        on its home instance, in block-table order."""
+        """Long-lived residents: per (layer, page) int32 sums of the pages on
+        their home instance, in block-table order."""
         torch = self.torch
         out = {}
         for iid, pool in self.pools.items():
-            inf = pool.info()
-            bt = runtime.device_bytes(inf.block_table,
-                                      inf.max_slots * self.L * inf.max_pages_per_seq * 4)
-            bt = bt.view(torch.int32).view(inf.max_slots, self.L, inf.max_pages_per_seq)
+            bt = self._bt_view(iid)
             kv = pool.kv_bytes().view(torch.int32).view(-1, pool.page_bytes // 4)
             for rid, home in self.home.items():
-                if home != iid:
+                if home != iid or rid in self.transient:
                     continue
-                slot = self.slots[iid].of[rid]
                 npg = -(-self.tokens[rid] // self.shape.block_tokens)
-                pages = bt[slot, :, :npg].reshape(-1).long()
+                pages = bt[self.slots[iid].of[rid], :, :npg].reshape(-1).long()
                 out[rid] = kv.index_select(0, pages).to(torch.int64).sum(dim=1).cpu()
         return out
 
@@ -154,14 +160,13 @@ class OverloadCycle:
         rep = CycleReport()
         st = self.te.bulk
         ev = {k: torch.cuda.Event(enable_timing=True) for k in
-              ("t0", "drop", "exch", "restore", "cons")}
+              ("t0", "drop", "exch", "drain", "restore", "cons")}
         kvbpt = self.model.kv_bytes_per_token
         L = self.L
         ev["t0"].record(st)
-        # ---- plan (engine.py:616-648)
+        # ---- plan (engine.py:616-648): a queued burst that outgrows every
+        # replica's free KV by a quarter of one parameter copy
         groups = [Group(i, [i], {i: (0, L)}) for i in sorted(self.instances)]
-        # a queued burst that outgrows every replica's free KV by a quarter of
-        # one parameter copy: the planner answers with one merge per pair
         demand = 0
         for i, inst in sorted(self.instances.items()):
             free = inst.kv.free_tokens * kvbpt
@@ -173,7 +178,8 @@ class OverloadCycle:
         # ---- merge: drops, then re-share (engine.py:751-830)
         live = {g.gid: g for g in groups}
         for m in plan.merges:
-            ga, gb = live.pop(m.gid_a), live.pop(m.gid_b)
+            live.pop(m.gid_a)
+            live.pop(m.gid_b)
             new = Group(m.gid, list(m.members), dict(m.stage_layer_map))
             new.validate_coverage(L)
             for iid in m.members:
@@ -214,14 +220,17 @@ class OverloadCycle:
                 rep.n_tasks += len(tasks)
         done = self.te.drain()
         rep.bytes_kv_exchange = sum(p.bytes_moved for p in done)
+        rep.kv_kernel_ms += sum(p.start_event.elapsed_time(p.event) for p in done)
         self.te.finish_flow_sources()
         ev["exch"].record(st)
         self.merged = live
-        return self._restore_and_dissolve(rep, live, ev, tid)
+        if self.pause_merged:
+            self._paused = (rep, live, ev, tid)
+            return rep
+        return self._finish(rep, live, ev, tid)
 
     def merged_decode_layout(self):
-        """(instance -> (layers, [(rid, slot, ctx)])) of the merged state, for
-        the decode measurement that runs between exchange and restore."""
+        """instance -> ((lo, hi), [(rid, slot, ctx)]) of the merged state."""
         out = {}
         for g in self.merged.values():
             for iid in g.member_instances:
@@ -230,15 +239,26 @@ class OverloadCycle:
                 out[iid] = (g.stage_layer_map[iid], res)
         return out
 
-    def _restore_and_dissolve(self, rep: CycleReport, live: dict, ev: dict,
-                              tid: int) -> CycleReport:
+    def resume(self) -> CycleReport:
+        rep, live, ev, tid = self._paused
+        self._paused = None
+        self.pause_merged = False
+        return self._finish(rep, live, ev, tid)
+
+    def _finish(self, rep: CycleReport, live: dict, ev: dict, tid: int) -> CycleReport:
         torch = self.torch
         st = self.te.bulk
         L = self.L
         kvbpt = self.model.kv_bytes_per_token
-        if self.pause_merged:
-            self._paused = (rep, live, ev, tid)
-            return rep
+        # ---- drain: transient residents finish (engine.py:_finish -> group_free)
+        for rid in sorted(self.transient):
+            for iid, inst in self.instances.items():
+                inst.kv.free(rid)
+                slot = self.slots[iid].of.get(rid)
+                if slot is not None:
+                    self.pools[iid].release([slot], 0, L, stream=st)
+                    self.slots[iid].drop(rid)
+        ev["drain"].record(st)
         # ---- restore (engine.py:1093-1157): reserve + compaction + remap, pulls
         for g in sorted(live.values(), key=lambda g: g.gid):
             missing, holders = {}, {}
@@ -262,24 +282,24 @@ class OverloadCycle:
             rep.n_tasks += len(tasks)
             done = self.te.drain()
             rep.bytes_param += sum(p.bytes_moved for p in done)
-            rep.param_kernel_ms += sum(p.start_event.elapsed_time(p.event) for p in done
-                                       if p.start_event is not None)
+            rep.param_kernel_ms += sum(p.start_event.elapsed_time(p.event) for p in done)
             for iid, rngs in missing.items():
                 for rng in rngs:
                     memory.complete_restore(self.instances[iid], rng)
-        rep.bytes_compaction = rep.pages_compacted * self.shape.page_bytes * 2  # read + write
+        rep.bytes_compaction = rep.pages_compacted * self.shape.page_bytes
         ev["restore"].record(st)
         # ---- dissolve + consolidation (engine.py:1159-1254)
         cons_tasks = []
         for rid in sorted(self.tokens):
+            if rid in self.transient:
+                continue
             home = self.home[rid]
             g = next(g for g in live.values() if home in g.member_instances)
             for iid in g.member_instances:
                 if iid == home:
                     continue
                 lo, hi = g.stage_layer_map[iid]
-                nbytes = share_bytes(self.tokens[rid], lo, hi, L, kvbpt)
-                left = nbytes
+                left = share_bytes(self.tokens[rid], lo, hi, L, kvbpt)
                 chunks = []
                 while left > 0:
                     take = min(self.kv_chunk, left)
@@ -294,8 +314,11 @@ class OverloadCycle:
         rep.n_tasks += len(cons_tasks)
         done = self.te.drain()
         rep.bytes_kv_consolidate = sum(p.bytes_moved for p in done)
+        rep.kv_kernel_ms += sum(p.start_event.elapsed_time(p.event) for p in done)
         self.te.finish_flow_sources()
         for rid, tok in self.tokens.items():
+            if rid in self.transient:
+                continue
             home = self.home[rid]
             for iid, inst in self.instances.items():
                 if iid != home:
@@ -306,16 +329,31 @@ class OverloadCycle:
             if extra:
                 assert inst.kv.alloc(rid, extra)
         ev["cons"].record(st)
+        # ---- refill: the next burst re-admits the transient residents
+        self.refill()
         ev["cons"].synchronize()
-        rep.ms = {"drop": ev["t0"].elapsed_time(ev["drop"]),
-                  "exchange": ev["drop"].elapsed_time(ev["exch"]),
-                  "restore": ev["exch"].elapsed_time(ev["restore"]),
-                  "consolidate": ev["restore"].elapsed_time(ev["cons"]),
-                  "total": ev["t0"].elapsed_time(ev["cons"])}
+        parts = {"drop": ev["t0"].elapsed_time(ev["drop"]),
+                 "exchange": ev["drop"].elapsed_time(ev["exch"]),
+                 "restore": ev["drain"].elapsed_time(ev["restore"]),
+                 "consolidate": ev["restore"].elapsed_time(ev["cons"])}
+        parts["total"] = sum(parts.values())
+        parts["drain_untimed"] = ev["exch"].elapsed_time(ev["drain"])
+        rep.ms = parts
         return rep
 
-    def resume(self) -> CycleReport:
-        rep, live, ev, tid = self._paused
-        self._paused = None
-        self.pause_merged = False
-        return self._restore_and_dissolve(rep, live, ev, tid)
+    def refill(self) -> None:
+        torch = self.torch
+        for rid in sorted(self.transient):
+            self._admit(rid)
+        for iid, pool in self.pools.items():
+            bt = self._bt_view(iid)
+            rows = []
+            for rid in sorted(self.transient):
+                if self.home[rid] == iid:
+                    npg = -(-self.tokens[rid] // self.shape.block_tokens)
+                    rows.append(bt[self.slots[iid].of[rid], :, :npg].reshape(-1))
+            if rows:
+                kv = pool.kv_bytes().view(torch.int32).view(-1, pool.page_bytes // 4)
+                pages = torch.cat(rows).long()
+                kv.index_fill_(0, pages, 0x5A5A5A5A)
+        torch.cuda.synchronize()

@@ -256,9 +256,10 @@ class DevicePool:
         return device_bytes(ptr, self.model.bytes_per_layer)
 
     def kv_bytes(self):
-        """uint8 view of the mapped KV extent (pages [0, extent))."""
+        """uint8 view of the whole KV VA (pages [0, max_pages)): head pages and
+        every layer slab's alias, dropped or not."""
         inf = self.info()
-        return device_bytes(inf.kv_base, inf.extent_pages * self.page_bytes)
+        return device_bytes(inf.kv_base, inf.max_pages * self.page_bytes)
 
     # -- N2: block tables
     def grow(self, reqs: Sequence[tuple[int, int, int, int]], stream=None) -> bool:
@@ -291,7 +292,7 @@ class DevicePool:
 
     def bitmap(self, n_pages: Optional[int] = None):
         import numpy as np
-        n_pages = n_pages or self.info().extent_pages
+        n_pages = n_pages or self.info().max_pages
         words = (n_pages + 31) // 32
         buf = (C.c_uint32 * words)()
         _check(_lib.kb_read_bitmap(self.h, buf, words))
@@ -300,7 +301,7 @@ class DevicePool:
 
     def owners(self, n_pages: Optional[int] = None):
         import numpy as np
-        n_pages = n_pages or self.info().extent_pages
+        n_pages = n_pages or self.info().max_pages
         buf = (C.c_int32 * n_pages)()
         _check(_lib.kb_read_owner(self.h, buf, n_pages))
         return np.frombuffer(bytes(buf), dtype=np.int32).copy()

@@ -40,15 +40,11 @@ def oracle_for(pool):
 
 def assert_same_state(pool, orc, slots):
     inf = pool.info()
-    assert inf.extent_pages == orc.extent
+    assert inf.max_pages == orc.max_pages
+    assert inf.extent_pages == orc.usable_pages
     assert inf.live_pages == orc.live_pages
-    bits = pool.bitmap(orc.extent)
-    assert (bits == orc.live[:orc.extent]).all()
-    owners = pool.owners(orc.extent)
-    want = np.full(orc.extent, -1, dtype=np.int32)
-    for pg, cell in orc.owner.items():
-        want[pg] = cell
-    assert (owners == want).all()
+    assert (pool.bitmap() == orc.bitmap()).all()
+    assert (pool.owners() == orc.owner_array()).all()
     for s in slots:
         for l in range(orc.num_layers):
             assert pool.block_table(s, l) == orc.bt.get((s, l), []), (s, l)
@@ -61,7 +57,7 @@ def test_pool_ops_match_oracle_bit_exact(rt):
     orc = oracle_for(pool)
     rng = random.Random(17)
     slots = list(range(rt.max_slots))
-    dropped = 0
+    dropped = set()
     for step in range(300):
         r = rng.random()
         if r < 0.45:
@@ -86,19 +82,22 @@ def test_pool_ops_match_oracle_bit_exact(rt):
             hi = rng.randrange(lo + 1, 3)
             pool.release(s, lo, hi)
             orc.release(s, lo, hi)
-        elif r < 0.87 and dropped < 2:
-            pool.drop_layers(dropped, dropped + 1)
-            orc.drop(1)
-            dropped += 1
-        elif dropped > 0:
-            want = orc.restore(1)
+        elif r < 0.87:
+            l = rng.randrange(2)
+            if l not in dropped:
+                pool.drop_layers(l, l + 1)
+                orc.drop(l, l + 1)
+                dropped.add(l)
+        elif dropped:
+            l = rng.choice(sorted(dropped))
+            want = orc.restore(l, l + 1)
             if want < 0:
                 with pytest.raises(runtime.Refused):
-                    pool.restore_begin(dropped - 1, dropped)
+                    pool.restore_begin(l, l + 1)
             else:
-                assert pool.restore_begin(dropped - 1, dropped) == want
-                pool.restore_complete(dropped - 1, dropped)
-                dropped -= 1
+                assert pool.restore_begin(l, l + 1) == want
+                pool.restore_complete(l, l + 1)
+                dropped.discard(l)
         assert_same_state(pool, orc, slots)
     pool.close()
 
@@ -149,7 +148,7 @@ def test_append_exchange_compaction_bytes(rt):
     kk, vv = device_gather(a, 2, 0, ctx, 1, 64)
     assert (kk == k.view(torch.int16).numpy().view(np.uint16)).all()
     assert (vv == v.view(torch.int16).numpy().view(np.uint16)).all()
-    assert max(a.block_table(2, 0)) >= 192  # lives in the dropped slab's pages
+    assert max(a.block_table(2, 0)) >= 256  # lives in layer 1's dropped slab (pages 256..319)
     # exchange a -> b (two chunks), byte exact
     assert b.grow([(7, 0, 1, pages)])
     runtime.copy_pages(b, a, [(2, 7, 0, 1, pages, 0, 2), (2, 7, 0, 1, pages, 2, pages)])
