@@ -33,6 +33,15 @@ from .traceio import synth_burst
 from .transfer import SlotTable, TransferEngine
 
 
+def _span_ms(done) -> float:
+    """Device time of completed submissions (each (start, end) event pair once)."""
+    seen = {}
+    for p in done:
+        if p.start_event is not None:
+            seen[id(p.event)] = p.start_event.elapsed_time(p.event)
+    return sum(seen.values())
+
+
 @dataclass
 class CycleReport:
     bytes_kv_exchange: int = 0
@@ -75,7 +84,6 @@ class OverloadCycle:
         self.pools = {i: inst.pool for i, inst in self.instances.items()}
         self.slots = {i: SlotTable(runtimes[i].max_slots) for i in self.instances}
         self.te = TransferEngine(self.pools, self.slots, timing=True)
-        self._fill_weights()
         trace = synth_burst(10_000.0, 4.0, 16.0, 0.0, 10_000.0, input_mean, 373, seed=seed)
         self.tokens: dict[int, int] = {}
         self.home: dict[int, int] = {}
@@ -96,11 +104,15 @@ class OverloadCycle:
             self.home[rid] = iid
             self._admit(rid)
         self.transient = set(sorted(self.tokens)[1::2])
-        for iid, pool in self.pools.items():  # synthetic KV content on every mapped page
+        for iid, pool in self.pools.items():
+            # synthetic KV content on the head pages (the residents live there;
+            # the slab pages alias the weights and are filled next)
             g = torch.Generator(device=f"cuda:{pool.rt.device}").manual_seed(77 + iid)
-            kv = pool.kv_bytes().view(torch.int32)
+            head = pool.info().extent_pages * pool.page_bytes
+            kv = pool.kv_bytes()[:head].view(torch.int32)
             kv.copy_(torch.randint(-2**31, 2**31 - 1, (kv.numel(),), dtype=torch.int32,
                                    device=kv.device, generator=g))
+        self._fill_weights()
         torch.cuda.synchronize()
         self.pause_merged = False  # set True to stop after the exchange (see resume())
         self._paused = None
@@ -122,7 +134,9 @@ class OverloadCycle:
         for l in range(self.L):
             for iid, pool in self.pools.items():
                 g = torch.Generator(device=f"cuda:{pool.rt.device}").manual_seed(1000 + l)
-                w = pool.weight_bytes(l)[:2 * n].view(torch.bfloat16)
+                slab = pool.weight_bytes(l)
+                slab[2 * n:].zero_()  # 2 MiB rounding tail
+                w = slab[:2 * n].view(torch.bfloat16)
                 w.copy_((torch.randn(n, device=w.device, generator=g) * 0.02).to(torch.bfloat16))
         torch.cuda.synchronize()
 
@@ -215,12 +229,11 @@ class OverloadCycle:
                                       tid_start=tid)
                 tid += len(tasks)
                 self.te.register_exchange(tasks, old_map, g.stage_layer_map, toks)
-                for t in tasks:
-                    self.te.submit(t)
+                self.te.submit_many(tasks)
                 rep.n_tasks += len(tasks)
         done = self.te.drain()
         rep.bytes_kv_exchange = sum(p.bytes_moved for p in done)
-        rep.kv_kernel_ms += sum(p.start_event.elapsed_time(p.event) for p in done)
+        rep.kv_kernel_ms += _span_ms(done)
         self.te.finish_flow_sources()
         ev["exch"].record(st)
         self.merged = live
@@ -282,7 +295,7 @@ class OverloadCycle:
             rep.n_tasks += len(tasks)
             done = self.te.drain()
             rep.bytes_param += sum(p.bytes_moved for p in done)
-            rep.param_kernel_ms += sum(p.start_event.elapsed_time(p.event) for p in done)
+            rep.param_kernel_ms += _span_ms(done)
             for iid, rngs in missing.items():
                 for rng in rngs:
                     memory.complete_restore(self.instances[iid], rng)
@@ -309,12 +322,11 @@ class OverloadCycle:
                     tid += 1
                 self.te.register_chunked_kv(chunks, (lo, hi), {rid: self.tokens[rid]})
                 cons_tasks += chunks
-        for t in cons_tasks:
-            self.te.submit(t)
+        self.te.submit_many(cons_tasks)
         rep.n_tasks += len(cons_tasks)
         done = self.te.drain()
         rep.bytes_kv_consolidate = sum(p.bytes_moved for p in done)
-        rep.kv_kernel_ms += sum(p.start_event.elapsed_time(p.event) for p in done)
+        rep.kv_kernel_ms += _span_ms(done)
         self.te.finish_flow_sources()
         for rid, tok in self.tokens.items():
             if rid in self.transient:

@@ -176,6 +176,57 @@ class TransferEngine:
         self.stats.tasks += 1
         self.pending.append(Pending(task, ev, cb, moved, start))
 
+    def submit_many(self, tasks: list[TransferTask], cb: Optional[Callable] = None) -> None:
+        """Submit a burst of KV / parameter tasks on the bulk stream with one
+        block-table growth per destination pool, one page-copy launch per
+        (src, dst) pair (up to 256 moves per launch) and one completion event
+        for the burst.  Used when nothing needs per-chunk completion times
+        (exchange right after a drop, restore pulls, consolidation)."""
+        torch = self.torch
+        stream = self.bulk
+        start = torch.cuda.Event(enable_timing=True) if self.timing else None
+        if start is not None:
+            start.record(stream)
+        grows: dict[int, list] = {}
+        for t in tasks:
+            if t.kind is TaskKind.KVCACHE_CHUNK:
+                fl = self.flows[self.chunk_of[t.tid][0]]
+                if not fl.grown:
+                    if fl.npages:
+                        grows.setdefault(fl.dst, []).append(
+                            (self.slots[fl.dst].get(fl.rid), fl.layers[0], fl.layers[1],
+                             fl.npages))
+                    fl.grown = True
+        for dst, reqs in grows.items():
+            if not self.pools[dst].grow(reqs, stream=stream):
+                raise runtime.DeviceError(f"instance {dst} out of KV pages for an exchange")
+        pairs: dict[tuple[int, int], list] = {}
+        moved = {}
+        for t in tasks:
+            if t.kind is TaskKind.KVCACHE_CHUNK:
+                key, idx = self.chunk_of.pop(t.tid)
+                fl = self.flows[key]
+                P = fl.total
+                a, b = idx * P // fl.n_chunks, (idx + 1) * P // fl.n_chunks
+                if b > a:
+                    pairs.setdefault((fl.src, fl.dst), []).append(
+                        (self.slots[fl.src].get(fl.rid), self.slots[fl.dst].get(fl.rid),
+                         fl.layers[0], fl.layers[1], fl.npages, a, b))
+                moved[t.tid] = (b - a) * self.pools[fl.src].page_bytes
+                self.stats.kv_bytes += moved[t.tid]
+            elif t.kind is TaskKind.PARAM_SHARD:
+                moved[t.tid] = self._run_param_shard(t, stream)
+                self.stats.param_bytes += moved[t.tid]
+            else:
+                raise ValueError("activation tasks go through submit_activation")
+        for (s, d), moves in pairs.items():
+            runtime.copy_pages(self.pools[d], self.pools[s], moves, stream=stream)
+        ev = torch.cuda.Event(enable_timing=self.timing)
+        ev.record(stream)
+        self.stats.tasks += len(tasks)
+        for t in tasks:
+            self.pending.append(Pending(t, ev, cb, moved[t.tid], start))
+
     def submit_activation(self, task: TransferTask, dst_ptr: int, src_ptr: int,
                           cb: Optional[Callable] = None) -> None:
         runtime.copy_bytes(dst_ptr, src_ptr, task.size_bytes, stream=self.urgent)
@@ -240,10 +291,9 @@ class TransferEngine:
             p.event.synchronize()
             self.pending.pop(0)
             if p.task.kind is TaskKind.KVCACHE_CHUNK:
-                for key, fl in self.flows.items():
-                    if key == (p.task.rid, p.task.src, p.task.dst):
-                        fl.done_chunks += 1
-                        break
+                fl = self.flows.get((p.task.rid, p.task.src, p.task.dst))
+                if fl is not None:
+                    fl.done_chunks += 1
             out.append(p)
             if p.cb is not None:
                 p.cb(p.task)
