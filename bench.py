@@ -167,9 +167,9 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
 
     def one_token():
         for pool, lo, hi, q, slots, ctx, mx, out, ws in work:
-            for l in range(lo, hi):
+            for l in range(lo, hi):  # one plan per decode step, reused by every layer
                 runtime.paged_decode(pool, l, q, slots, ctx, mx, out, ws, 128 ** -0.5,
-                                     max_splits=16, stream=st)
+                                     max_splits=16, reuse_plan=l > lo, stream=st)
     for _ in range(3):
         one_token()
     torch.cuda.synchronize()
@@ -180,7 +180,8 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
     b.record(st)
     b.synchronize()
     ms = a.elapsed_time(b) / iters
-    launches = sum(hi - lo for _, lo, hi, *_ in work) * 3  # plan + attention + combine
+    # per member: one plan, then attention + combine per layer
+    launches = sum(1 + 2 * (hi - lo) for _, lo, hi, *_ in work)
     gbs = algo_bytes / (ms / 1e3) / 1e9
     return {"value": round(nres / (ms / 1e3), 1), "unit": "tok/s",
             "tokens_per_step": nres, "ms_per_token_step": round(ms, 4),

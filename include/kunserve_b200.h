@@ -176,12 +176,17 @@ int kb_kv_append(kb_pool* pool, int32_t layer, uint64_t k, uint64_t v,
 /* Decode: q [nseq][n_q_heads][head_dim] bf16, one query token per sequence
  * attending to ctx_lens[i] cached tokens of slot slots[i] (including its
  * own, already appended).  out [nseq][n_q_heads][head_dim] bf16.
- * workspace: kb_decode_workspace_bytes() bytes of device scratch. */
+ * workspace: kb_decode_workspace_bytes() bytes of device scratch.  The work
+ * plan (KV splits, item order) depends only on ctx_lens: with
+ * flags & KB_DECODE_REUSE_PLAN the plan already in `workspace` (from an
+ * earlier call with the same ctx_lens, e.g. the previous layer of the same
+ * decode step) is reused and no plan kernel runs. */
+#define KB_DECODE_REUSE_PLAN 1
 int64_t kb_decode_workspace_bytes(int32_t nseq, int32_t n_q_heads, int32_t max_splits);
 int kb_paged_decode(kb_pool* pool, int32_t layer, int32_t n_q_heads, uint64_t q,
                     uint64_t slots, uint64_t ctx_lens, int32_t nseq, int32_t max_ctx,
                     float scale, uint64_t out, uint64_t workspace, int32_t max_splits,
-                    uintptr_t stream);
+                    int32_t flags, uintptr_t stream);
 /* Chunked prefill: for sequence i, q rows [q_off[i], q_off[i]+q_len[i]) are
  * positions [prefix[i], prefix[i]+q_len[i]) of slot slots[i]; they attend
  * causally over pages [0, prefix[i]+q_len[i]) (the chunk's K/V must be

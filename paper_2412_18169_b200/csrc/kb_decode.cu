@@ -6,12 +6,16 @@
 // (pkg/src/dropsim/costmodel.py:50-57).  Parity is against the fp32 CPU
 // restatement oracle/attention.py with max-abs <= 2e-2, mean-rel <= 1e-3.
 //
-// Work split: one CTA per (sequence, kv head, KV split); the split's partial
-// (o, m, l) go to a workspace and a combine kernel merges them.
+// Three launches per layer: plan (work items), the persistent tcgen05
+// kernel (kb_decode_tc.cuh), and the split-KV combine.
 #include "kb_common.cuh"
 #include "kb_decode_tc.cuh"
 
 namespace kb {
+
+constexpr int kPlanThreads = 1024;
+constexpr int kLenBuckets = 1024;
+constexpr int kItemsPerCta = 4;  // target work items per persistent CTA
 
 // Split-KV combine: one CTA per (sequence, q head), thread = head_dim lane.
 __global__ void decode_combine_kernel(const float* __restrict__ part_o,
@@ -21,6 +25,7 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
   const int sh = blockIdx.x;  // seq * Hq + head
   const int seq = sh / Hq;
   const int ns = nsplit_of[seq];
+  if (ns == 1) return;  // the attention kernel wrote this row directly
   const float* ml = part_ml + (int64_t)sh * max_splits * 2;
   float mstar = -INFINITY;
   for (int s = 0; s < ns; ++s) mstar = fmaxf(mstar, ml[2 * s]);
@@ -34,18 +39,77 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
   out[(int64_t)sh * 128 + threadIdx.x] = __float2bfloat16(l > 0.f ? o / l : 0.f);
 }
 
-// Per-sequence split count: pages of the sequence spread over at most
-// max_splits CTAs, at least `min_pages` pages each.
-__global__ void decode_plan_kernel(const int32_t* __restrict__ ctx, int nseq, int B,
-                                   int max_splits, int min_pages, int32_t* __restrict__ nsplit_of) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nseq) return;
-  int pages = (ctx[i] + B - 1) / B;
-  int s = (pages + min_pages - 1) / min_pages;
-  if (s > max_splits) s = max_splits;
-  if (s < 1) s = 1;
-  nsplit_of[i] = s;
+// Work items: sequence i is cut into s_i = clamp(ceil(tiles_i / T), 1,
+// max_splits) splits per kv head, T chosen so the items spread ~kItemsPerCta
+// per persistent CTA; items are bucket-sorted longest first.  Sequences with
+// no context get neutral partials here and no item.
+__global__ void __launch_bounds__(kPlanThreads)
+decode_plan_kernel(const int32_t* __restrict__ ctx, int nseq, int Hkv, int Hq, int max_splits,
+                   int grid_ctas, int min_tiles, int32_t* __restrict__ nsplit_of,
+                   DecodeItem* __restrict__ items, int32_t* __restrict__ n_items,
+                   float* __restrict__ part_ml) {
+  __shared__ int hist[kLenBuckets];
+  __shared__ int cursor[kLenBuckets];
+  __shared__ unsigned long long total_tiles;
+  __shared__ int T;
+  const int tid = threadIdx.x;
+  if (tid == 0) total_tiles = 0;
+  for (int b = tid; b < kLenBuckets; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  unsigned long long local = 0;
+  for (int i = tid; i < nseq; i += blockDim.x) local += (ctx[i] + kTileTok - 1) / kTileTok;
+  atomicAdd(&total_tiles, local);
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned long long work = total_tiles * (unsigned long long)Hkv;
+    const unsigned long long per = (work + (unsigned long long)grid_ctas * kItemsPerCta - 1) /
+                                   ((unsigned long long)grid_ctas * kItemsPerCta);
+    T = (int)(per > (unsigned long long)min_tiles ? per : min_tiles);
+  }
+  __syncthreads();
+  auto splits_of = [&](int tiles) {
+    int s = (tiles + T - 1) / T;
+    return s < 1 ? 1 : (s > max_splits ? max_splits : s);
+  };
+  for (int i = tid; i < nseq; i += blockDim.x) {
+    const int tiles = (ctx[i] + kTileTok - 1) / kTileTok;
+    const int s = splits_of(tiles);
+    // no context: no item; the combine kernel writes a zero row (0 splits)
+    nsplit_of[i] = tiles == 0 ? 0 : s;
+    if (tiles == 0) continue;
+    for (int k = 0; k < s; ++k) {
+      const int len = (k + 1) * tiles / s - k * tiles / s;
+      atomicAdd(&hist[kLenBuckets - 1 - min(len, kLenBuckets - 1)], Hkv);
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the (descending-length) histogram
+  if (tid == 0) {
+    int run = 0;
+    for (int b = 0; b < kLenBuckets; ++b) {
+      cursor[b] = run;
+      run += hist[b];
+    }
+    *n_items = run;
+  }
+  __syncthreads();
+  for (int i = tid; i < nseq; i += blockDim.x) {
+    const int tiles = (ctx[i] + kTileTok - 1) / kTileTok;
+    if (tiles == 0) continue;
+    const int s = splits_of(tiles);
+    for (int k = 0; k < s; ++k) {
+      const int beg = k * tiles / s, len = (k + 1) * tiles / s - beg;
+      const int b = kLenBuckets - 1 - min(len, kLenBuckets - 1);
+      for (int h = 0; h < Hkv; ++h) {
+        const int pos = atomicAdd(&cursor[b], 1);
+        items[pos] = DecodeItem{i, h, k, beg, len, {0, 0, 0}};
+      }
+    }
+  }
 }
+
+static int64_t ws_part_o(int64_t sh) { return round_up(sh * 128 * 4, 256); }
+static int64_t ws_part_ml(int64_t sh) { return round_up(sh * 2 * 4, 256); }
 
 }  // namespace kb
 
@@ -53,13 +117,15 @@ using namespace kb;
 
 extern "C" int64_t kb_decode_workspace_bytes(int32_t nseq, int32_t n_q_heads, int32_t max_splits) {
   const int64_t sh = (int64_t)nseq * n_q_heads * max_splits;
-  return round_up(sh * 128 * 4, 256) + round_up(sh * 2 * 4, 256) + round_up((int64_t)nseq * 4, 256);
+  // items: at most nseq * n_kv_heads * max_splits <= sh
+  return ws_part_o(sh) + ws_part_ml(sh) + round_up((int64_t)nseq * 4, 256) +
+         round_up(sh * (int64_t)sizeof(DecodeItem), 256) + 256;
 }
 
 extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uint64_t q,
                                uint64_t slots, uint64_t ctx_lens, int32_t nseq, int32_t max_ctx,
                                float scale, uint64_t out, uint64_t workspace, int32_t max_splits,
-                               uintptr_t stream) {
+                               int32_t flags, uintptr_t stream) {
   if (!p) return fail(KB_EINVAL, "null pool");
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
   if (p->m.head_dim != 128) return fail(KB_EINVAL, "head_dim must be 128");
@@ -68,24 +134,29 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   if (layer < 0 || layer >= p->m.num_layers) return fail(KB_EINVAL, "bad layer");
   if (max_splits < 1 || max_splits > 64) return fail(KB_EINVAL, "max_splits out of range");
   if (nseq <= 0) return KB_OK;
+  (void)max_ctx;
   KB_RT(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t sh = (int64_t)nseq * n_q_heads * max_splits;
-  float* part_o = reinterpret_cast<float*>(workspace);
-  float* part_ml = reinterpret_cast<float*>(workspace + round_up(sh * 128 * 4, 256));
-  int32_t* nsplit = reinterpret_cast<int32_t*>(workspace + round_up(sh * 128 * 4, 256) +
-                                               round_up(sh * 2 * 4, 256));
-  // Aim for >= 2 waves of CTAs over 148 SMs; a split covers >= 2 tiles.
-  const int64_t tiles_max = ceil_div(max_ctx, 128);
-  int64_t base_ctas = (int64_t)nseq * Hkv;
-  int min_tiles = (int)ceil_div(tiles_max * base_ctas, 148 * 4);
-  if (min_tiles < 2) min_tiles = 2;
-  const int min_pages = min_tiles * (128 / B);
-  decode_plan_kernel<<<(int)ceil_div(nseq, 128), 128, 0, st>>>(
-      reinterpret_cast<const int32_t*>(ctx_lens), nseq, B, max_splits, min_pages, nsplit);
-  KB_LAUNCH_CHECK();
-  int rc = launch_decode_tc(p, layer, n_q_heads, q, slots, ctx_lens, nseq, max_ctx, scale,
-                            part_o, part_ml, nsplit, max_splits, st);
+  char* ws = reinterpret_cast<char*>(workspace);
+  float* part_o = reinterpret_cast<float*>(ws);
+  float* part_ml = reinterpret_cast<float*>(ws + ws_part_o(sh));
+  int32_t* nsplit = reinterpret_cast<int32_t*>(ws + ws_part_o(sh) + ws_part_ml(sh));
+  DecodeItem* items = reinterpret_cast<DecodeItem*>(ws + ws_part_o(sh) + ws_part_ml(sh) +
+                                                     round_up((int64_t)nseq * 4, 256));
+  int32_t* n_items = reinterpret_cast<int32_t*>(
+      reinterpret_cast<char*>(items) + round_up(sh * (int64_t)sizeof(DecodeItem), 256));
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device);
+  const int grid = dev_sms;  // persistent: one CTA per SM (the kernel needs ~210 KB smem)
+  if (!(flags & KB_DECODE_REUSE_PLAN)) {
+    decode_plan_kernel<<<1, kPlanThreads, 0, st>>>(reinterpret_cast<const int32_t*>(ctx_lens),
+                                                   nseq, Hkv, n_q_heads, max_splits, grid, 2,
+                                                   nsplit, items, n_items, part_ml);
+    KB_LAUNCH_CHECK();
+  }
+  int rc = launch_decode_tc(p, layer, n_q_heads, q, slots, ctx_lens, grid, scale, part_o, part_ml,
+                            items, n_items, nsplit, out, max_splits, st);
   if (rc) return rc;
   decode_combine_kernel<<<nseq * n_q_heads, 128, 0, st>>>(part_o, part_ml, nsplit,
                                                           reinterpret_cast<__nv_bfloat16*>(out),

@@ -91,7 +91,7 @@ _sigs = {
     "kb_kv_append": (C.c_int, [_P, C.c_int32, _U, _U, _U, _U, C.c_int32, _S]),
     "kb_decode_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "kb_paged_decode": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, C.c_int32, C.c_int32,
-                                  C.c_float, _U, _U, C.c_int32, _S]),
+                                  C.c_float, _U, _U, C.c_int32, C.c_int32, _S]),
     "kb_paged_prefill": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, _U, _U, C.c_int32,
                                    C.c_int32, C.c_float, _U, _S]),
 }
@@ -347,13 +347,20 @@ def decode_workspace_bytes(nseq: int, n_q_heads: int, max_splits: int) -> int:
     return int(_lib.kb_decode_workspace_bytes(nseq, n_q_heads, max_splits))
 
 
+DECODE_REUSE_PLAN = 1
+
+
 def paged_decode(pool: DevicePool, layer: int, q, slots, ctx_lens, max_ctx: int, out,
-                 workspace, scale: float, max_splits: int = 16, stream=None) -> None:
-    """q/out: [nseq, n_q_heads, 128] bf16; slots/ctx_lens int32 [nseq] (device)."""
+                 workspace, scale: float, max_splits: int = 16, reuse_plan: bool = False,
+                 stream=None) -> None:
+    """q/out: [nseq, n_q_heads, 128] bf16; slots/ctx_lens int32 [nseq] (device).
+    reuse_plan: the workspace already holds the plan for these ctx_lens (a
+    previous layer of the same decode step)."""
+    flags = DECODE_REUSE_PLAN if reuse_plan else 0
     _check(_lib.kb_paged_decode(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
                                 ctx_lens.data_ptr(), q.shape[0], max_ctx, scale,
-                                out.data_ptr(), workspace.data_ptr(), max_splits,
-                                _stream(stream)), launches=3)
+                                out.data_ptr(), workspace.data_ptr(), max_splits, flags,
+                                _stream(stream)), launches=2 if reuse_plan else 3)
 
 
 def paged_prefill(pool: DevicePool, layer: int, q, slots, q_off, q_len, prefix, max_q_len: int,
