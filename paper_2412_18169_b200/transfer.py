@@ -269,16 +269,19 @@ class TransferEngine:
         return task.size_bytes
 
     def finish_flow_sources(self) -> list[KVFlow]:
-        """Release source pages of every flow whose chunks all landed."""
+        """Release source pages of every flow whose chunks all landed: one
+        release launch per (source pool, layer range)."""
         done = []
+        batches: dict[tuple[int, tuple[int, int]], list[int]] = {}
         for key, fl in list(self.flows.items()):
             if fl.done_chunks == fl.n_chunks:
                 slot = self.slots[fl.src].of.get(fl.rid)
                 if slot is not None:
-                    self.pools[fl.src].release([slot], fl.layers[0], fl.layers[1],
-                                               stream=self.bulk)
+                    batches.setdefault((fl.src, fl.layers), []).append(slot)
                 del self.flows[key]
                 done.append(fl)
+        for (src, (lo, hi)), slots in batches.items():
+            self.pools[src].release(slots, lo, hi, stream=self.bulk)
         return done
 
     def poll(self, block: bool = False) -> list[Pending]:
