@@ -107,8 +107,9 @@ class DeviceError(RuntimeError):
     pass
 
 
-class Refused(Exception):
-    """Expected refusal (KB_REFUSED): out of pages / restore cannot vacate."""
+class Refused(ValueError):
+    """Expected refusal (KB_REFUSED): out of pages / restore cannot vacate.
+    A ValueError like the reference's "restore blocked" (memory.py:193-196)."""
 
 
 # Kernel launches issued by this process through the library (the bench's
