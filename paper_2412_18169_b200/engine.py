@@ -354,14 +354,33 @@ class Engine:
         L = self.model.num_layers
         spans = [grun.group.stage_layer_map[i][1] - grun.group.stage_layer_map[i][0]
                  for i in members]
-        costs = [batch_cost(mb.chunks, self.coeffs) for mb in mbs]
-        times = [[max(1, int(round(c * 1_000_000 * span / L))) for c in costs] for span in spans]
+        times = self._stage_times(grun, mbs, spans)
         act_ready = [[self.now if s == 0 else None for _ in mbs] for s in range(len(members))]
         grun.rstate = RoundState(grun.round_no, mbs, members, times, act_ready,
                                  [0] * len(members), [self.now] * len(members))
         self.log("ROUND", group=gid, rnd=grun.round_no, n_mb=len(mbs), prefill=len(items),
                  decode=len(decode))
         self._try_start_stage(gid, 0)
+
+    def _stage_times(self, grun: GroupRun, mbs: list[Microbatch], spans: list[int]) -> list:
+        """[stage][mb] execution us: the cost model scaled by each stage's
+        layer share (engine.py:389-397).  serving.DeviceEngine measures them."""
+        L = self.model.num_layers
+        costs = [batch_cost(mb.chunks, self.coeffs) for mb in mbs]
+        return [[max(1, int(round(c * 1_000_000 * span / L))) for c in costs] for span in spans]
+
+    # device hooks (no-ops in model mode; serving.DeviceEngine implements them)
+    def _on_exchange_planned(self, tasks, old_map, new_map, tokens) -> None:
+        pass
+
+    def _on_params_planned(self, tasks, fetch: bool) -> None:
+        pass
+
+    def _on_consolidation_planned(self, rid: int, peer: int, home: int, layers, tasks) -> None:
+        pass
+
+    def _on_consolidated(self, rid: int, peers) -> None:
+        pass
 
     def _try_start_stage(self, gid: int, s: int) -> None:
         grun = self.groups.get(gid)
@@ -615,6 +634,7 @@ class Engine:
                 tasks = plan_exchange(toks, dict(key), grun.group.stage_layer_map, L, kvbpt,
                                       chunk, tid_start=self._tid + 1)
                 self._tid += len(tasks)
+                self._on_exchange_planned(tasks, dict(key), grun.group.stage_layer_map, toks)
                 if tasks:
                     self.log("EXCHANGE", group=gid, tasks=len(tasks),
                              bytes=sum(t.size_bytes for t in tasks))
@@ -671,6 +691,7 @@ class Engine:
                 self.model.bytes_per_layer, self._exchange_chunk_bytes(),
                 tid_start=self._tid + 1)
             self._tid += len(fetch_tasks)
+            self._on_params_planned(fetch_tasks, fetch=True)
             for t in fetch_tasks:
                 if t.src != HOST and t.layers:
                     protected.update((t.src, l) for l in range(*t.layers))
@@ -967,6 +988,7 @@ class Engine:
         tasks = plan_restore_transfers(flat, holders, self.model.bytes_per_layer, chunk,
                                        tid_start=self._tid + 1)
         self._tid += len(tasks)
+        self._on_params_planned(tasks, fetch=False)
         left: dict[int, int] = {}
         for t in tasks:
             left[t.dst] = left.get(t.dst, 0) + 1
@@ -1048,11 +1070,14 @@ class Engine:
             st["left"] = 0
             for iid in sorted(st["peers"]):
                 left = st["peers"][iid]
+                tasks = []
                 while left > 0:
                     take = min(chunk, left)
                     left -= take
-                    task = TransferTask(self._next_tid(), TaskKind.KVCACHE_CHUNK, iid,
-                                        st["home"], take, rid=rid)
+                    tasks.append(TransferTask(self._next_tid(), TaskKind.KVCACHE_CHUNK, iid,
+                                              st["home"], take, rid=rid))
+                self._on_consolidation_planned(rid, iid, st["home"], st["layers"][iid], tasks)
+                for task in tasks:
                     st["left"] += 1
                     self.transition_tasks += 1
                     self.enqueue_task(task, lambda t, when, r=rid:
@@ -1064,6 +1089,7 @@ class Engine:
         st["left"] -= 1
         if st["left"] > 0:
             return
+        self._on_consolidated(rid, sorted(st["peers"]))
         for iid in sorted(st["peers"]):
             self.instances[iid].kv.free(rid)
         del self.consolidating[rid]

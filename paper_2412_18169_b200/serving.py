@@ -1,0 +1,362 @@
+"""Device-backed serving: the reference's engine driving real B200 pools.
+
+`DeviceEngine` keeps every scheduling decision of engine.Engine (itself a
+byte-for-byte mirror of the reference's event loop, pkg/src/dropsim/engine.py)
+and replaces the emulated device with real work:
+
+  * every instance is a VMM slab pool with a paged KV pool
+    (memory.build_instance(device=...)); drops / restores are device page
+    remaps and compactions;
+  * KV token allocations (group_alloc, engine.py:214-225) grow the members'
+    block tables on the device; frees release pages;
+  * every TransferTask executes on the GPU when its link starts it
+    (transfer.TransferEngine): KV chunks are page copies between pools,
+    parameter shards are slab pulls, activations are byte copies;
+  * stage execution times are MEASURED: each microbatch's stage runs the
+    member's Llama layers on its pool (cuBLAS GEMMs + this repo's kv_append,
+    paged prefill and paged decode kernels over the pool's block tables),
+    timed with CUDA events, and those times drive the event clock instead of
+    the cost model (engine.py:389-397).
+Link times (activations, KV exchange, restores) stay on the reference's link
+model with the configured bandwidth (NVLink-5 in bench.py), because the
+replicas of a one-GPU run share one HBM rather than an NVLink.
+Supported policies: kunserve and recompute (the others move KV to host /
+between groups outside the drop path).
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Optional
+
+from . import runtime
+from .engine import Engine, GroupRun
+from .exchange import TaskKind, TransferTask
+from .transfer import SlotTable, TransferEngine
+
+
+class LayerWeights:
+    """bf16 views of one layer's slab: [Wqkv | Wo | Wgate_up | Wdown | norm1 | norm2],
+    each stored as x @ W ([in, out], row-major)."""
+
+    def __init__(self, slab, shape):
+        import torch
+        H, Hq, Hkv, d, F = shape.hidden, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, shape.ffn
+        w = slab.view(torch.bfloat16)
+        off = 0
+
+        def take(n, dims):
+            nonlocal off
+            t = w[off:off + n].view(*dims)
+            off += n
+            return t
+        self.wqkv = take(H * (Hq + 2 * Hkv) * d, (H, (Hq + 2 * Hkv) * d))
+        self.wo = take(Hq * d * H, (Hq * d, H))
+        self.wgu = take(H * 2 * F, (H, 2 * F))
+        self.wd = take(F * H, (F, H))
+        self.n1 = take(H, (H,))
+        self.n2 = take(H, (H,))
+
+
+def init_weights(pool, shape, layers, seed: int = 1000) -> None:
+    """Identical replicas: layer l draws from seed + l (bf16 randn x 0.02,
+    norms 1, 2 MiB rounding tail zero)."""
+    import torch
+    n = shape.layer_weight_bytes // 2
+    for l in layers:
+        slab = pool.weight_bytes(l)
+        slab[2 * n:].zero_()
+        g = torch.Generator(device=slab.device).manual_seed(seed + l)
+        w = slab[:2 * n].view(torch.bfloat16)
+        w.copy_((torch.randn(n, device=w.device, generator=g) * 0.02).to(torch.bfloat16))
+        lw = LayerWeights(slab, shape)
+        lw.n1.fill_(1.0)
+        lw.n2.fill_(1.0)
+
+
+class StageRunner:
+    """Runs layers [lo, hi) of one pool for a microbatch of prefill chunks
+    and decode tokens."""
+
+    def __init__(self, pool, shape, max_seqs: int = 1024, max_splits: int = 16):
+        import torch
+        self.torch = torch
+        self.pool = pool
+        self.shape = shape
+        self.max_splits = max_splits
+        self.ws = torch.empty(runtime.decode_workspace_bytes(max_seqs, shape.n_q_heads, max_splits),
+                              dtype=torch.uint8, device=f"cuda:{pool.rt.device}")
+        self.max_seqs = max_seqs
+        self.scale = shape.head_dim ** -0.5
+
+    def _weights(self, l):
+        return LayerWeights(self.pool.weight_bytes(l), self.shape)
+
+    @staticmethod
+    def _rmsnorm(x, w, torch):
+        xf = x.float()
+        return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5)).to(x.dtype) * w
+
+    def run(self, lo: int, hi: int, x, batch: dict):
+        torch = self.torch
+        sh = self.shape
+        Hq, Hkv, d = sh.n_q_heads, sh.n_kv_heads, sh.head_dim
+        n = x.shape[0]
+        for l in range(lo, hi):
+            w = self._weights(l)
+            h = self._rmsnorm(x, w.n1, torch)
+            qkv = h @ w.wqkv
+            q = qkv[:, :Hq * d].reshape(n, Hq, d)
+            k = qkv[:, Hq * d:(Hq + Hkv) * d].reshape(n, Hkv, d).contiguous()
+            v = qkv[:, (Hq + Hkv) * d:].reshape(n, Hkv, d).contiguous()
+            runtime.kv_append(self.pool, l, k, v, batch["slots"], batch["pos"])
+            o = torch.empty((n, Hq, d), dtype=x.dtype, device=x.device)
+            if batch["np"]:
+                qp = q.index_select(0, batch["p_rows"]).contiguous()
+                op = torch.empty_like(qp)
+                runtime.paged_prefill(self.pool, l, qp, batch["p_slots"], batch["p_off"],
+                                      batch["p_len"], batch["p_prefix"], batch["p_max"], op,
+                                      self.scale)
+                o.index_copy_(0, batch["p_rows"], op)
+            if batch["nd"]:
+                qd = q.index_select(0, batch["d_rows"]).contiguous()
+                od = torch.empty_like(qd)
+                runtime.paged_decode(self.pool, l, qd, batch["d_slots"], batch["d_ctx"],
+                                     batch["d_max"], od, self.ws, self.scale,
+                                     max_splits=self.max_splits, reuse_plan=l > lo)
+                o.index_copy_(0, batch["d_rows"], od)
+            x = x + o.reshape(n, Hq * d) @ w.wo
+            h2 = self._rmsnorm(x, w.n2, torch)
+            gu = h2 @ w.wgu
+            F = sh.ffn
+            x = x + (torch.nn.functional.silu(gu[:, :F]) * gu[:, F:]) @ w.wd
+        return x
+
+
+class DeviceEngine(Engine):
+    def __init__(self, cfg, trace, policy: Optional[str] = None, seed: int = 0,
+                 runtimes: Optional[dict] = None, max_seqs: int = 512):
+        import torch
+        self.torch = torch
+        pol = policy or cfg.policy.kind
+        if pol not in ("kunserve", "recompute"):
+            raise ValueError(f"device mode supports kunserve and recompute, not {pol}")
+        if runtimes is None:
+            runtimes = {d: runtime.Runtime(d, max_slots=cfg.device.max_slots,
+                                           max_pages_per_seq=cfg.device.max_pages_per_seq)
+                        for d in cfg.device.devices}
+        self.runtimes = runtimes
+        super().__init__(cfg, trace, policy=policy, seed=seed, runtimes=runtimes)
+        self.shape = cfg.device.shape
+        self.B = self.shape.block_tokens
+        self.pools = {i: inst.pool for i, inst in self.instances.items()}
+        self.slots = {i: SlotTable(cfg.device.max_slots) for i in self.instances}
+        self.te = TransferEngine(self.pools, self.slots)
+        self.transfer_hook = self._run_task
+        for iid, inst in self.instances.items():
+            init_weights(inst.pool, self.shape, inst.table.layers_held())
+        self.runners = {iid: StageRunner(p, self.shape, max_seqs=max_seqs)
+                        for iid, p in self.pools.items()}
+        self.emb = {}
+        for d in set(cfg.device.devices):
+            g = torch.Generator(device=f"cuda:{d}").manual_seed(7)
+            self.emb[d] = torch.randn((self.shape.vocab, self.shape.hidden), device=f"cuda:{d}",
+                                      generator=g).to(torch.bfloat16)
+        self.acts: dict = {}
+        self.stage_samples: list = []   # (tokens, prefill_units, decode_tokens, layers, us)
+        self.fetch_left: dict = {}
+        torch.cuda.synchronize()
+
+    def _dev_of(self, iid: int) -> int:
+        return self.pools[iid].rt.device
+
+    # ---------------------------------------------------------- KV pages
+    def _ensure_pages(self, iid: int, rid: int, tokens: int, lo: int, hi: int) -> None:
+        pool = self.pools[iid]
+        slot = self.slots[iid].get(rid)
+        need = -(-tokens // self.B)
+        reqs = []
+        for l in range(lo, hi):
+            add = need - pool.npages(slot, l)
+            if add > 0:
+                if reqs and reqs[-1][2] == l and reqs[-1][3] == add:
+                    reqs[-1] = (slot, reqs[-1][1], l + 1, add)
+                else:
+                    reqs.append((slot, l, l + 1, add))
+        # page ops share one stream (the transfer stream) so a grow always
+        # sees every earlier release; execution waits on that stream
+        if reqs and not pool.grow(reqs, stream=self.te.bulk):
+            raise runtime.DeviceError(f"instance {iid}: out of KV pages for request {rid} "
+                                      "(page slack exhausted)")
+
+    def group_alloc(self, grun: GroupRun, rid: int, delta: int) -> bool:
+        if not super().group_alloc(grun, rid, delta):
+            return False
+        total = self.total_alloc[rid]
+        for iid in grun.group.member_instances:
+            lo, hi = grun.group.stage_layer_map[iid]
+            self._ensure_pages(iid, rid, total, lo, hi)
+        return True
+
+    def _release_everywhere(self, rid: int) -> None:
+        L = self.model.num_layers
+        for iid, slots in self.slots.items():
+            slot = slots.of.get(rid)
+            if slot is not None:
+                self.pools[iid].release([slot], 0, L, stream=self.te.bulk)
+                slots.drop(rid)
+
+    def group_free(self, grun: GroupRun, rid: int) -> None:
+        super().group_free(grun, rid)
+        self._release_everywhere(rid)
+
+    # ---------------------------------------------------------- transfers
+    def _run_task(self, task: TransferTask) -> None:
+        if task.kind is TaskKind.ACTIVATION:
+            return  # the stage inputs were handed over when the round executed
+        self.te.submit(task)
+
+    def _on_exchange_planned(self, tasks, old_map, new_map, tokens) -> None:
+        self.te.register_exchange(tasks, old_map, new_map, tokens)
+
+    def _on_params_planned(self, tasks, fetch: bool) -> None:
+        self.te.register_restore(tasks, self.model.bytes_per_layer)
+        if fetch:  # merge-time fetch: vacate the destination slab first
+            for t in tasks:
+                key = (t.dst, t.layers)
+                if key not in self.fetch_left:
+                    self.pools[t.dst].restore_begin(*t.layers)
+                    self.fetch_left[key] = 0
+                self.fetch_left[key] += 1
+
+    def _fetch_done(self, gid, task, when) -> None:
+        self.te.drain()
+        key = (task.dst, task.layers)
+        if key in self.fetch_left:
+            self.fetch_left[key] -= 1
+            if self.fetch_left[key] == 0:
+                del self.fetch_left[key]
+                self.pools[task.dst].restore_complete(*task.layers)
+        super()._fetch_done(gid, task, when)
+
+    def _exchange_chunk_done(self, task, when) -> None:
+        self.te.drain()
+        self.te.finish_flow_sources()
+        super()._exchange_chunk_done(task, when)
+
+    def _restore_chunk_done(self, gid, task, when) -> None:
+        self.te.drain()  # the slab bytes land before complete_restore flips ownership
+        super()._restore_chunk_done(gid, task, when)
+
+    def _on_consolidation_planned(self, rid, peer, home, layers, tasks) -> None:
+        self.te.register_chunked_kv(tasks, layers, {rid: self.requests[rid].context_len})
+
+    def _on_consolidated(self, rid, peers) -> None:
+        self.te.drain()
+        self.te.finish_flow_sources()
+        L = self.model.num_layers
+        for iid in peers:
+            slot = self.slots[iid].of.get(rid)
+            if slot is not None:
+                self.pools[iid].release([slot], 0, L, stream=self.te.bulk)
+                self.slots[iid].drop(rid)
+
+    # ---------------------------------------------------------- execution
+    def _batch(self, iid: int, mb) -> dict:
+        torch = self.torch
+        dev = f"cuda:{self._dev_of(iid)}"
+        slots, pos = [], []
+        p_rows, p_slots, p_off, p_len, p_prefix = [], [], [], [], []
+        d_rows, d_slots, d_ctx = [], [], []
+        last_rows = []  # rows that produce a token: decodes, last row of each prefill chunk
+        row = 0
+        for ch in mb.chunks:
+            slot = self.slots[iid].of[ch.rid]
+            if ch.decode:
+                ctx = ch.prefix_len  # context incl. the token being decoded
+                slots.append(slot)
+                pos.append(ctx - 1)
+                d_rows.append(row)
+                d_slots.append(slot)
+                d_ctx.append(ctx)
+                last_rows.append(row)
+                row += 1
+            else:
+                c, p = ch.token_count, ch.prefix_len
+                slots.extend([slot] * c)
+                pos.extend(range(p, p + c))
+                p_off.append(len(p_rows))
+                p_rows.extend(range(row, row + c))
+                p_slots.append(slot)
+                p_len.append(c)
+                p_prefix.append(p)
+                row += c
+                last_rows.append(row - 1)
+        i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
+        i64 = lambda xs: torch.tensor(xs, dtype=torch.int64, device=dev)  # noqa: E731
+        return {"n": row, "slots": i32(slots), "pos": i32(pos),
+                "np": len(p_slots), "p_rows": i64(p_rows), "p_slots": i32(p_slots),
+                "p_off": i32(p_off), "p_len": i32(p_len), "p_prefix": i32(p_prefix),
+                "p_max": max(p_len) if p_len else 0,
+                "nd": len(d_slots), "d_rows": i64(d_rows), "d_slots": i32(d_slots),
+                "d_ctx": i32(d_ctx), "d_max": max(d_ctx) if d_ctx else 0,
+                "last": i64(last_rows),
+                "units": sum(ch.token_count * ch.prefix_len + (ch.token_count ** 2 + ch.token_count) / 2
+                             for ch in mb.chunks if not ch.decode)}
+
+    def _stage_times(self, grun: GroupRun, mbs, spans) -> list:
+        """Execute every (microbatch, stage) of the round on its member's pool
+        and return the measured times in us (one device sync per round)."""
+        torch = self.torch
+        members = grun.group.member_instances
+        st = torch.cuda.current_stream()
+        st.wait_stream(self.te.bulk)  # KV moves / restores this round depends on
+        events = []
+        for k, mb in enumerate(mbs):
+            x = None
+            for s, iid in enumerate(members):
+                lo, hi = grun.group.stage_layer_map[iid]
+                b = self._batch(iid, mb)
+                if x is None:
+                    ids = torch.randint(0, self.shape.vocab, (b["n"],), device=b["slots"].device)
+                    x = self.emb[self._dev_of(iid)].index_select(0, ids)
+                elif x.device != b["slots"].device:
+                    x = x.to(b["slots"].device)
+                a = torch.cuda.Event(enable_timing=True)
+                e = torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                x = self.runners[iid].run(lo, hi, x, b)
+                if s == len(members) - 1:  # sample the next token of each sequence
+                    lw = self.emb[self._dev_of(iid)]
+                    if b["last"].numel():
+                        logits = x.index_select(0, b["last"]) @ lw.t()
+                        logits.argmax(dim=-1)
+                e.record(st)
+                events.append((s, k, a, e, b["n"], b["units"], b["nd"], hi - lo))
+        e.synchronize()
+        times = [[1] * len(mbs) for _ in members]
+        for s, k, a, e, n, units, nd, layers in events:
+            us = max(1, int(round(a.elapsed_time(e) * 1000)))
+            times[s][k] = us
+            self.stage_samples.append((n, units, nd, layers, us))
+        return times
+
+
+def device_config(shape, instances: int = 2, kv_bytes: int = 8 << 30, devices=(0,),
+                  nvlink_bandwidth: int = 900_000_000_000, link_latency_us: int = 5,
+                  map_latency_us: int = 0):
+    """SimConfig for `instances` replicas of `shape` with `kv_bytes` of KV
+    budget each, NVLink-5 links and the aliased-slab remap cost."""
+    from .config import SimConfig
+    cfg = SimConfig()
+    cfg.model = shape.spec()
+    cfg.cluster.instances = instances
+    cfg.cluster.hbm_bytes = cfg.model.param_bytes + kv_bytes
+    cfg.cluster.nic_bandwidth = nvlink_bandwidth
+    cfg.cluster.link_base_latency_us = link_latency_us
+    cfg.cluster.map_latency_us = map_latency_us
+    cfg.device.shape = shape
+    cfg.device.devices = tuple(devices)
+    cfg.device.max_pages_per_seq = max(64, math.ceil(32768 / shape.block_tokens))
+    cfg.device.max_slots = 512
+    return cfg

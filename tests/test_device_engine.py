@@ -1,0 +1,55 @@
+"""The reference's engine on real device pools (serving.DeviceEngine).
+
+Same scheduler as the model-mode engine (byte-identical to the reference's
+logs), with pools, page tables, transfers and measured stage times on the
+GPU.  Checks the drop cycle happens, every request finishes, and the device
+ends in its boot state: all layers held, no live KV page, no reservation.
+"""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2412_18169_b200.core import SHAPES  # noqa: E402
+from paper_2412_18169_b200.metrics import collect, parse_line  # noqa: E402
+from paper_2412_18169_b200.traceio import TraceRecord  # noqa: E402
+
+
+def kinds(lines):
+    out = {}
+    for l in lines:
+        k = parse_line(l)[1]
+        out[k] = out.get(k, 0) + 1
+    return out
+
+
+@pytest.fixture(scope="module")
+def built():
+    from paper_2412_18169_b200 import build
+    build.build()
+
+
+@pytest.mark.parametrize("policy", ["kunserve", "recompute"])
+def test_device_engine_overload_cycle(built, policy):
+    from paper_2412_18169_b200.serving import DeviceEngine, device_config
+    shape = SHAPES["tiny"]
+    cfg = device_config(shape, instances=2, kv_bytes=1 << 20)
+    cfg.policy.kind = policy
+    trace = [TraceRecord(1000 * i, 250, 20) for i in range(8)]
+    eng = DeviceEngine(cfg, trace)
+    res = eng.run()
+    k = kinds(res.log_lines)
+    assert k.get("FINISH", 0) == len(trace)
+    if policy == "kunserve":
+        assert k.get("PLAN", 0) >= 1 and k.get("EXCHANGE", 0) >= 1
+        assert k.get("RESTORE_DONE", 0) >= 1 and k.get("DISSOLVE", 0) >= 1
+        assert res.evictions == 0
+    for iid, inst in eng.instances.items():
+        assert inst.table.layers_held() == list(range(shape.num_layers))
+        assert inst.kv.allocated_tokens == {} and inst.kv.reserved_bytes == 0
+        info = inst.pool.info()
+        assert info.live_pages == 0 and info.layers_mapped == shape.num_layers
+    st = collect(res.log_lines)
+    assert len(st.ttfts()) == len(trace)
+    assert eng.stage_samples and all(s[-1] >= 1 for s in eng.stage_samples)
