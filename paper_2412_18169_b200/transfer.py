@@ -125,11 +125,21 @@ class TransferEngine:
             rid, j, k = key
             lo = max(old_map[j][0], new_map[k][0])
             hi = min(old_map[j][1], new_map[k][1])
-            B = self.pools[j].shape.block_tokens
-            npages = -(-context_tokens[rid] // B)
+            npages = self._flow_pages(j, rid, context_tokens[rid], lo)
             self.flows[key] = KVFlow(rid, j, k, (lo, hi), npages, len(chunks))
             for idx, t in enumerate(chunks):
                 self.chunk_of[t.tid] = (key, idx)
+
+    def _flow_pages(self, src: int, rid: int, tokens: int, layer: int) -> int:
+        """Pages a flow moves: the request's context in pages, capped by what
+        the source holds.  (The reference's context_len counts the token just
+        emitted, whose KV is written only when its decode round allocates it,
+        engine.py:335-345 -- so the source may hold one page fewer.)"""
+        B = self.pools[src].shape.block_tokens
+        want = -(-tokens // B)
+        slot = self.slots[src].of.get(rid)
+        have = self.pools[src].npages(slot, layer) if slot is not None else 0
+        return min(want, have)
 
     def register_restore(self, tasks: list[TransferTask], bytes_per_layer: int) -> None:
         """Byte offsets of every PARAM_SHARD chunk inside its layer run."""
@@ -149,9 +159,8 @@ class TransferEngine:
             per_flow.setdefault((t.rid, t.src, t.dst), []).append(t)
         for key, chunks in per_flow.items():
             rid, j, _ = key
-            B = self.pools[j].shape.block_tokens
-            self.flows[key] = KVFlow(rid, j, key[2], layers, -(-context_tokens[rid] // B),
-                                     len(chunks))
+            npages = self._flow_pages(j, rid, context_tokens[rid], layers[0])
+            self.flows[key] = KVFlow(rid, j, key[2], layers, npages, len(chunks))
             for idx, t in enumerate(chunks):
                 self.chunk_of[t.tid] = (key, idx)
 
