@@ -7,18 +7,19 @@ Workload (BASELINE.json configs[1] on one GPU): two Llama-3-8B bf16 replicas
 paged KV pools -- each filled to 90% of its KV budget with ShareGPT-shaped
 residents (lognormal, mean 1660 tokens).  A step is one overload cycle
 through the public API (cycle.OverloadCycle): plan_drop -> drop 16 layers
-per replica (VMM remap into the KV pool) -> coordinated KV exchange (page
-gather/scatter kernels) -> restore (device page compaction, remap, peer
-slab pull of 16 layers per replica) -> dissolve + KV consolidation.  Every
-step ends in the boot layout; the run checks bit-exact weights and KV
-checksums after the timed steps.
+per replica (their aliased slabs join the paged KV pool) -> coordinated KV
+exchange (page gather/scatter kernels) -> burst drains (untimed) -> restore
+(device page compaction + peer slab pull of 16 layers per replica) ->
+dissolve + KV consolidation.  Every step ends in the boot layout; the run
+checks bit-exact weights and KV checksums after the timed steps.
 
 metric   drop/restore GB/s = payload bytes moved per step / step device time
          (CUDA events on the transfer stream, remaps included)
 paged_decode   tcgen05 paged-decode attention over the merged (enlarged)
          pools, all 32 layers per token, tok/s
-p99_ttft  not measured on hardware this round (the engine's sim mode
-         reproduces the reference's event logs)
+p99_ttft  the reference's scheduler on real Llama-3-8B pools with measured
+         stage times (serving.DeviceEngine), KunServe vs recompute on one 4x
+         ShareGPT-shaped burst (ttft.py)
 With --gpus N each rank runs its own pair of replicas on its GPU (the path
 shards into independent groups: scaling "weak", no data-path collective).
 """
@@ -201,6 +202,8 @@ def main():
     ap.add_argument("--kv-gib", type=float, default=16.0)
     ap.add_argument("--decode-iters", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ttft", action="store_true",
+                    help="skip the device-engine P99 TTFT measurement (~90 s)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -291,6 +294,15 @@ def main():
         res.copy_(tok_d.to(torch.int64) * 0 + r.n_tasks, non_blocking=True)
         torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    r_last = reps[-1]
+    cyc.close()
+
+    # P99 TTFT: the reference's scheduler on real pools with measured stage
+    # times, KunServe vs the recompute baseline on one 4x burst
+    ttft = None
+    if not args.no_ttft:
+        from paper_2412_18169_b200.ttft import measure
+        ttft = measure(kv_gib=1.0, base_rps=2.0)
 
     line = None
     if rank == 0:
@@ -311,7 +323,7 @@ def main():
                    "kind": "port",
                    "sample": f"3 CPU cycles of 2 of 32 layer slabs + {len(res_toks)} residents' "
                              f"pages, numpy copies on {cc.threads} threads"}
-        r0 = reps[-1]
+        r0 = r_last
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
@@ -333,7 +345,7 @@ def main():
                          "kernel": "copy_flat_kernel (peer slab pull; same-GPU replicas: "
                                    "read+write HBM)", "peak_source": peak_src},
             "paged_decode": dec,
-            "p99_ttft": None,
+            "p99_ttft": ttft,
             "parity": parity,
             "e2e": {"value": round(e_moved / e2e_s / 1e9, 1), "unit": "GB/s",
                     "h2d_bytes_per_step": tok.numel() * 4, "d2h_bytes_per_step": res.numel() * 8},

@@ -353,6 +353,11 @@ class OverloadCycle:
         rep.ms = parts
         return rep
 
+    def close(self) -> None:
+        self.torch.cuda.synchronize()
+        for pool in self.pools.values():
+            pool.close()
+
     def refill(self) -> None:
         torch = self.torch
         for rid in sorted(self.transient):

@@ -35,11 +35,19 @@ def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None) -> dict:
     wall = time.perf_counter() - t0
     st = collect(res.log_lines)
     ttfts = st.ttfts()
+    # a request that never got its first token inside the run counts as
+    # infinitely late in the all-requests P99 (the served-only P99 is the
+    # reference's metrics.collect view)
+    unserved = len(trace) - len(ttfts)
+    all_sorted = sorted(ttfts) + [float("inf")] * unserved
     kinds = {}
     for line in res.log_lines:
         k = line.split(" ", 2)[1]
         kinds[k] = kinds.get(k, 0) + 1
+    p99_all = percentile(all_sorted, 99) if all_sorted else None
     out = {"policy": policy, "requests": len(trace), "finished": st.finished(),
+           "served": len(ttfts),
+           "p99_ttft_all_s": None if p99_all in (None, float("inf")) else round(p99_all, 4),
            "p99_ttft_s": round(percentile(ttfts, 99), 4) if ttfts else None,
            "p50_ttft_s": round(percentile(ttfts, 50), 4) if ttfts else None,
            "p50_tpot_s": round(percentile(st.tpots(), 50), 5) if st.tpots() else None,
@@ -55,6 +63,10 @@ def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None) -> dict:
 def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b", **trace_kw) -> dict:
     shape = SHAPES[shape_name]
     trace = burst_trace(**trace_kw)
+    # warm-up: load every kernel / cuBLAS heuristic and walk one drop cycle
+    # so the measured runs see steady-state stage times
+    warm = burst_trace(duration_s=4.0, base_rps=4.0, input_mean=1660, output_mean=8, seed=11)
+    run_policy("kunserve", warm, shape, int(0.25 * (1 << 30)))
     res = {}
     samples_all = []
     for pol in ("kunserve", "recompute"):
@@ -63,8 +75,10 @@ def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b", **trace_kw) -> d
         samples_all += samples
     k, r = res["kunserve"], res["recompute"]
     ratio = (r["p99_ttft_s"] / k["p99_ttft_s"]) if k["p99_ttft_s"] and r["p99_ttft_s"] else None
-    return {"value": k["p99_ttft_s"], "unit": "s", "baseline_recompute_s": r["p99_ttft_s"],
-            "p99_ratio_recompute_over_kunserve": round(ratio, 2) if ratio else None,
+    return {"value": k["p99_ttft_all_s"], "unit": "s",
+            "baseline_recompute_s": r["p99_ttft_all_s"],
+            "baseline_recompute_served_only_s": r["p99_ttft_s"],
+            "p99_ratio_recompute_over_kunserve_served_only": round(ratio, 2) if ratio else None,
             "kunserve": k, "recompute": r,
             "trace": {"requests": len(trace), "input_mean": trace_kw.get("input_mean", 1660),
                       "output_mean": trace_kw.get("output_mean", 64), "burst": "4x",
