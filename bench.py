@@ -139,6 +139,58 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def prefill_measure(rt, tensor_peak: float, ctx: int = 32768, chunk: int = 2048,
+                    iters: int = 3) -> dict:
+    """Config 4 attention: one Qwen2.5-14B layer, a 32k-token prompt prefilled
+    in 2048-token chunks over the paged pool (each chunk attends to its
+    prefix + itself causally).  FLOPs = 4*Hq*d*(p*c + c(c+1)/2) per chunk
+    (costmodel.attention_units)."""
+    import torch
+    from paper_2412_18169_b200 import runtime
+    from paper_2412_18169_b200.core import SHAPES
+    shape = SHAPES["qwen25_14b"]
+    model = shape.spec()
+    rt = runtime.Runtime(rt.device, max_slots=4, max_pages_per_seq=ctx // shape.block_tokens)
+    pool = rt.create_pool(0, model, model.param_bytes + (1 << 30), shape)
+    B, Hq, Hkv = shape.block_tokens, shape.n_q_heads, shape.n_kv_heads
+    assert pool.grow([(0, 0, 1, ctx // B)])
+    g = torch.Generator(device="cuda").manual_seed(21)
+    dev = lambda xs: torch.tensor(xs, dtype=torch.int32, device="cuda")  # noqa: E731
+    for s in range(0, ctx, 4096):
+        k = torch.randn((4096, Hkv, 128), device="cuda", generator=g).to(torch.bfloat16)
+        v = torch.randn((4096, Hkv, 128), device="cuda", generator=g).to(torch.bfloat16)
+        runtime.kv_append(pool, 0, k, v, dev([0] * 4096), torch.arange(s, s + 4096, dtype=torch.int32,
+                                                                       device="cuda"))
+    q = torch.randn((chunk, Hq, 128), device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    flops = 0
+    calls = []
+    for p in range(0, ctx, chunk):
+        flops += 4 * Hq * 128 * (p * chunk + chunk * (chunk + 1) // 2)
+        calls.append((dev([0]), dev([0]), dev([chunk]), dev([p])))
+
+    def run():
+        for sl, off, ln, pre in calls:
+            runtime.paged_prefill(pool, 0, q, sl, off, ln, pre, chunk, out, 128 ** -0.5)
+    run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        run()
+    b.record()
+    b.synchronize()
+    ms = a.elapsed_time(b) / iters
+    tf = flops / (ms / 1e3) / 1e12
+    pool.close()
+    return {"value": round(ctx / (ms / 1e3), 1), "unit": "tok/s (one layer, 32k prompt)",
+            "ms_per_layer": round(ms, 3), "chunks": len(calls),
+            "roofline": {"bound": "tensor", "achieved": round(tf, 1), "peak": tensor_peak,
+                         "unit": "TFLOP/s", "frac": round(tf / tensor_peak, 4),
+                         "traffic": None,
+                         "flops_per_layer": flops}}
+
+
 def decode_measure(cyc, iters: int, hbm_peak: float):
     """tcgen05 paged decode over the merged pools: one token for every
     resident through all 32 layers (each member decodes its stage)."""
@@ -296,6 +348,8 @@ def main():
     e2e_s = time.perf_counter() - t0
     r_last = reps[-1]
     cyc.close()
+    _, tensor_peak, _ = load_peaks()
+    prefill = prefill_measure(rt, tensor_peak or 1590.0)
 
     # P99 TTFT: the reference's scheduler on real pools with measured stage
     # times, KunServe vs the recompute baseline on one 4x burst
@@ -345,6 +399,7 @@ def main():
                          "kernel": "copy_flat_kernel (peer slab pull; same-GPU replicas: "
                                    "read+write HBM)", "peak_source": peak_src},
             "paged_decode": dec,
+            "paged_prefill": prefill,
             "p99_ttft": ttft,
             "parity": parity,
             "e2e": {"value": round(e_moved / e2e_s / 1e9, 1), "unit": "GB/s",

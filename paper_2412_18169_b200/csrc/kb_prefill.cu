@@ -6,13 +6,21 @@
 // (pkg/src/dropsim/costmodel.py:50-57, used for stage time at
 // engine.py:389-397).  FLOPs per layer = 4 * Hq * head_dim * attention_units.
 //
-// CTA = (128-row query tile, query head).  Per 128-key tile:
-//   S[128 q x 128 k]  = Q[128 x 128 d] . K^T        (K-major A and B)
-//   O_t[128 q x 128 d] = P[128 q x 128 k] . V        (V is an MN-major B)
-// S double-buffered in TMEM, P staged bf16 in smem (SW128), O folded into
-// registers with the online-softmax rescale.  Warp roles (192 threads):
-// 0-3 softmax / epilogue (thread = query row), 4 TMA producer (K/V pages
-// named by the block table), 5 MMA issuer + TMEM owner.
+// CTA = two 128-row query tiles of one head (256 query rows) sharing every
+// K/V tile.  Per 128-key tile j and query tile t:
+//   S_t = Q_t . K_j^T                 (tcgen05, A and B from smem, K-major)
+//   P_t = exp2(S_t*scale - m_t)       (softmax warpgroup t, one row per thread)
+//   O_t += [P_t,hi | P_t,lo] . [V_j ; V_j]   (A = P from TMEM, B = V MN-major)
+// S, P and O live in TMEM (S0 | S1 | O0 | O1 = 512 columns); P overwrites S
+// chunk by chunk, as bf16 hi + bf16 residual so P keeps ~16 mantissa bits
+// (a single bf16 P alone costs ~1.1e-3 relative error).  The two tiles
+// ping-pong: the MMA warp issues QK0(j) QK1(j) PV0(j) QK0(j+1) PV1(j)
+// QK1(j+1) ..., so the tensor pipe works on one tile while the other tile's
+// softmax runs.  O is rescaled lazily, only when a row max grows by more
+// than 2^8 (the probabilities stay bounded by 256, exact in bf16 / fp32).
+//
+// Warp roles (320 threads): 0-3 softmax tile 0, 4-7 softmax tile 1, 8 TMA
+// producer (K/V pages named by the block table), 9 MMA issuer + TMEM owner.
 #include <cuda_bf16.h>
 
 #include "kb_common.cuh"
@@ -21,21 +29,27 @@
 namespace kb {
 
 constexpr int kPfStages = 2;
-constexpr int kPfThreads = 192;
+constexpr int kPfThreads = 320;
 constexpr int kPfTile = 128;
 constexpr int kPfHalf = 16384;                     // 128 rows x 64 el x 2 B
 constexpr int kPfKV = 4 * kPfHalf;                 // K + V for one 128-key tile
-constexpr int kPfQ = 2 * kPfHalf;
-constexpr int kPfP = 4 * kPfHalf;                  // P_hi + P_lo
-constexpr int kPfSmem = kPfStages * kPfKV + kPfQ + kPfP + 1024 + 1024;
-constexpr uint32_t kPfTmemCols = 512;               // S0 | S1 | O
+constexpr int kPfQ = 2 * kPfHalf;                  // one 128-row Q tile
+constexpr int kPfSmem = kPfStages * kPfKV + 2 * kPfQ + 1024 + 1024;
+constexpr uint32_t kPfTmemCols = 512;              // S0 | S1 | O0 | O1
+constexpr float kRescaleLog2 = 8.0f;               // lazy-rescale threshold
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 struct PrefillMisc {
   uint64_t full[kPfStages];
   uint64_t empty[kPfStages];
   uint64_t s_full[2];
-  uint64_t o_full;
-  uint64_t p_full;
+  uint64_t p_ready[2];
+  uint64_t o_done[2];
   uint64_t q_full;
   uint32_t tmem_base;
 };
@@ -51,12 +65,12 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
   using namespace sm100;
   constexpr int kPPT = kPfTile / kB;
   const int hq = blockIdx.y;
-  const int seq = blockIdx.x / mtiles, mt = blockIdx.x % mtiles;
+  const int seq = blockIdx.x / mtiles, mt = blockIdx.x % mtiles;  // mt: 256-row CTA tile
   const int h = hq / (Hq / Hkv);
   const int qlen = q_len[seq], pre = prefix[seq], qo = q_off[seq];
-  const int row0 = mt * kPfTile;
+  const int row0 = mt * 2 * kPfTile;
   if (row0 >= qlen) return;  // grid is sized for the longest chunk
-  const int rows = min(kPfTile, qlen - row0);
+  const int rows = min(2 * kPfTile, qlen - row0);
   const int kv_len = pre + row0 + rows;  // keys visible to the last row
   const int nt = (kv_len + kPfTile - 1) / kPfTile;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -64,34 +78,35 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sQ = smem + kPfStages * kPfKV;
-  uint8_t* sP = sQ + kPfQ;
-  PrefillMisc* misc = reinterpret_cast<PrefillMisc*>(sP + kPfP);
+  uint8_t* sQ = smem + kPfStages * kPfKV;  // Q0 then Q1
+  PrefillMisc* misc = reinterpret_cast<PrefillMisc*>(sQ + 2 * kPfQ);
 
-  if (warp == 5) {
+  if (warp == 9) {
     if (lane == 0) {
       for (int s = 0; s < kPfStages; ++s) {
         mbar_init(&misc->full[s], 1);
         mbar_init(&misc->empty[s], 1);
       }
-      mbar_init(&misc->s_full[0], 1);
-      mbar_init(&misc->s_full[1], 1);
-      mbar_init(&misc->o_full, 1);
-      mbar_init(&misc->p_full, 128);
-      mbar_init(&misc->q_full, 128);
+      for (int t = 0; t < 2; ++t) {
+        mbar_init(&misc->s_full[t], 1);
+        mbar_init(&misc->p_ready[t], 128);
+        mbar_init(&misc->o_done[t], 1);
+      }
+      mbar_init(&misc->q_full, 256);
       fence_barrier_init();
     }
     __syncwarp();
     tmem_alloc(&misc->tmem_base, kPfTmemCols);
   }
-  if (warp == 4 && lane == 0) tma_prefetch_desc(&tmap);
+  if (warp == 8 && lane == 0) tma_prefetch_desc(&tmap);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = misc->tmem_base;
   const int32_t* bt_row = bt + ((int64_t)slots[seq] * L + layer) * maxp;
 
-  if (warp == 4) {
+  if (warp == 8) {
+    // ------------------------------------------------ TMA producer
     if (lane == 0) {
       for (int j = 0; j < nt; ++j) {
         const int stage = j % kPfStages;
@@ -120,175 +135,211 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
+    // ------------------------------------------------ MMA issuer
     constexpr uint32_t kIdQK = idesc_bf16_f32(128, 128, false, false);
     constexpr uint32_t kIdPV = idesc_bf16_f32(128, 128, false, true);
-    const uint32_t q_addr = smem_u32(sQ), p_addr = smem_u32(sP);
-    auto issue_qk = [&](int j) {
+    auto issue_qk = [&](int t, int j) {
       const int stage = j % kPfStages;
-      mbar_wait(&misc->full[stage], (j / kPfStages) & 1);
-      tc_fence_after();
+      if (t == 0) {
+        mbar_wait(&misc->full[stage], (j / kPfStages) & 1);
+        tc_fence_after();
+      }
       if (lane == 0) {
+        const uint32_t q_addr = smem_u32(sQ + t * kPfQ);
         const uint32_t k_addr = smem_u32(smem + stage * kPfKV);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t a = sw128_desc(q_addr + (kk >> 2) * kPfHalf + (kk & 3) * 32, 16, 1024);
           const uint64_t b = sw128_desc(k_addr + (kk >> 2) * kPfHalf + (kk & 3) * 32, 16, 1024);
-          mma_f16_ss(tmem + (j & 1) * 128, a, b, kIdQK, kk > 0);
+          mma_f16_ss(tmem + t * 128, a, b, kIdQK, kk > 0);
         }
-        mma_commit(&misc->s_full[j & 1]);
+        mma_commit(&misc->s_full[t]);
       }
       __syncwarp();
     };
-    mbar_wait(&misc->q_full, 0);
-    issue_qk(0);
-    for (int j = 0; j < nt; ++j) {
-      if (j + 1 < nt) issue_qk(j + 1);
-      mbar_wait(&misc->p_full, j & 1);
+    auto issue_pv = [&](int t, int j) {
+      mbar_wait(&misc->p_ready[t], j & 1);
       tc_fence_after();
       if (lane == 0) {
         const int stage = j % kPfStages;
         const uint32_t v_addr = smem_u32(smem + stage * kPfKV + 2 * kPfHalf);
+        const uint32_t p_base = tmem + t * 128;
+        // 16-key group m: P_hi at column 32*(m/2) + 8*(m%2), P_lo 16 columns later
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          const int k8 = kk & 7;  // kk < 8: P_hi, kk >= 8: P_lo; both against V
-          const uint64_t a = sw128_desc(p_addr + (kk >> 3) * 2 * kPfHalf + (k8 >> 2) * kPfHalf +
-                                            (k8 & 3) * 32, 16, 1024);
-          const uint64_t b = sw128_desc(v_addr + k8 * 2048, kPfHalf, 1024);  // MN-major V
-          mma_f16_ss(tmem + 256, a, b, kIdPV, kk > 0);
+        for (int m = 0; m < 8; ++m) {
+          const uint64_t b = sw128_desc(v_addr + m * 2048, kPfHalf, 1024);  // MN-major V
+          const uint32_t a_hi = p_base + 32 * (m >> 1) + 8 * (m & 1);
+          mma_f16_ts(tmem + 256 + t * 128, a_hi, b, kIdPV, (j > 0 || m > 0) ? 1u : 0u);
+          mma_f16_ts(tmem + 256 + t * 128, a_hi + 16, b, kIdPV, 1u);
         }
-        mma_commit(&misc->o_full);
-        mma_commit(&misc->empty[stage]);
+        mma_commit(&misc->o_done[t]);
+        if (t == 1) mma_commit(&misc->empty[stage]);
       }
       __syncwarp();
+    };
+    mbar_wait(&misc->q_full, 0);
+    tc_fence_after();
+    issue_qk(0, 0);
+    issue_qk(1, 0);
+    for (int j = 0; j < nt; ++j) {
+      issue_pv(0, j);
+      if (j + 1 < nt) issue_qk(0, j + 1);
+      issue_pv(1, j);
+      if (j + 1 < nt) issue_qk(1, j + 1);
     }
   } else {
-    // Q tile -> SW128 K-major image (row = query row, 2 d-halves)
-    {
-      const int r = tid;
-      const int4* src = reinterpret_cast<const int4*>(q + ((int64_t)(qo + row0 + r) * Hq + hq) * 128);
+    // ------------------------------------------------ softmax warpgroup t
+    const int t = warp >> 2;              // query tile of this warpgroup
+    const int r = tid & 127;              // row within the tile (= TMEM lane)
+    const int qrow = row0 + t * kPfTile + r;  // row within the chunk
+    const bool row_ok = qrow < qlen;
+    const int qpos = pre + qrow;
+    {  // Q tile t -> SW128 K-major image
+      const int4* src = reinterpret_cast<const int4*>(q + ((int64_t)(qo + qrow) * Hq + hq) * 128);
+      uint8_t* dst = sQ + t * kPfQ;
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
-        int4 v = r < rows ? src[c] : make_int4(0, 0, 0, 0);
+        int4 v = row_ok ? src[c] : make_int4(0, 0, 0, 0);
         const uint32_t off = (c >> 3) * kPfHalf + r * 128 + ((((c & 7) ^ (r & 7)) & 7) << 4);
-        *reinterpret_cast<int4*>(sQ + off) = v;
+        *reinterpret_cast<int4*>(dst + off) = v;
       }
     }
     fence_proxy_async_smem();
     mbar_arrive(&misc->q_full);
-
-    const int qpos = pre + row0 + tid;  // this thread's query position
-    const bool row_ok = tid < rows;
-    float o[128];
-#pragma unroll
-    for (int i = 0; i < 128; ++i) o[i] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f, alpha_prev = 1.f;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t s_addr = tmem + lane_base + t * 128;
+    const uint32_t o_addr = tmem + lane_base + 256 + t * 128;
+    float m_ref = -INFINITY, l_run = 0.f;
     for (int j = 0; j < nt; ++j) {
-      mbar_wait(&misc->s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&misc->s_full[t], j & 1);
       tc_fence_after();
-      // pass 1: row max over this key tile (S re-read from TMEM in pass 2)
       const int kbase = j * kPfTile;
-      const uint32_t s_addr = tmem + lane_base + (j & 1) * 128;
-      float mx = -INFINITY;
+      // Tiles wholly below the warp's first query position need no mask
+      // (warp-uniform); diagonal / tail tiles take the masked path.
+      const int warp_q0 = pre + row0 + t * kPfTile + (warp & 3) * 32;
+      const bool full_tile = kbase + kPfTile - 1 <= warp_q0 &&
+                             row0 + t * kPfTile + (warp & 3) * 32 + 31 < qlen;
+      // pass 1: row max of this key tile (on raw scores; scaled once)
+      float mraw = -INFINITY;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float part[32];
         tmem_ld_32x32b_x32(s_addr + c * 32, part);
+        if (full_tile) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const bool ok = row_ok && (kbase + c * 32 + i) <= qpos;
-          mx = fmaxf(mx, ok ? part[i] * scale_log2 : -INFINITY);
+          for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, part[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const bool ok = row_ok && (kbase + c * 32 + i) <= qpos;
+            mraw = fmaxf(mraw, ok ? part[i] : -INFINITY);
+          }
         }
       }
-      const float m_new = fmaxf(m_run, mx);
-      const float alpha = m_new == -INFINITY ? 1.f : exp2f(m_run - m_new);
-      if (j > 0) {  // fold the previous tile's O (frees the P buffer)
-        mbar_wait(&misc->o_full, (j - 1) & 1);
-        tc_fence_after();
+      const float mx = mraw * scale_log2;
+      // lazy rescale: move the reference max only when it grows by > 2^8.
+      // TMEM ld/st are warp-collective, so the whole warp rescales when any
+      // of its rows needs it (alpha = 1 for the others).
+      const bool need = mx > m_ref + kRescaleLog2;
+      if (__any_sync(0xffffffffu, need)) {
+        const float alpha = !need ? 1.f : (m_ref == -INFINITY ? 0.f : exp2f(m_ref - mx));
+        if (j > 0) {
+          // O_t += P.V of tile j-1 completed before QK_t(j) (in-order pipe,
+          // and s_full tracks every earlier MMA of the issuer)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float part[32];
-          tmem_ld_32x32b_x32(tmem + lane_base + 256 + c * 32, part);
+          for (int c = 0; c < 4; ++c) {
+            float part[32];
+            tmem_ld_32x32b_x32(o_addr + c * 32, part);
+            uint32_t w[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[c * 32 + i] = o[c * 32 + i] * alpha_prev + part[i];
+            for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(part[i] * alpha);
+            tmem_st_32x32b_x32(o_addr + c * 32, w);
+          }
+        }
+        if (need) {
+          l_run *= alpha;
+          m_ref = mx;
         }
       }
-      alpha_prev = alpha;
-      if (kbase + kPfTile > kv_len) {  // partial tile: zero V rows past kv_len
+      if (kbase + kPfTile > kv_len && t == 0) {  // partial tile: zero V rows past kv_len
         const int stage = j % kPfStages;
         mbar_wait(&misc->full[stage], (j / kPfStages) & 1);
-        if (kbase + tid >= kv_len) {
+        if (kbase + r >= kv_len) {
           uint8_t* sV = smem + stage * kPfKV + 2 * kPfHalf;
-          int4* r0 = reinterpret_cast<int4*>(sV + tid * 128);
-          int4* r1 = reinterpret_cast<int4*>(sV + kPfHalf + tid * 128);
+          int4* r0 = reinterpret_cast<int4*>(sV + r * 128);
+          int4* r1 = reinterpret_cast<int4*>(sV + kPfHalf + r * 128);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             r0[c] = make_int4(0, 0, 0, 0);
             r1[c] = make_int4(0, 0, 0, 0);
           }
         }
+        fence_proxy_async_smem();
       }
-      // pass 2: P = exp2(S*scale - m) -> bf16 SW128 K-major image (row = query row)
+      // pass 2: P = exp2(S*scale - m_ref) over S, 32 keys per chunk:
+      // columns [32c, 32c+16) = bf16x2 P_hi, [32c+16, 32c+32) = bf16x2 P_lo.
+      // P_hi = P truncated to bf16 (a mask), P_lo = bf16(P - P_hi) (exact
+      // remainder, rounded): P_hi + P_lo carries ~16 mantissa bits.
       float rs = 0.f;
+      const bool live = m_ref != -INFINITY;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float part[32];
         tmem_ld_32x32b_x32(s_addr + c * 32, part);
+        uint32_t w[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const bool ok = row_ok && (kbase + c * 32 + i) <= qpos && m_new != -INFINITY;
-          part[i] = ok ? exp2f(part[i] * scale_log2 - m_new) : 0.f;
-          rs += part[i];
+        for (int i = 0; i < 16; ++i) {
+          float x[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            float v = fast_exp2(fmaf(part[2 * i + e], scale_log2, -m_ref));
+            if (!full_tile) {
+              const int key = kbase + c * 32 + 2 * i + e;
+              v = (row_ok && key <= qpos && live) ? v : 0.f;
+            }
+            x[e] = v;
+          }
+          const uint32_t b0 = __float_as_uint(x[0]) & 0xFFFF0000u;
+          const uint32_t b1 = __float_as_uint(x[1]) & 0xFFFF0000u;
+          const __nv_bfloat162 lo =
+              __floats2bfloat162_rn(x[0] - __uint_as_float(b0), x[1] - __uint_as_float(b1));
+          rs += x[0] + x[1];
+          w[i] = __byte_perm(b0, b1, 0x7632);
+          w[16 + i] = *reinterpret_cast<const uint32_t*>(&lo);
         }
+        tmem_st_32x32b_x32(s_addr + c * 32, w);
+      }
+      tmem_st_wait();
+      l_run += rs;
+      tc_fence_before();
+      mbar_arrive(&misc->p_ready[t]);
+    }
+    // epilogue: O_t / l -> bf16 rows
+    mbar_wait(&misc->o_done[t], (nt - 1) & 1);
+    tc_fence_after();
+    {
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      int4* dst = reinterpret_cast<int4*>(out + ((int64_t)(qo + qrow) * Hq + hq) * 128);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float part[32];
+        tmem_ld_32x32b_x32(o_addr + c * 32, part);  // warp-collective: every lane
+        if (!row_ok) continue;
 #pragma unroll
         for (int q8 = 0; q8 < 4; ++q8) {
-          const int ch = c * 4 + q8;  // 16-byte chunk (8 keys) of the 128-key row
-          // P = P_hi + P_lo, both bf16: the PV chain runs over K = 256
-          // ([P_hi | P_lo] . [V ; V]) so P carries ~16 mantissa bits.
-          __nv_bfloat162 hi[4], lo[4];
+          __nv_bfloat162 pk[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float x0 = part[q8 * 8 + 2 * e], x1 = part[q8 * 8 + 2 * e + 1];
-            hi[e] = __floats2bfloat162_rn(x0, x1);
-            const float2 hf = __bfloat1622float2(hi[e]);
-            lo[e] = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
-          }
-          const uint32_t off = (ch >> 3) * kPfHalf + tid * 128 + ((((ch & 7) ^ (tid & 7)) & 7) << 4);
-          *reinterpret_cast<int4*>(sP + off) = *reinterpret_cast<int4*>(hi);
-          *reinterpret_cast<int4*>(sP + 2 * kPfHalf + off) = *reinterpret_cast<int4*>(lo);
+          for (int e = 0; e < 4; ++e)
+            pk[e] = __floats2bfloat162_rn(part[q8 * 8 + 2 * e] * inv, part[q8 * 8 + 2 * e + 1] * inv);
+          dst[c * 4 + q8] = *reinterpret_cast<int4*>(pk);
         }
-      }
-      l_run = l_run * alpha + rs;
-      m_run = m_new;
-      fence_proxy_async_smem();
-      mbar_arrive(&misc->p_full);
-    }
-    mbar_wait(&misc->o_full, (nt - 1) & 1);
-    tc_fence_after();
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      float part[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + c * 32, part);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o[c * 32 + i] = o[c * 32 + i] * alpha_prev + part[i];
-    }
-    if (row_ok) {
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      int4* dst = reinterpret_cast<int4*>(out + ((int64_t)(qo + row0 + tid) * Hq + hq) * 128);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        __nv_bfloat162 pk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          pk[e] = __floats2bfloat162_rn(o[c * 8 + 2 * e] * inv, o[c * 8 + 2 * e + 1] * inv);
-        dst[c] = *reinterpret_cast<int4*>(pk);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, kPfTmemCols);
   }
@@ -312,38 +363,25 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
   KB_RT(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
   if (max_q_len <= 0) return KB_OK;
-  // grid = (seq x m-tiles of the longest chunk) x q heads; CTAs past their
-  // sequence's chunk exit at once, so no host copy of q_len is needed
-  const int mtiles = (int)ceil_div(max_q_len, kPfTile);
+  // grid = (seq x 256-row tiles of the longest chunk) x q heads; CTAs past
+  // their sequence's chunk exit at once, so no host copy of q_len is needed
+  const int mtiles = (int)ceil_div(max_q_len, 2 * kPfTile);
   const float scale_log2 = scale * 1.4426950408889634f;
   dim3 grid((unsigned)(nseq * mtiles), n_q_heads);
-  if (B == 64) {
+  auto launch = [&](auto kernel) -> int {
     static bool attr = false;
     if (!attr) {
-      KB_RT(cudaFuncSetAttribute(prefill_tc_kernel<64>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kPfSmem));
+      KB_RT(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPfSmem));
       attr = true;
     }
-    prefill_tc_kernel<64><<<grid, kPfThreads, kPfSmem, st>>>(
+    kernel<<<grid, kPfThreads, kPfSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(q_off),
         reinterpret_cast<const int32_t*>(q_len), reinterpret_cast<const int32_t*>(prefix), mtiles,
-        reinterpret_cast<__nv_bfloat16*>(out), Hkv, n_q_heads, p->m.num_layers, p->maxp,
-        layer, scale_log2);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      KB_RT(cudaFuncSetAttribute(prefill_tc_kernel<128>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kPfSmem));
-      attr = true;
-    }
-    prefill_tc_kernel<128><<<grid, kPfThreads, kPfSmem, st>>>(
-        p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
-        reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(q_off),
-        reinterpret_cast<const int32_t*>(q_len), reinterpret_cast<const int32_t*>(prefix), mtiles,
-        reinterpret_cast<__nv_bfloat16*>(out), Hkv, n_q_heads, p->m.num_layers, p->maxp,
-        layer, scale_log2);
-  }
-  KB_LAUNCH_CHECK();
-  return KB_OK;
+        reinterpret_cast<__nv_bfloat16*>(out), Hkv, n_q_heads, p->m.num_layers, p->maxp, layer,
+        scale_log2);
+    KB_LAUNCH_CHECK();
+    return KB_OK;
+  };
+  return B == 64 ? launch(prefill_tc_kernel<64>) : launch(prefill_tc_kernel<128>);
 }
