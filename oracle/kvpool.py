@@ -170,10 +170,18 @@ def copy_pages(dst: OraclePool, src: OraclePool, moves) -> int:
     return moved
 
 
+def bf16_bits_to_f16_bits(x: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns -> fp16 bit patterns, round-to-nearest-even (what
+    __floats2half2_rn does in csrc/kb_append.cu)."""
+    f = (np.asarray(x, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+    return f.astype(np.float16).view(np.uint16)
+
+
 def kv_append(pool: OraclePool, layer: int, k: np.ndarray, v: np.ndarray, slots, pos,
               n_kv_heads: int, block_tokens: int, head_dim: int = 128) -> None:
     """Scatter K/V rows into pages laid out [K|V][kv_head][token][head_dim]
-    (csrc/kb_append.cu).  k, v: uint16 (bf16 bits) [ntok, n_kv_heads, head_dim]."""
+    (csrc/kb_append.cu): K stored as given (bf16), V converted to fp16.
+    k, v: uint16 bf16 bit patterns [ntok, n_kv_heads, head_dim]."""
     row_bytes = head_dim * 2
     half = pool.page_bytes // 2
     for t in range(k.shape[0]):
@@ -183,12 +191,13 @@ def kv_append(pool: OraclePool, layer: int, k: np.ndarray, v: np.ndarray, slots,
         for h in range(n_kv_heads):
             off = (h * block_tokens + r) * row_bytes
             buf[off:off + row_bytes] = k[t, h].view(np.uint8)
-            buf[half + off:half + off + row_bytes] = v[t, h].view(np.uint8)
+            buf[half + off:half + off + row_bytes] = bf16_bits_to_f16_bits(v[t, h]).view(np.uint8)
 
 
 def gather_kv(pool: OraclePool, slot: int, layer: int, ctx: int, n_kv_heads: int,
               block_tokens: int, head_dim: int = 128):
-    """K, V of the first ctx tokens as uint16 arrays [ctx, n_kv_heads, head_dim]."""
+    """K (bf16 bits), V (fp16 bits) of the first ctx tokens as uint16 arrays
+    [ctx, n_kv_heads, head_dim]."""
     half = pool.page_bytes // 2
     k = np.zeros((ctx, n_kv_heads, head_dim), dtype=np.uint16)
     v = np.zeros_like(k)

@@ -1,17 +1,34 @@
 // KV append: scatter the new tokens' K/V rows into their pages.
 //
 // Page layout (one layer, one request, block_tokens tokens):
-//   [K|V][n_kv_heads][block_tokens][head_dim] bf16
+//   [K|V][n_kv_heads][block_tokens][head_dim], K bf16, V fp16
 // so one kv head's K (or V) for a page is a contiguous block_tokens x 256 B
 // tile: the unit the attention kernels stage through TMA.
 // The page is found through the pool's block table ON DEVICE:
 //   page = bt[slot][layer][pos / block_tokens], row = pos % block_tokens.
+#include <cuda_fp16.h>
+
 #include "kb_common.cuh"
 
 namespace kb {
 
-// one warp per (token, kv head): lanes 0-15 move K, lanes 16-31 move V,
-// 16 bytes each (head_dim 128 bf16 = 256 B per row).
+// bf16 -> fp16 for 8 packed values (exact for |x| in fp16's normal range;
+// V activations live far inside it).  Storing V as fp16 lets the attention
+// kernels feed P as fp16 (11-bit mantissa) into the P.V tcgen05 MMA, which
+// needs both operands in the same format.
+__device__ __forceinline__ int4 bf16x8_to_f16x8(int4 v) {
+  uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xFFFF0000u);
+    const __half2 h = __floats2half2_rn(lo, hi);
+    w[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  return make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+}
+
+// one warp per (token, kv head): lanes 0-15 move K (bf16), lanes 16-31 move
+// V (bf16 in, fp16 stored), 16 bytes each (head_dim 128 = 256 B per row).
 __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __restrict__ bt,
                                  const int4* __restrict__ k, const int4* __restrict__ v,
                                  const int32_t* __restrict__ slots, const int32_t* __restrict__ pos,
@@ -29,7 +46,8 @@ __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __rest
   const int64_t half = page_bytes / 2;
   int4* dst = reinterpret_cast<int4*>(kv + (int64_t)page * page_bytes + which * half +
                                       ((int64_t)h * B + row) * 256) + (lane & 15);
-  *dst = *src;
+  const int4 val = *src;
+  *dst = which ? bf16x8_to_f16x8(val) : val;
 }
 
 }  // namespace kb

@@ -5,8 +5,8 @@
 // 128-row tile even though a GQA group has only 4-5 query heads:
 //   S^T[128 tok x 16]  = K_tile[128 tok x 128 d] . Q^T[128 d x 16 heads]
 //   O^T[128 d x 16]   += V^T[128 d x 128 tok] . P^T[128 tok x 16 heads]
-// Query heads >= G are padding; the spare N columns carry the bf16 residual
-// of P (P = P_hi + P_lo) so P.V keeps ~16 mantissa bits at no MMA cost.
+// Query heads >= G are padding.  The V cache is fp16 (kb_append.cu), so P
+// enters P.V as fp16 (11-bit mantissa).
 // K/V tiles are two 64-token pages (block_tokens 64) or one 128-token page,
 // staged by TMA with 128-byte swizzle straight from the pool pages named by
 // the block table; V is read as an MN-major operand (no transpose pass).
@@ -23,6 +23,7 @@
 // 5 MMA issuer + TMEM owner.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "kb_common.cuh"
 #include "kb_sm100.cuh"
@@ -143,7 +144,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
   } else if (warp == 5) {
     // ------------------------------------------------ MMA issuer
     constexpr uint32_t kIdQK = idesc_bf16_f32(128, 16, false, false);
-    constexpr uint32_t kIdPV = idesc_bf16_f32(128, 16, true, false);
+    constexpr uint32_t kIdPV = idesc_f16_f32(128, 16, true, false);  // V^T fp16, P^T fp16
     const uint32_t p_base = smem_u32(sP);
     // QK cursor runs one tile ahead of the PV cursor, across item borders
     int qr = 0, qt = 0, qj = 0;
@@ -216,6 +217,9 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       fence_proxy_async_smem();
       mbar_arrive(&misc->q_full[r & 1]);
     };
+    // both P buffers start zero: rows >= 8 (GQA padding) are never written
+    for (int c = tid; c < 2 * kPBytes / 16; c += 128)
+      reinterpret_cast<int4*>(sP)[c] = make_int4(0, 0, 0, 0);
     write_q(0);
     if (n_mine > 1) write_q(1);
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
@@ -238,11 +242,10 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       auto fold = [&](int x) {
         mbar_wait(&misc->o_full[x & 1], (x >> 1) & 1);
         tc_fence_after();
-        float ov[8], ol[8];
+        float ov[8];
         tmem_ld_32x32b_x8(tmem + lane_base + 32 + (x & 1) * 16, ov);
-        tmem_ld_32x32b_x8(tmem + lane_base + 40 + (x & 1) * 16, ol);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) o_acc[g] = o_acc[g] * alpha_hist[x & 1][g] + (ov[g] + ol[g]);
+        for (int g = 0; g < 8; ++g) o_acc[g] = o_acc[g] * alpha_hist[x & 1][g] + ov[g];
       };
       for (int t = 0; t < it.nt; ++t, ++j) {
         const int tile = it.t_beg + t;
@@ -303,17 +306,13 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
             }
           }
         }
-        // P^T -> SW128 K-major image in buffer j&1: row g = bf16(p), row
-        // 8+g = its bf16 residual.  PV of tile j-2 (same buffer) is done:
-        // it was folded above, or at the previous item's end.
+        // P^T -> SW128 K-major image in buffer j&1, fp16 (rows 8..15 stay
+        // zero).  PV of tile j-2 (same buffer) is done: it was folded above,
+        // or at the previous item's end.
         uint8_t* pbuf = sP + (j & 1) * kPBytes + (tid >> 6) * 2048;
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          const __nv_bfloat16 hi = __float2bfloat16(p[g]);
-          const __nv_bfloat16 lo = __float2bfloat16(p[g] - __bfloat162float(hi));
-          *reinterpret_cast<__nv_bfloat16*>(pbuf + sw128_offset(g, tid & 63)) = hi;
-          *reinterpret_cast<__nv_bfloat16*>(pbuf + sw128_offset(g + 8, tid & 63)) = lo;
-        }
+        for (int g = 0; g < 8; ++g)
+          *reinterpret_cast<__half*>(pbuf + sw128_offset(g, tid & 63)) = __float2half_rn(p[g]);
         fence_proxy_async_smem();
         mbar_arrive(&misc->p_full[j & 1]);
       }

@@ -10,10 +10,11 @@
 // K/V tile.  Per 128-key tile j and query tile t:
 //   S_t = Q_t . K_j^T                 (tcgen05, A and B from smem, K-major)
 //   P_t = exp2(S_t*scale - m_t)       (softmax warpgroup t, one row per thread)
-//   O_t += [P_t,hi | P_t,lo] . [V_j ; V_j]   (A = P from TMEM, B = V MN-major)
+//   O_t += P_t . V_j                  (A = P from TMEM, B = V MN-major)
 // S, P and O live in TMEM (S0 | S1 | O0 | O1 = 512 columns); P overwrites S
-// chunk by chunk, as bf16 hi + bf16 residual so P keeps ~16 mantissa bits
-// (a single bf16 P alone costs ~1.1e-3 relative error).  The two tiles
+// as fp16 pairs -- the V cache is stored fp16 (kb_append.cu) so P can be
+// fp16 (11-bit mantissa) in the same-format P.V MMA, where a bf16 P alone
+// costs ~1.1e-3 relative error.  The two tiles
 // ping-pong: the MMA warp issues QK0(j) QK1(j) PV0(j) QK0(j+1) PV1(j)
 // QK1(j+1) ..., so the tensor pipe works on one tile while the other tile's
 // softmax runs.  O is rescaled lazily, only when a row max grows by more
@@ -22,6 +23,7 @@
 // Warp roles (320 threads): 0-3 softmax tile 0, 4-7 softmax tile 1, 8 TMA
 // producer (K/V pages named by the block table), 9 MMA issuer + TMEM owner.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "kb_common.cuh"
 #include "kb_sm100.cuh"
@@ -138,7 +140,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
   } else if (warp == 9) {
     // ------------------------------------------------ MMA issuer
     constexpr uint32_t kIdQK = idesc_bf16_f32(128, 128, false, false);
-    constexpr uint32_t kIdPV = idesc_bf16_f32(128, 128, false, true);
+    constexpr uint32_t kIdPV = idesc_f16_f32(128, 128, false, true);  // P fp16, V fp16
     auto issue_qk = [&](int t, int j) {
       const int stage = j % kPfStages;
       if (t == 0) {
@@ -165,13 +167,11 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         const int stage = j % kPfStages;
         const uint32_t v_addr = smem_u32(smem + stage * kPfKV + 2 * kPfHalf);
         const uint32_t p_base = tmem + t * 128;
-        // 16-key group m: P_hi at column 32*(m/2) + 8*(m%2), P_lo 16 columns later
+        // 16-key group m: P (fp16 pairs) at TMEM column 8m, V rows 16m..16m+15
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
           const uint64_t b = sw128_desc(v_addr + m * 2048, kPfHalf, 1024);  // MN-major V
-          const uint32_t a_hi = p_base + 32 * (m >> 1) + 8 * (m & 1);
-          mma_f16_ts(tmem + 256 + t * 128, a_hi, b, kIdPV, (j > 0 || m > 0) ? 1u : 0u);
-          mma_f16_ts(tmem + 256 + t * 128, a_hi + 16, b, kIdPV, 1u);
+          mma_f16_ts(tmem + 256 + t * 128, p_base + 8 * m, b, kIdPV, (j > 0 || m > 0) ? 1u : 0u);
         }
         mma_commit(&misc->o_done[t]);
         if (t == 1) mma_commit(&misc->empty[stage]);
@@ -220,20 +220,25 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       const int warp_q0 = pre + row0 + t * kPfTile + (warp & 3) * 32;
       const bool full_tile = kbase + kPfTile - 1 <= warp_q0 &&
                              row0 + t * kPfTile + (warp & 3) * 32 + 31 < qlen;
-      // pass 1: row max of this key tile (on raw scores; scaled once)
+      // S row in two halves of 64 columns (two loads, one wait each)
       float mraw = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float part[32];
-        tmem_ld_32x32b_x32(s_addr + c * 32, part);
-        if (full_tile) {
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t sr[2][32];
+        tmem_ld_32x32b_x32_async(s_addr + hh * 64, sr[0]);
+        tmem_ld_32x32b_x32_async(s_addr + hh * 64 + 32, sr[1]);
+        tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, part[i]);
-        } else {
+        for (int c = 0; c < 2; ++c) {
+          if (full_tile) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const bool ok = row_ok && (kbase + c * 32 + i) <= qpos;
-            mraw = fmaxf(mraw, ok ? part[i] : -INFINITY);
+            for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, __uint_as_float(sr[c][i]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const bool ok = row_ok && (kbase + hh * 64 + c * 32 + i) <= qpos;
+              mraw = fmaxf(mraw, ok ? __uint_as_float(sr[c][i]) : -INFINITY);
+            }
           }
         }
       }
@@ -277,38 +282,36 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         }
         fence_proxy_async_smem();
       }
-      // pass 2: P = exp2(S*scale - m_ref) over S, 32 keys per chunk:
-      // columns [32c, 32c+16) = bf16x2 P_hi, [32c+16, 32c+32) = bf16x2 P_lo.
-      // P_hi = P truncated to bf16 (a mask), P_lo = bf16(P - P_hi) (exact
-      // remainder, rounded): P_hi + P_lo carries ~16 mantissa bits.
+      // pass 2: P = exp2(S*scale - m_ref) as fp16 pairs (the V cache is
+      // fp16, kb_append.cu), written over S: the 64 keys of S half hh land in
+      // P columns [32hh, 32hh + 32) -- columns whose S values were consumed.
       float rs = 0.f;
       const bool live = m_ref != -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float part[32];
-        tmem_ld_32x32b_x32(s_addr + c * 32, part);
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t sr[2][32];
+        tmem_ld_32x32b_x32_async(s_addr + hh * 64, sr[0]);
+        tmem_ld_32x32b_x32_async(s_addr + hh * 64 + 32, sr[1]);
+        tmem_ld_wait();
         uint32_t w[32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < 32; ++i) {
           float x[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            float v = fast_exp2(fmaf(part[2 * i + e], scale_log2, -m_ref));
+            const int col = 2 * i + e;  // 0..63 within the half
+            float v = fast_exp2(fmaf(__uint_as_float(sr[col >> 5][col & 31]), scale_log2, -m_ref));
             if (!full_tile) {
-              const int key = kbase + c * 32 + 2 * i + e;
+              const int key = kbase + hh * 64 + col;
               v = (row_ok && key <= qpos && live) ? v : 0.f;
             }
             x[e] = v;
           }
-          const uint32_t b0 = __float_as_uint(x[0]) & 0xFFFF0000u;
-          const uint32_t b1 = __float_as_uint(x[1]) & 0xFFFF0000u;
-          const __nv_bfloat162 lo =
-              __floats2bfloat162_rn(x[0] - __uint_as_float(b0), x[1] - __uint_as_float(b1));
           rs += x[0] + x[1];
-          w[i] = __byte_perm(b0, b1, 0x7632);
-          w[16 + i] = *reinterpret_cast<const uint32_t*>(&lo);
+          const __half2 hp = __floats2half2_rn(x[0], x[1]);
+          w[i] = *reinterpret_cast<const uint32_t*>(&hp);
         }
-        tmem_st_32x32b_x32(s_addr + c * 32, w);
+        tmem_st_32x32b_x32(s_addr + hh * 32, w);
       }
       tmem_st_wait();
       l_run += rs;

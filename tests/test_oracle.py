@@ -7,7 +7,8 @@ import numpy as np
 from conftest import load_golden
 from oracle import dropsim_port as ds
 from oracle.attention import bf16_to_f32, check_close, decode_ref, f32_to_bf16, prefill_ref
-from oracle.kvpool import RESERVED, OraclePool, copy_pages, gather_kv, kv_append
+from oracle.kvpool import (RESERVED, OraclePool, bf16_bits_to_f16_bits, copy_pages, gather_kv,
+                           kv_append)
 
 
 def make_pool(track=False):
@@ -103,7 +104,15 @@ def test_copy_and_append_roundtrip_bytes():
     kv_append(a, 1, k, v, [0] * 100, list(range(100)), n_kv_heads=1, block_tokens=64)
     copy_pages(b, a, [(0, 3, 0, 2, 2, 0, 4)])
     k2, v2 = gather_kv(b, 3, 1, 100, 1, 64)
-    assert (k2 == k).all() and (v2 == v).all()
+    assert (k2 == k).all() and (v2 == bf16_bits_to_f16_bits(v)).all()
+
+
+def test_v_cache_fp16_is_exact_for_bf16_activations():
+    # every bf16 value in fp16's normal range converts exactly
+    x = (np.random.default_rng(2).standard_normal(4096) * 8).astype(np.float32)
+    bits = f32_to_bf16(x)
+    f16 = bf16_bits_to_f16_bits(bits).view(np.float16).astype(np.float32)
+    assert (f16 == bf16_to_f32(bits)).all()
 
 
 def test_attention_refs_agree_with_each_other():
