@@ -139,6 +139,53 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def copy_sweep(rt, iters: int = 5) -> dict:
+    """Config 5 on one GPU: KV-block migration (scattered 256 KiB pages named
+    by block tables) and layer restore (contiguous slab ranges) from 64 KiB
+    to 2 GiB.  Same-GPU copies read and write HBM, so the payload roofline
+    is HBM/2; NVLink (peer pools) is 900 GB/s per direction nominal."""
+    import torch
+    from paper_2412_18169_b200 import runtime
+    from paper_2412_18169_b200.core import SHAPES
+    shape = SHAPES["llama3_8b"]
+    model = shape.spec()
+    rt2 = runtime.Runtime(rt.device, max_slots=4, max_pages_per_seq=8192)
+    a = rt2.create_pool(0, model, model.param_bytes + (2 << 30) + (64 << 20), shape)
+    b = rt2.create_pool(1, model, model.param_bytes + (2 << 30) + (64 << 20), shape)
+    pb = shape.page_bytes
+    npg = (2 << 30) // pb
+    assert a.grow([(0, 0, 1, npg)]) and b.grow([(0, 0, 1, npg)])
+    b.drop_layers(0, 5)
+    b.restore_begin(0, 5)  # a 5-slab (2.19 GB) pull target
+    out = {"pages": [], "slabs": []}
+    st = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    size = 64 << 10
+    while size <= (2 << 30):
+        n = max(1, size // pb)
+        for kind in ("pages", "slabs"):
+            def run():
+                if kind == "pages":
+                    runtime.copy_pages(b, a, [(0, 0, 0, 1, npg, 0, n)], stream=st)
+                else:
+                    runtime.copy_slabs(b, a, 0, 5, 0, size, stream=st)
+            run()
+            ev0.record(st)
+            for _ in range(iters):
+                run()
+            ev1.record(st)
+            ev1.synchronize()
+            ms = ev0.elapsed_time(ev1) / iters
+            moved = n * pb if kind == "pages" else size
+            out[kind].append([size, round(moved / (ms / 1e3) / 1e9, 1)])
+        size *= 4
+    b.restore_complete(0, 5)
+    a.close()
+    b.close()
+    out["unit"] = "payload GB/s (same GPU: read + write HBM)"
+    return out
+
+
 def prefill_measure(rt, tensor_peak: float, ctx: int = 32768, chunk: int = 2048,
                     iters: int = 3) -> dict:
     """Config 4 attention: one Qwen2.5-14B layer, a 32k-token prompt prefilled
@@ -353,8 +400,9 @@ def main():
 
     # P99 TTFT: the reference's scheduler on real pools with measured stage
     # times, KunServe vs the recompute baseline on one 4x burst
+    sweep = copy_sweep(rt) if ws == 1 else None
     ttft = None
-    if not args.no_ttft:
+    if not args.no_ttft and ws == 1:  # a single-GPU measurement (two replicas per GPU)
         from paper_2412_18169_b200.ttft import measure
         ttft = measure(kv_gib=1.0, base_rps=2.0)
 
@@ -400,6 +448,7 @@ def main():
                                    "read+write HBM)", "peak_source": peak_src},
             "paged_decode": dec,
             "paged_prefill": prefill,
+            "copy_sweep": sweep,
             "p99_ttft": ttft,
             "parity": parity,
             "e2e": {"value": round(e_moved / e2e_s / 1e9, 1), "unit": "GB/s",

@@ -55,9 +55,27 @@ def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None) -> dict:
            "exchanges": kinds.get("EXCHANGE", 0), "restores": kinds.get("RESTORE_DONE", 0),
            "rounds": kinds.get("ROUND", 0), "stages_measured": len(eng.stage_samples),
            "wall_s": round(wall, 1)}
+    out["cost_fit"] = fit_stage_samples(eng.stage_samples, shape.num_layers)
     for pool in eng.pools.values():
         pool.close()
     return out, eng.stage_samples
+
+
+def fit_stage_samples(samples, num_layers: int) -> dict:
+    """The reference's cost model (alpha*units + beta*tokens + gamma seconds
+    per microbatch, costmodel.py:50-69) least-squares fitted to the measured
+    B200 stage times, each scaled to the full model by L / stage layers --
+    the refit SURVEY.md 8f item 2 asks for."""
+    import numpy as np
+    if len(samples) < 3:
+        return None
+    m = np.array([[units, float(n), 1.0] for n, units, nd, layers, us in samples])
+    y = np.array([us * num_layers / layers / 1e6 for n, units, nd, layers, us in samples])
+    sol = np.maximum(np.linalg.lstsq(m, y, rcond=None)[0], 0.0)
+    rms = float(np.sqrt(np.mean((m @ sol - y) ** 2)))
+    return {"alpha": float(sol[0]), "beta": float(sol[1]), "gamma": float(sol[2]),
+            "rms_s": rms, "samples": len(samples),
+            "reference_defaults": {"alpha": 6.6e-9, "beta": 2.8e-6, "gamma": 9.6e-3}}
 
 
 def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b", **trace_kw) -> dict:
