@@ -173,7 +173,8 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
           const uint64_t b = sw128_desc(v_addr + m * 2048, kPfHalf, 1024);  // MN-major V
           mma_f16_ts(tmem + 256 + t * 128, p_base + 8 * m, b, kIdPV, (j > 0 || m > 0) ? 1u : 0u);
         }
-        mma_commit(&misc->o_done[t]);
+        // O_t is read only by the epilogue: signal once, after the last tile
+        if (j == nt - 1) mma_commit(&misc->o_done[t]);
         if (t == 1) mma_commit(&misc->empty[stage]);
       }
       __syncwarp();
@@ -319,7 +320,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       mbar_arrive(&misc->p_ready[t]);
     }
     // epilogue: O_t / l -> bf16 rows
-    mbar_wait(&misc->o_done[t], (nt - 1) & 1);
+    mbar_wait(&misc->o_done[t], 0);
     tc_fence_after();
     {
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
