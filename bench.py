@@ -404,7 +404,7 @@ def main():
     ttft = None
     if not args.no_ttft and ws == 1:  # a single-GPU measurement (two replicas per GPU)
         from paper_2412_18169_b200.ttft import measure
-        ttft = measure(kv_gib=1.25, base_rps=3.0)
+        ttft = measure(kv_gib=1.25, base_rps=3.0, output_mean=128)
 
     line = None
     if rank == 0:
