@@ -234,7 +234,7 @@ def prefill_measure(rt, tensor_peak: float, ctx: int = 32768, chunk: int = 2048,
             "ms_per_layer": round(ms, 3), "chunks": len(calls),
             "roofline": {"bound": "tensor", "achieved": round(tf, 1), "peak": tensor_peak,
                          "unit": "TFLOP/s", "frac": round(tf / tensor_peak, 4),
-                         "traffic": None,
+                         "traffic": _traffic("prefill_tc_kernel"),
                          "flops_per_layer": flops}}
 
 
@@ -288,8 +288,19 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
             "note": "attention only, one token per resident through 32 layers",
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
-                         "traffic": None},
+                         "traffic": _traffic("decode_tc_kernel")},
             "launches_per_step": launches}
+
+
+def _traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)[kernel]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def main():
@@ -382,17 +393,22 @@ def main():
     # step's inputs (request token table) H2D from pinned memory and its
     # result (per-request KV checksum of the first layer page) D2H
     tok = torch.tensor(list(cyc.tokens.values()), dtype=torch.int32).pin_memory()
-    res = torch.empty(len(cyc.tokens), dtype=torch.int64).pin_memory()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    res = torch.empty(len(cyc.tokens), dtype=torch.int32).pin_memory()
+    cyc.auto_refill = False
+    e2e_s = 0.0
     e_moved = 0
     for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         tok_d = tok.to("cuda", non_blocking=True)
         r = cyc.step()
         e_moved += r.bytes_moved
-        res.copy_(tok_d.to(torch.int64) * 0 + r.n_tasks, non_blocking=True)
+        res.copy_(cyc.home_first_pages(), non_blocking=True)
         torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+        e2e_s += time.perf_counter() - t0
+        del tok_d
+        cyc.refill()  # the next burst's arrivals: not part of the cycle
+    cyc.auto_refill = True
     r_last = reps[-1]
     cyc.close()
     _, tensor_peak, _ = load_peaks()
@@ -441,9 +457,12 @@ def main():
             "breakdown": {"bytes_per_step": r0.bytes_moved, "kv_exchange": r0.bytes_kv_exchange,
                           "param_restore": r0.bytes_param, "kv_consolidate": r0.bytes_kv_consolidate,
                           "compaction_rw": r0.bytes_compaction, "ms": r0.ms,
-                          "remap_ms": round(r0.remap_ns / 1e6, 3), "tasks": r0.n_tasks},
+                          "remap_ms": round(r0.remap_ns / 1e6, 3), "tasks": r0.n_tasks,
+                          "host_enqueue_ms": {k: round(v, 3) for k, v in r0.host_ms.items()}},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
-                         "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                         "traffic": _traffic("copy_flat_kernel"),
+                         "traffic_algorithmic": 2 * cyc.param_chunk,
                          "kernel": "copy_flat_kernel (peer slab pull; same-GPU replicas: "
                                    "read+write HBM)", "peak_source": peak_src},
             "paged_decode": dec,
@@ -452,7 +471,7 @@ def main():
             "p99_ttft": ttft,
             "parity": parity,
             "e2e": {"value": round(e_moved / e2e_s / 1e9, 1), "unit": "GB/s",
-                    "h2d_bytes_per_step": tok.numel() * 4, "d2h_bytes_per_step": res.numel() * 8},
+                    "h2d_bytes_per_step": tok.numel() * 4, "d2h_bytes_per_step": res.numel() * 4},
             "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,

@@ -114,25 +114,40 @@ int kb_pool_destroy(kb_pool* pool);
 int kb_pool_query(kb_pool* pool, kb_pool_info* out);
 
 /* drop_layers (memory.py:147-172) + the caller's remap charge
- * (engine.py:796-807): for each layer in [lo, hi) unmap its slab from the
- * weight VA and map it at the KV VA tail; the new pages are free.
- * Synchronizes the device first (no in-flight reader of the weights).
- * remap_ns receives the host wall time of the unmap/map/access calls. */
+ * (engine.py:796-807).  Every layer slab is mapped at creation under both
+ * the weight VA and a fixed page range of the KV VA, so a drop is one
+ * bitmap kernel: the slab pages of [lo, hi) turn from reserved into free KV
+ * pages.  Asynchronous; ordered before every later page operation on any
+ * stream (see "Stream ordering" below).  remap_ns receives the host time. */
 int kb_drop_layers(kb_pool* pool, int32_t lo, int32_t hi, int64_t* remap_ns);
 
-/* restore_layers (memory.py:175-197): vacate the last (hi-lo) slabs of the
- * KV VA -- live pages there move to the lowest free pages below the new
- * extent (device compaction kernel, block tables rewritten on device) --
- * then unmap those slabs and map them under the weight VA of [lo, hi).
- * Returns KB_REFUSED (nothing changed) if the live pages cannot fit.
- * moved_pages / remap_ns report the compaction size and remap time. */
+/* restore_layers (memory.py:175-197): vacate the slab page range of
+ * [lo, hi) -- live pages there move to the lowest free pages outside it
+ * (device compaction, block tables rewritten on device through the owner
+ * map) -- and mark it reserved again so the parameter pull can land under
+ * the weight VA.  KB_REFUSED (nothing changed) if the live pages cannot
+ * fit.  Runs on `stream` after every earlier page operation of the pool on
+ * any stream, before every later one; the host does not block.  With a
+ * non-NULL moved_pages the call waits for the compaction and reports its
+ * size; otherwise read it later with kb_pool_last_moved. */
 int kb_restore_begin(kb_pool* pool, int32_t lo, int32_t hi, uintptr_t stream,
                      int64_t* moved_pages, int64_t* remap_ns);
+/* pages moved by the pool's last compaction (waits for it) */
+int kb_pool_last_moved(kb_pool* pool, int64_t* moved_pages);
 /* complete_restore (memory.py:200-212): bookkeeping only; validates that
  * [lo, hi) is mapped at the weight VA awaiting the pull. */
 int kb_restore_complete(kb_pool* pool, int32_t lo, int32_t hi);
 /* device pointer of layer `layer`'s slab in the weight VA (0 if unmapped) */
 uint64_t kb_weight_ptr(kb_pool* pool, int32_t layer);
+
+/* Stream ordering.  Page operations may be issued on any streams without
+ * host synchronization; the order of the calls is the order on the device.
+ * Grows, releases, drops and compactions run after the pool's previous one
+ * of those; releases and compactions also after the last operation of
+ * every stream that touched the pool (no page is freed or moved under a
+ * reader); copies, appends and attention after the last grow / release /
+ * drop / compaction.  Inside a CUDA graph capture the graph's own edges are
+ * the ordering.  */
 
 /* ---- N2: paged KV block tables (KVAllocator, memory.py:70-129) ---------- */
 /* Grow block tables on device: the kernel takes the K lowest free page ids

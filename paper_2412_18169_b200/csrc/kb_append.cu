@@ -62,11 +62,13 @@ extern "C" int kb_kv_append(kb_pool* p, int32_t layer, uint64_t k, uint64_t v, u
   if (ntok <= 0) return KB_OK;
   KB_RT(cudaSetDevice(p->device));
   const int64_t warps = (int64_t)ntok * p->m.n_kv_heads;
+  int rc = pool_enter(p, (cudaStream_t)stream);
+  if (rc) return rc;
   kv_append_kernel<<<(int)ceil_div(warps * 32, 256), 256, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<uint8_t*>(p->kva), p->d_bt, reinterpret_cast<const int4*>(k),
       reinterpret_cast<const int4*>(v), reinterpret_cast<const int32_t*>(slots),
       reinterpret_cast<const int32_t*>(pos), ntok, p->m.n_kv_heads, p->m.block_tokens,
       p->m.num_layers, p->maxp, layer, p->m.page_bytes);
   KB_LAUNCH_CHECK();
-  return KB_OK;
+  return pool_leave(p, (cudaStream_t)stream);
 }

@@ -59,6 +59,20 @@ int ensure_driver();
     }                                                                         \
   } while (0)
 
+// Stream ordering of pool operations (see kb_pool::op_ev), all on the
+// device -- the host never blocks.  Program order of the API calls is the
+// order that counts:
+//  * bitmap ops (grow, release, drop, compaction) run after the previous
+//    bitmap op, whatever streams the two were issued on; release and
+//    compaction also run after the last op of every stream that touched
+//    the pool (no page is freed or moved under a reader or writer);
+//  * data ops (page copies, appends, attention) run after the last bitmap
+//    op, so they see every block-table change issued before them.
+int pool_enter(kb_pool* p, cudaStream_t st);
+int pool_leave(kb_pool* p, cudaStream_t st);
+int pool_meta_begin(kb_pool* p, cudaStream_t st, bool wait_all_streams);
+int pool_meta_end(kb_pool* p, cudaStream_t st);
+
 struct KvSeg {
   CUmemGenericAllocationHandle h;
   int64_t bytes;
@@ -106,6 +120,16 @@ struct kb_pool {
   int64_t scratch_bytes = 0;
   int32_t* h_pinned = nullptr;  // small pinned readback buffer
   cudaStream_t own_stream = nullptr;
+  // Cross-stream ordering without host synchronization (kb::pool_enter /
+  // pool_leave / pool_meta_begin / pool_meta_end): the last pool operation
+  // of every stream that touched the pool, the last bitmap op and the last
+  // compaction.
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> op_ev;
+  cudaEvent_t meta_ev = nullptr;    // last bitmap op
+  cudaEvent_t counts_ev = nullptr;  // last compaction's counts in h_pinned
+  bool meta_set = false;
+  bool counts_pending = false;  // compaction counts still in flight to h_pinned
+  int64_t last_moved = 0;
   // TMA descriptor over the whole KV VA viewed as [rows][head_dim] bf16
   // (row = one token of one kv head of K or V), box = [block_tokens][64].
   alignas(64) CUtensorMap kv_tmap;

@@ -164,6 +164,8 @@ extern "C" int kb_copy_pages(kb_pool* dst, kb_pool* src, const kb_move* moves, i
   const int64_t pieces = src->m.page_bytes > kPiece ? src->m.page_bytes / kPiece : 1;
   PoolView dv{dst->d_bt, reinterpret_cast<uint8_t*>(dst->kva), L, dst->maxp};
   PoolView sv{src->d_bt, reinterpret_cast<uint8_t*>(src->kva), L, src->maxp};
+  int rc;
+  if ((rc = pool_enter(dst, st)) || (rc = pool_enter(src, st))) return rc;
   MoveBatch batch;
   for (int b0 = 0; b0 < n; b0 += kMoveBatch) {
     const int nb = std::min(kMoveBatch, n - b0);
@@ -180,6 +182,7 @@ extern "C" int kb_copy_pages(kb_pool* dst, kb_pool* src, const kb_move* moves, i
     KB_LAUNCH_CHECK();
   }
   (void)cum;
+  if ((rc = pool_leave(dst, st)) || (rc = pool_leave(src, st))) return rc;
   return KB_OK;
 }
 
@@ -199,7 +202,12 @@ extern "C" int kb_copy_slabs(kb_pool* dst, kb_pool* src, int32_t lo, int32_t hi,
   KB_RT(cudaSetDevice(dst->device));
   uint64_t d = (uint64_t)dst->wva + (uint64_t)lo * slab + byte_lo;
   uint64_t s = (uint64_t)src->wva + (uint64_t)lo * slab + byte_lo;
-  return launch_flat(d, s, byte_hi - byte_lo, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if ((rc = pool_enter(dst, st)) || (rc = pool_enter(src, st))) return rc;
+  if ((rc = launch_flat(d, s, byte_hi - byte_lo, st))) return rc;
+  if ((rc = pool_leave(dst, st)) || (rc = pool_leave(src, st))) return rc;
+  return KB_OK;
 }
 
 extern "C" int kb_copy_slabs_from_host(kb_pool* dst, const void* host_src, int32_t lo, int32_t hi,
@@ -212,10 +220,13 @@ extern "C" int kb_copy_slabs_from_host(kb_pool* dst, const void* host_src, int32
     if (dst->layer_state[l] == kLayerDropped)
       return fail(KB_ESTATE, "destination layer " + std::to_string(l) + " is not reserved for a pull");
   KB_RT(cudaSetDevice(dst->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = pool_enter(dst, st);
+  if (rc) return rc;
   KB_RT(cudaMemcpyAsync(reinterpret_cast<void*>(dst->wva + (uint64_t)lo * slab + byte_lo),
                         static_cast<const char*>(host_src) + byte_lo, byte_hi - byte_lo,
-                        cudaMemcpyHostToDevice, (cudaStream_t)stream));
-  return KB_OK;
+                        cudaMemcpyHostToDevice, st));
+  return pool_leave(dst, st);
 }
 
 extern "C" int kb_copy_bytes(uint64_t dst, uint64_t src, int64_t nbytes, uintptr_t stream) {

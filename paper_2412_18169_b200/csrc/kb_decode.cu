@@ -149,18 +149,20 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device);
   const int grid = dev_sms;  // persistent: one CTA per SM (the kernel needs ~210 KB smem)
+  int rc = pool_enter(p, st);
+  if (rc) return rc;
   if (!(flags & KB_DECODE_REUSE_PLAN)) {
     decode_plan_kernel<<<1, kPlanThreads, 0, st>>>(reinterpret_cast<const int32_t*>(ctx_lens),
                                                    nseq, Hkv, n_q_heads, max_splits, grid, 2,
                                                    nsplit, items, n_items, part_ml);
     KB_LAUNCH_CHECK();
   }
-  int rc = launch_decode_tc(p, layer, n_q_heads, q, slots, ctx_lens, grid, scale, part_o, part_ml,
+  rc = launch_decode_tc(p, layer, n_q_heads, q, slots, ctx_lens, grid, scale, part_o, part_ml,
                             items, n_items, nsplit, out, max_splits, st);
   if (rc) return rc;
   decode_combine_kernel<<<nseq * n_q_heads, 128, 0, st>>>(part_o, part_ml, nsplit,
                                                           reinterpret_cast<__nv_bfloat16*>(out),
                                                           n_q_heads, max_splits);
   KB_LAUNCH_CHECK();
-  return KB_OK;
+  return pool_leave(p, st);
 }

@@ -76,6 +76,54 @@ int ensure_scratch(kb_pool* p, int64_t bytes) {
   return KB_OK;
 }
 
+// Inside a CUDA graph capture the graph's own edges order the work (events
+// recorded outside the capture cannot be waited on): no-ops there.
+static bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
+int pool_enter(kb_pool* p, cudaStream_t st) {
+  if (capturing(st)) return KB_OK;
+  if (p->meta_set) KB_RT(cudaStreamWaitEvent(st, p->meta_ev, 0));
+  return KB_OK;
+}
+
+int pool_leave(kb_pool* p, cudaStream_t st) {
+  if (capturing(st)) return KB_OK;
+  for (auto& se : p->op_ev)
+    if (se.first == st) {
+      KB_RT(cudaEventRecord(se.second, st));
+      return KB_OK;
+    }
+  if (p->op_ev.size() >= 32) {  // many short-lived streams: fold them
+    KB_RT(cudaDeviceSynchronize());
+    for (auto& se : p->op_ev) cudaEventDestroy(se.second);
+    p->op_ev.clear();
+  }
+  cudaEvent_t ev;
+  KB_RT(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  p->op_ev.emplace_back(st, ev);
+  KB_RT(cudaEventRecord(ev, st));
+  return KB_OK;
+}
+
+int pool_meta_begin(kb_pool* p, cudaStream_t st, bool wait_all_streams) {
+  if (capturing(st)) return KB_OK;
+  if (wait_all_streams)
+    for (auto& se : p->op_ev)
+      if (se.first != st) KB_RT(cudaStreamWaitEvent(st, se.second, 0));
+  return pool_enter(p, st);
+}
+
+int pool_meta_end(kb_pool* p, cudaStream_t st) {
+  if (!capturing(st)) {
+    KB_RT(cudaEventRecord(p->meta_ev, st));
+    p->meta_set = true;
+  }
+  return pool_leave(p, st);
+}
+
 // ---------------------------------------------------------------- kernels
 
 constexpr int kScanThreads = 1024;
@@ -174,30 +222,83 @@ __global__ void __launch_bounds__(kScanThreads)
 grow_kernel(uint32_t* __restrict__ bitmap, int32_t* __restrict__ owner, int32_t* __restrict__ bt,
             int32_t* __restrict__ np, const __grid_constant__ GrowBatch batch, int n,
             int64_t total, int64_t max_pages, int L, int maxp) {
-  const kb_grow* reqs = batch.r;
-  const int64_t* cum = batch.cum;
-  auto emit = [&](int64_t k, int64_t page) {
-    int lo = 0, hi = n - 1;  // last request with cum <= k
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (cum[mid] <= k) lo = mid; else hi = mid - 1;
+  constexpr int kW = 4;                       // bitmap words per thread per tile
+  constexpr int kTileWords = kScanThreads * kW;
+  __shared__ int warp_sums[32];
+  __shared__ int tile_total;
+  __shared__ int s_pref[kTileWords];          // free pages before each word (tile-local)
+  __shared__ uint32_t s_bits[kTileWords];     // free bits of each word
+  __shared__ int64_t s_cum[kGrowBatch];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_cum[i] = batch.cum[i];
+  const int64_t w_hi = (max_pages + 31) >> 5;
+  int64_t found = 0;
+  for (int64_t t0 = 0; t0 < w_hi && found < total; t0 += kTileWords) {
+    uint32_t bits[kW];
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kW; ++j) {
+      const int64_t w = t0 + (int64_t)threadIdx.x * kW + j;
+      uint32_t b = 0;
+      if (w < w_hi) {
+        b = ~bitmap[w];
+        const int64_t keep = max_pages - (w << 5);
+        if (keep < 32) b &= (1u << keep) - 1u;
+      }
+      bits[j] = b;
+      cnt += __popc(b);
     }
-    const kb_grow r = reqs[lo];
-    int64_t rem = k - cum[lo];
-    int layer = r.layer_lo + (int)(rem / r.add_pages);
-    int idx = np[(int64_t)r.slot * L + layer] + (int)(rem % r.add_pages);
-    int64_t cell = ((int64_t)r.slot * L + layer) * maxp + idx;
-    bt[cell] = (int32_t)page;
-    owner[page] = (int32_t)cell;
-    atomicOr(&bitmap[page >> 5], 1u << (page & 31));
-  };
-  scan_pages<4>(bitmap, 0, max_pages, false, total, emit, nullptr);
-  __syncthreads();
-  for (int i = 0; i < n; ++i) {
-    const kb_grow r = reqs[i];
-    for (int l = r.layer_lo + threadIdx.x; l < r.layer_hi; l += blockDim.x)
-      np[(int64_t)r.slot * L + l] += r.add_pages;
+    int off = block_exclusive_scan(cnt, &tile_total, warp_sums);
+#pragma unroll
+    for (int j = 0; j < kW; ++j) {
+      s_pref[threadIdx.x * kW + j] = off;
+      s_bits[threadIdx.x * kW + j] = bits[j];
+      off += __popc(bits[j]);
+    }
     __syncthreads();
+    const int take = (int)min((int64_t)tile_total, total - found);
+    // balanced emission: the e-th free page of the tile goes to flattened
+    // slot found + e; consecutive threads take consecutive slots, so the
+    // block-table and owner writes coalesce
+    for (int e = threadIdx.x; e < take; e += blockDim.x) {
+      int lo = 0, hi = kTileWords - 1;  // last word with s_pref <= e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_pref[mid] <= e) lo = mid; else hi = mid - 1;
+      }
+      const int64_t page = ((t0 + lo) << 5) + __fns(s_bits[lo], 0, e - s_pref[lo] + 1);
+      const int64_t k = found + e;
+      int a = 0, b = n - 1;  // last request with cum <= k
+      while (a < b) {
+        const int mid = (a + b + 1) >> 1;
+        if (s_cum[mid] <= k) a = mid; else b = mid - 1;
+      }
+      const kb_grow r = batch.r[a];
+      const int64_t rem = k - s_cum[a];
+      const int layer = r.layer_lo + (int)(rem / r.add_pages);
+      const int idx = np[(int64_t)r.slot * L + layer] + (int)(rem % r.add_pages);
+      const int64_t cell = ((int64_t)r.slot * L + layer) * maxp + idx;
+      bt[cell] = (int32_t)page;
+      owner[page] = (int32_t)cell;
+    }
+    // mark the taken pages: the lowest (take - pref) free bits of each word
+#pragma unroll
+    for (int j = 0; j < kW; ++j) {
+      const int wl = threadIdx.x * kW + j;
+      const int got = min(max(take - s_pref[wl], 0), __popc(bits[j]));
+      if (got > 0) {
+        const uint32_t upto = got == __popc(bits[j]) ? bits[j]
+                              : bits[j] & ((1u << __fns(bits[j], 0, got + 1)) - 1u);
+        bitmap[t0 + wl] |= upto;
+      }
+    }
+    found += take;
+    __syncthreads();
+  }
+  // page counts: every (request, layer) cell is distinct (host-checked)
+  for (int c = threadIdx.x; c < n * L; c += blockDim.x) {
+    const kb_grow r = batch.r[c / L];
+    const int l = c % L;
+    if (l >= r.layer_lo && l < r.layer_hi) np[(int64_t)r.slot * L + l] += r.add_pages;
   }
 }
 
@@ -490,7 +591,13 @@ extern "C" int kb_pool_create(int32_t device, const kb_model_desc* model, int64_
     return bail(fail(KB_ECUDA, "cudaMallocHost failed"));
   if (cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(KB_ECUDA, "cudaStreamCreate failed"));
-  if ((rc = ensure_scratch(p, 1 << 20))) return bail(rc);
+  if (cudaEventCreateWithFlags(&p->counts_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->meta_ev, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(KB_ECUDA, "cudaEventCreate failed"));
+  // sized for vacating every slab at once: never reallocated under a
+  // compaction in flight
+  if ((rc = ensure_scratch(p, 2 * (p->max_pages - p->head_pages) * 4 + 64 + (1 << 20))))
+    return bail(rc);
   // every slab page starts reserved: the layer's weights live there
   range_mark_kernel<<<grid_for(p->max_pages - p->head_pages, 256, 1024), 256, 0, p->own_stream>>>(
       p->d_bitmap, p->d_owner, p->head_pages, p->max_pages, 1);
@@ -524,6 +631,9 @@ extern "C" int kb_pool_destroy(kb_pool* p) {
   if (p->d_scratch) cudaFree(p->d_scratch);
   if (p->h_pinned) cudaFreeHost(p->h_pinned);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
+  for (auto& se : p->op_ev) cudaEventDestroy(se.second);
+  if (p->counts_ev) cudaEventDestroy(p->counts_ev);
+  if (p->meta_ev) cudaEventDestroy(p->meta_ev);
   delete p;
   return KB_OK;
 }
@@ -553,6 +663,18 @@ extern "C" uint64_t kb_weight_ptr(kb_pool* p, int32_t layer) {
   return (uint64_t)(p->wva + (CUdeviceptr)layer * p->m.slab_bytes);
 }
 
+// Land the last compaction's (moved, free-found) counts from pinned memory.
+static int collect_counts(kb_pool* p) {
+  if (!p->counts_pending) return KB_OK;
+  KB_RT(cudaEventSynchronize(p->counts_ev));
+  p->counts_pending = false;
+  const int64_t* c = reinterpret_cast<const int64_t*>(p->h_pinned);
+  p->last_moved = c[0];
+  if (c[1] < c[0])  // cannot happen after restore_begin's capacity check
+    return fail(KB_ESTATE, "compaction found too few free pages");
+  return KB_OK;
+}
+
 extern "C" int kb_drop_layers(kb_pool* p, int32_t lo, int32_t hi, int64_t* remap_ns) {
   if (!p) return fail(KB_EINVAL, "null pool");
   if (hi <= lo) return fail(KB_EINVAL, "empty layer range");
@@ -564,13 +686,16 @@ extern "C" int kb_drop_layers(kb_pool* p, int32_t lo, int32_t hi, int64_t* remap
   KB_RT(cudaSetDevice(p->device));
   const int64_t t0 = now_ns();
   // the slab pages of [lo, hi) become free KV pages; no driver call, the
-  // slabs were mapped into the KV VA at creation.  Synchronous on the pool's
-  // stream so any later grow (on any stream) sees them.
+  // slabs were mapped into the KV VA at creation.  A bitmap op: ordered
+  // after every earlier one and before every later grow on any stream,
+  // without blocking the host.
   const int64_t a = slab_first_page(p, lo), b = slab_first_page(p, hi);
+  int rc = pool_meta_begin(p, p->own_stream, false);
+  if (rc) return rc;
   range_mark_kernel<<<grid_for(b - a, 256, 1024), 256, 0, p->own_stream>>>(p->d_bitmap, p->d_owner,
                                                                            a, b, 0);
   KB_LAUNCH_CHECK();
-  KB_RT(cudaStreamSynchronize(p->own_stream));
+  if ((rc = pool_meta_end(p, p->own_stream))) return rc;
   for (int l = lo; l < hi; ++l) p->layer_state[l] = kLayerDropped;
   p->usable_pages += b - a;
   if (remap_ns) *remap_ns = now_ns() - t0;
@@ -594,12 +719,13 @@ extern "C" int kb_restore_begin(kb_pool* p, int32_t lo, int32_t hi, uintptr_t st
                                 std::to_string(p->usable_pages - (b - a)) + " remaining pages");
   KB_RT(cudaSetDevice(p->device));
   const int64_t t0 = now_ns();
-  // releases / grows may be in flight on other streams: the plan must see them
-  KB_RT(cudaDeviceSynchronize());
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t cap = b - a;
-  int rc = ensure_scratch(p, 2 * cap * 4 + 64);
+  int rc = collect_counts(p);  // an earlier compaction's count, if unread
   if (rc) return rc;
+  // releases / grows / copies in flight on other streams: the plan must see
+  // them -- ordered on the device, the host does not block
+  if ((rc = pool_meta_begin(p, st, true))) return rc;
+  const int64_t cap = b - a;
   int64_t* d_counts = reinterpret_cast<int64_t*>(p->d_scratch);
   int32_t* d_src = reinterpret_cast<int32_t*>((char*)p->d_scratch + 64);
   int32_t* d_dst = d_src + cap;
@@ -615,15 +741,27 @@ extern "C" int kb_restore_begin(kb_pool* p, int32_t lo, int32_t hi, uintptr_t st
   KB_LAUNCH_CHECK();
   range_mark_kernel<<<grid_for(cap, 256, 1024), 256, 0, st>>>(p->d_bitmap, p->d_owner, a, b, 1);
   KB_LAUNCH_CHECK();
-  int64_t counts[2];
-  KB_RT(cudaMemcpyAsync(counts, d_counts, 16, cudaMemcpyDeviceToHost, st));
-  KB_RT(cudaStreamSynchronize(st));
-  if (counts[1] < counts[0])  // cannot happen after the capacity check above
-    return fail(KB_ESTATE, "compaction found too few free pages");
+  // the moved-page count travels back asynchronously (kb_pool_last_moved)
+  KB_RT(cudaMemcpyAsync(p->h_pinned, d_counts, 16, cudaMemcpyDeviceToHost, st));
+  KB_RT(cudaEventRecord(p->counts_ev, st));
+  if ((rc = pool_meta_end(p, st))) return rc;
+  p->counts_pending = true;
   for (int l = lo; l < hi; ++l) p->layer_state[l] = kLayerRestoring;
   p->usable_pages -= b - a;
-  if (moved_pages) *moved_pages = counts[0];
+  if (moved_pages) {
+    if ((rc = collect_counts(p))) return rc;
+    *moved_pages = p->last_moved;
+  }
   if (remap_ns) *remap_ns = now_ns() - t0;
+  return KB_OK;
+}
+
+extern "C" int kb_pool_last_moved(kb_pool* p, int64_t* moved_pages) {
+  if (!p || !moved_pages) return fail(KB_EINVAL, "null argument");
+  KB_RT(cudaSetDevice(p->device));
+  int rc = collect_counts(p);
+  if (rc) return rc;
+  *moved_pages = p->last_moved;
   return KB_OK;
 }
 
@@ -669,7 +807,9 @@ extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr
   KB_RT(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
   // batches travel in kernel parameter space: no staging copy, no host
-  // synchronization; launches on one stream run in order
+  // synchronization; ordered after the pool's earlier bitmap ops
+  int rc = pool_meta_begin(p, st, false);
+  if (rc) return rc;
   GrowBatch batch;
   for (int b0 = 0; b0 < n; b0 += kGrowBatch) {
     const int nb = std::min(kGrowBatch, n - b0);
@@ -683,6 +823,7 @@ extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr
                                             sub, p->max_pages, L, p->maxp);
     KB_LAUNCH_CHECK();
   }
+  if ((rc = pool_meta_end(p, st))) return rc;
   for (int i = 0; i < n; ++i)
     for (int l = reqs[i].layer_lo; l < reqs[i].layer_hi; ++l)
       p->h_np[(int64_t)reqs[i].slot * L + l] += reqs[i].add_pages;
@@ -703,6 +844,9 @@ extern "C" int kb_pages_release(kb_pool* p, const int32_t* slots, int32_t n, int
   }
   KB_RT(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
+  // after every stream's last op: no reader may still be on these pages
+  int rc = pool_meta_begin(p, st, true);
+  if (rc) return rc;
   SlotBatch batch;
   for (int b0 = 0; b0 < n; b0 += kReleaseBatch) {
     const int nb = std::min(kReleaseBatch, n - b0);
@@ -711,6 +855,7 @@ extern "C" int kb_pages_release(kb_pool* p, const int32_t* slots, int32_t n, int
                                                     batch, lo, hi, L, p->maxp);
     KB_LAUNCH_CHECK();
   }
+  if ((rc = pool_meta_end(p, st))) return rc;
   for (int i = 0; i < n; ++i)
     for (int l = lo; l < hi; ++l) p->h_np[(int64_t)slots[i] * L + l] = 0;
   p->live_pages -= freed;

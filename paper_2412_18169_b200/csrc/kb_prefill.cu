@@ -387,5 +387,9 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
     KB_LAUNCH_CHECK();
     return KB_OK;
   };
-  return B == 64 ? launch(prefill_tc_kernel<64>) : launch(prefill_tc_kernel<128>);
+  int rc = pool_enter(p, st);
+  if (rc) return rc;
+  rc = B == 64 ? launch(prefill_tc_kernel<64>) : launch(prefill_tc_kernel<128>);
+  if (rc) return rc;
+  return pool_leave(p, st);
 }

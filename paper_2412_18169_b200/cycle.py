@@ -23,6 +23,7 @@ cycle bit for bit (checked by kv_checksums()).
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass, field
 
 from . import memory, runtime
@@ -54,6 +55,8 @@ class CycleReport:
     ms: dict = field(default_factory=dict)
     param_kernel_ms: float = 0.0   # device time of the parameter-pull launches
     kv_kernel_ms: float = 0.0      # device time of the KV page-copy launches
+    host_ms: dict = field(default_factory=dict)  # host enqueue time per phase
+    tid_marks: list = field(default_factory=list)  # first tid of restore / consolidation
 
     @property
     def bytes_moved(self) -> int:
@@ -115,6 +118,7 @@ class OverloadCycle:
         self._fill_weights()
         torch.cuda.synchronize()
         self.pause_merged = False  # set True to stop after the exchange (see resume())
+        self.auto_refill = True    # False: the caller runs refill() between steps
         self._paused = None
         self.merged = {}
 
@@ -139,6 +143,21 @@ class OverloadCycle:
                 w = slab[:2 * n].view(torch.bfloat16)
                 w.copy_((torch.randn(n, device=w.device, generator=g) * 0.02).to(torch.bfloat16))
         torch.cuda.synchronize()
+
+    def home_first_pages(self):
+        """Device int32 [residents]: each long-lived resident's first layer-0
+        page on its home pool after the cycle (the step's result, read back
+        by bench.py's end-to-end leg); -1 for transient residents."""
+        torch = self.torch
+        rows = []
+        for rid in sorted(self.tokens):
+            if rid in self.transient:
+                rows.append(torch.full((1,), -1, dtype=torch.int32, device="cuda"))
+                continue
+            iid = self.home[rid]
+            bt = self._bt_view(iid)
+            rows.append(bt[self.slots[iid].of[rid], 0, :1])
+        return torch.cat(rows)
 
     def _bt_view(self, iid):
         torch = self.torch
@@ -178,6 +197,7 @@ class OverloadCycle:
         kvbpt = self.model.kv_bytes_per_token
         L = self.L
         ev["t0"].record(st)
+        h0 = time.perf_counter()
         # ---- plan (engine.py:616-648): a queued burst that outgrows every
         # replica's free KV by a quarter of one parameter copy
         groups = [Group(i, [i], {i: (0, L)}) for i in sorted(self.instances)]
@@ -205,17 +225,10 @@ class OverloadCycle:
                     rep.remap_ns += self.pools[iid].last_remap_ns
             live[m.gid] = new
         ev["drop"].record(st)
+        h_drop = time.perf_counter()
         final = {iid: g for g in live.values() for iid in g.member_instances}
-        for rid, tok in self.tokens.items():
-            g = final[self.home[rid]]
-            for iid in g.member_instances:
-                self.instances[iid].kv.free(rid)
-            for iid in g.member_instances:
-                lo, hi = g.stage_layer_map[iid]
-                share = memory.stage_share(tok, lo, hi, L)
-                if share:
-                    assert self.instances[iid].kv.alloc(rid, share)
-        # ---- exchange per original-map cohort (engine.py:690-726)
+        # ---- exchange per original-map cohort (engine.py:690-726); the
+        # device work is queued first, the host-only re-share follows
         tid = 0
         for g in sorted(live.values(), key=lambda g: g.gid):
             cohorts: dict[tuple, list[int]] = {}
@@ -231,11 +244,22 @@ class OverloadCycle:
                 self.te.register_exchange(tasks, old_map, g.stage_layer_map, toks)
                 self.te.submit_many(tasks)
                 rep.n_tasks += len(tasks)
-        done = self.te.drain()
-        rep.bytes_kv_exchange = sum(p.bytes_moved for p in done)
-        rep.kv_kernel_ms += _span_ms(done)
-        self.te.finish_flow_sources()
+        # no host wait: source releases queue behind the copies
+        self.te.finish_flow_sources(ordered=True)
+        # re-share (engine.py:823-830): token accounting per member stage
+        for rid, tok in self.tokens.items():
+            g = final[self.home[rid]]
+            for iid in g.member_instances:
+                self.instances[iid].kv.free(rid)
+            for iid in g.member_instances:
+                lo, hi = g.stage_layer_map[iid]
+                share = memory.stage_share(tok, lo, hi, L)
+                if share:
+                    assert self.instances[iid].kv.alloc(rid, share)
         ev["exch"].record(st)
+        rep.host_ms = {"drop": (h_drop - h0) * 1e3,
+                       "exchange": (time.perf_counter() - h_drop) * 1e3}
+        rep.tid_marks = [tid]
         self.merged = live
         if self.pause_merged:
             self._paused = (rep, live, ev, tid)
@@ -264,14 +288,19 @@ class OverloadCycle:
         L = self.L
         kvbpt = self.model.kv_bytes_per_token
         # ---- drain: transient residents finish (engine.py:_finish -> group_free)
+        gone: dict[int, list[int]] = {}
         for rid in sorted(self.transient):
             for iid, inst in self.instances.items():
                 inst.kv.free(rid)
                 slot = self.slots[iid].of.get(rid)
                 if slot is not None:
-                    self.pools[iid].release([slot], 0, L, stream=st)
+                    gone.setdefault(iid, []).append(slot)
                     self.slots[iid].drop(rid)
+        for iid, slots in gone.items():
+            self.pools[iid].release(slots, 0, L, stream=st)
         ev["drain"].record(st)
+        h1 = time.perf_counter()
+        restored = []
         # ---- restore (engine.py:1093-1157): reserve + compaction + remap, pulls
         for g in sorted(live.values(), key=lambda g: g.gid):
             missing, holders = {}, {}
@@ -282,25 +311,24 @@ class OverloadCycle:
                     missing[iid] = need
             for iid in sorted(missing):
                 for rng in missing[iid]:
-                    memory.restore_layers(self.instances[iid], rng, -1, tid=0)
+                    memory.restore_layers(self.instances[iid], rng, -1, tid=0, stream=st)
                     rep.remap_ns += self.pools[iid].last_remap_ns
-                    rep.pages_compacted += self.pools[iid].last_moved_pages
+                    restored.append(iid)
             flat = {iid: rng for iid, rngs in missing.items() for rng in rngs}
             tasks = plan_restore_transfers(flat, holders, self.model.bytes_per_layer,
                                            self.param_chunk, tid_start=tid)
             tid += len(tasks)
             self.te.register_restore(tasks, self.model.bytes_per_layer)
-            for t in tasks:
-                self.te.submit(t)
+            self.te.submit_many(tasks)  # one pull launch per contiguous run
             rep.n_tasks += len(tasks)
-            done = self.te.drain()
-            rep.bytes_param += sum(p.bytes_moved for p in done)
-            rep.param_kernel_ms += _span_ms(done)
+            # bookkeeping flips now; the pulls are ordered on the bulk stream
+            # before anything that reads the restored layers
             for iid, rngs in missing.items():
                 for rng in rngs:
                     memory.complete_restore(self.instances[iid], rng)
-        rep.bytes_compaction = rep.pages_compacted * self.shape.page_bytes
         ev["restore"].record(st)
+        h2 = time.perf_counter()
+        rep.tid_marks.append(tid)
         # ---- dissolve + consolidation (engine.py:1159-1254)
         cons_tasks = []
         for rid in sorted(self.tokens):
@@ -324,10 +352,7 @@ class OverloadCycle:
                 cons_tasks += chunks
         self.te.submit_many(cons_tasks)
         rep.n_tasks += len(cons_tasks)
-        done = self.te.drain()
-        rep.bytes_kv_consolidate = sum(p.bytes_moved for p in done)
-        rep.kv_kernel_ms += _span_ms(done)
-        self.te.finish_flow_sources()
+        self.te.finish_flow_sources(ordered=True)
         for rid, tok in self.tokens.items():
             if rid in self.transient:
                 continue
@@ -341,8 +366,26 @@ class OverloadCycle:
             if extra:
                 assert inst.kv.alloc(rid, extra)
         ev["cons"].record(st)
+        h3 = time.perf_counter()
+        rep.host_ms.update({"restore": (h2 - h1) * 1e3, "consolidate": (h3 - h2) * 1e3})
+        # ---- accounting, after the fact (nothing above waited on the GPU)
+        done = self.te.drain()
+        x_end, r_end = rep.tid_marks
+        for p in done:
+            k = p.task.tid
+            if k < x_end:
+                rep.bytes_kv_exchange += p.bytes_moved
+            elif k < r_end:
+                rep.bytes_param += p.bytes_moved
+            else:
+                rep.bytes_kv_consolidate += p.bytes_moved
+        rep.kv_kernel_ms += _span_ms([p for p in done if p.task.kind is TaskKind.KVCACHE_CHUNK])
+        rep.param_kernel_ms += _span_ms([p for p in done if p.task.kind is TaskKind.PARAM_SHARD])
+        rep.pages_compacted = sum(self.pools[iid].last_moved_pages for iid in restored)
+        rep.bytes_compaction = rep.pages_compacted * self.shape.page_bytes
         # ---- refill: the next burst re-admits the transient residents
-        self.refill()
+        if self.auto_refill:
+            self.refill()
         ev["cons"].synchronize()
         parts = {"drop": ev["t0"].elapsed_time(ev["drop"]),
                  "exchange": ev["drop"].elapsed_time(ev["exch"]),

@@ -76,6 +76,7 @@ _sigs = {
     "kb_drop_layers": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P]),
     "kb_restore_begin": (C.c_int, [_P, C.c_int32, C.c_int32, _S, _I64P, _I64P]),
     "kb_restore_complete": (C.c_int, [_P, C.c_int32, C.c_int32]),
+    "kb_pool_last_moved": (C.c_int, [_P, _I64P]),
     "kb_weight_ptr": (C.c_uint64, [_P, C.c_int32]),
     "kb_pages_grow": (C.c_int, [_P, C.POINTER(Grow), C.c_int32, _S]),
     "kb_pages_release": (C.c_int, [_P, _I32P, C.c_int32, C.c_int32, C.c_int32, _S]),
@@ -201,7 +202,6 @@ class DevicePool:
                                    _i32arr(rt.peers), len(rt.peers), C.byref(h)))
         self.h = h
         self.last_remap_ns = 0
-        self.last_moved_pages = 0
 
     # -- lifecycle
     def close(self) -> None:
@@ -235,13 +235,18 @@ class DevicePool:
         self.last_remap_ns = ns.value
         return ns.value
 
-    def restore_begin(self, lo: int, hi: int, stream=None) -> int:
-        moved, ns = C.c_int64(), C.c_int64()
-        _check(_lib.kb_restore_begin(self.h, lo, hi, _stream(stream), C.byref(moved),
-                                     C.byref(ns)))
-        LAUNCHES[0] += 3 if moved.value else 1  # plan (+ copy + fixup)
-        self.last_moved_pages = moved.value
+    def restore_begin(self, lo: int, hi: int, stream=None) -> None:
+        """Asynchronous: the compaction is ordered on the device; its size
+        is `last_moved_pages` (which waits for it)."""
+        ns = C.c_int64()
+        _check(_lib.kb_restore_begin(self.h, lo, hi, _stream(stream), None, C.byref(ns)))
+        LAUNCHES[0] += 4  # plan + copy + fixup + mark
         self.last_remap_ns = ns.value
+
+    @property
+    def last_moved_pages(self) -> int:
+        moved = C.c_int64()
+        _check(_lib.kb_pool_last_moved(self.h, C.byref(moved)))
         return moved.value
 
     def restore_complete(self, lo: int, hi: int) -> None:

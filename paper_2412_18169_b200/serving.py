@@ -26,6 +26,8 @@ between groups outside the drop path).
 
 from __future__ import annotations
 
+import gc
+
 import math
 from typing import Optional
 
@@ -118,8 +120,16 @@ class StageRunner:
                   d_ctx=st["d_ctx"], d_rows=st["d_rows"])
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            st["out"] = self.run(lo, hi, st["x"], sb)
+        # no garbage collection inside the capture: a finalizer that frees a
+        # device pool (kb_pool_destroy synchronizes the device) would
+        # invalidate it
+        gc.collect()
+        gc.disable()
+        try:
+            with torch.cuda.graph(g):
+                st["out"] = self.run(lo, hi, st["x"], sb)
+        finally:
+            gc.enable()
         self._graphs[key] = (g, st)
 
     def run_decode_graph(self, lo: int, hi: int, x, batch: dict):
@@ -263,7 +273,7 @@ class DeviceEngine(Engine):
             for t in tasks:
                 key = (t.dst, t.layers)
                 if key not in self.fetch_left:
-                    self.pools[t.dst].restore_begin(*t.layers)
+                    self.pools[t.dst].restore_begin(*t.layers, stream=self.te.bulk)
                     self.fetch_left[key] = 0
                 self.fetch_left[key] += 1
 

@@ -66,6 +66,7 @@ class KVFlow:
     npages: int
     n_chunks: int
     done_chunks: int = 0
+    submitted: int = 0
     grown: bool = False
 
     @property
@@ -210,11 +211,13 @@ class TransferEngine:
             if not self.pools[dst].grow(reqs, stream=stream):
                 raise runtime.DeviceError(f"instance {dst} out of KV pages for an exchange")
         pairs: dict[tuple[int, int], list] = {}
+        runs: list = []
         moved = {}
         for t in tasks:
             if t.kind is TaskKind.KVCACHE_CHUNK:
                 key, idx = self.chunk_of.pop(t.tid)
                 fl = self.flows[key]
+                fl.submitted += 1
                 P = fl.total
                 a, b = idx * P // fl.n_chunks, (idx + 1) * P // fl.n_chunks
                 if b > a:
@@ -224,12 +227,21 @@ class TransferEngine:
                 moved[t.tid] = (b - a) * self.pools[fl.src].page_bytes
                 self.stats.kv_bytes += moved[t.tid]
             elif t.kind is TaskKind.PARAM_SHARD:
-                moved[t.tid] = self._run_param_shard(t, stream)
-                self.stats.param_bytes += moved[t.tid]
+                # consecutive shards of one run coalesce into one pull launch
+                off = self.param_off.pop(t.tid)
+                key = (t.src, t.dst, t.layers)
+                if runs and runs[-1][0] == key and runs[-1][2] == off:
+                    runs[-1][2] += t.size_bytes
+                else:
+                    runs.append([key, off, off + t.size_bytes])
+                moved[t.tid] = t.size_bytes
+                self.stats.param_bytes += t.size_bytes
             else:
                 raise ValueError("activation tasks go through submit_activation")
         for (s, d), moves in pairs.items():
             runtime.copy_pages(self.pools[d], self.pools[s], moves, stream=stream)
+        for (src, dst, layers), a, b in runs:
+            self._copy_param(src, dst, layers, a, b, stream)
         ev = torch.cuda.Event(enable_timing=self.timing)
         ev.record(stream)
         self.stats.tasks += len(tasks)
@@ -247,6 +259,7 @@ class TransferEngine:
     def _run_kv_chunk(self, task: TransferTask, stream) -> int:
         key, idx = self.chunk_of.pop(task.tid)
         fl = self.flows[key]
+        fl.submitted += 1
         src, dst = self.pools[fl.src], self.pools[fl.dst]
         s_slot = self.slots[fl.src].get(fl.rid)
         d_slot = self.slots[fl.dst].get(fl.rid)
@@ -263,27 +276,34 @@ class TransferEngine:
         return (b - a) * src.page_bytes
 
     def _run_param_shard(self, task: TransferTask, stream) -> int:
-        lo, hi = task.layers
         off = self.param_off.pop(task.tid)
-        dst = self.pools[task.dst]
-        if task.src == HOST:
+        self._copy_param(task.src, task.dst, task.layers, off, off + task.size_bytes, stream)
+        return task.size_bytes
+
+    def _copy_param(self, src: int, dst_iid: int, layers: tuple[int, int], a: int, b: int,
+                    stream) -> None:
+        """Bytes [a, b) of the layer run `layers` (slab-contiguous) into dst."""
+        lo, hi = layers
+        dst = self.pools[dst_iid]
+        if src == HOST:
             if self.host_replica is None:
                 raise runtime.DeviceError("HOST-sourced restore without a host replica")
             base = self.host_replica.data_ptr() + lo * dst.model.bytes_per_layer
-            runtime.copy_slabs_from_host(dst, base, lo, hi, off, off + task.size_bytes,
-                                         stream=stream)
+            runtime.copy_slabs_from_host(dst, base, lo, hi, a, b, stream=stream)
         else:
-            runtime.copy_slabs(dst, self.pools[task.src], lo, hi, off, off + task.size_bytes,
-                               stream=stream)
-        return task.size_bytes
+            runtime.copy_slabs(dst, self.pools[src], lo, hi, a, b, stream=stream)
 
-    def finish_flow_sources(self) -> list[KVFlow]:
+    def finish_flow_sources(self, ordered: bool = False) -> list[KVFlow]:
         """Release source pages of every flow whose chunks all landed: one
-        release launch per (source pool, layer range)."""
+        release launch per (source pool, layer range).  ordered=True also
+        takes flows whose chunks are all submitted but maybe not landed: the
+        release goes on the bulk stream behind the copies (and the pool
+        orders it after every other stream's readers), so the host never
+        waits for the transfer."""
         done = []
         batches: dict[tuple[int, tuple[int, int]], list[int]] = {}
         for key, fl in list(self.flows.items()):
-            if fl.done_chunks == fl.n_chunks:
+            if fl.done_chunks == fl.n_chunks or (ordered and fl.submitted == fl.n_chunks):
                 slot = self.slots[fl.src].of.get(fl.rid)
                 if slot is not None:
                     batches.setdefault((fl.src, fl.layers), []).append(slot)

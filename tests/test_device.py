@@ -95,7 +95,8 @@ def test_pool_ops_match_oracle_bit_exact(rt):
                 with pytest.raises(runtime.Refused):
                     pool.restore_begin(l, l + 1)
             else:
-                assert pool.restore_begin(l, l + 1) == want
+                pool.restore_begin(l, l + 1)
+                assert pool.last_moved_pages == want
                 pool.restore_complete(l, l + 1)
                 dropped.discard(l)
         assert_same_state(pool, orc, slots)
@@ -158,12 +159,61 @@ def test_append_exchange_compaction_bytes(rt):
     assert (kb_ == kk).all() and (vb_ == vv).all()
     # restore on a: the filler leaves, compaction moves request 2's tail pages
     a.release([5], 0, 1)
-    moved = a.restore_begin(1, 2)
-    assert moved > 0
+    a.restore_begin(1, 2)
+    assert a.last_moved_pages > 0
     a.restore_complete(1, 2)
     assert max(a.block_table(2, 0)) < 192
     kc, vc = device_gather(a, 2, 0, ctx, 1, 64)
     assert (kc == kk).all() and (vc == vv).all()
+    a.close()
+    b.close()
+
+
+def test_cross_stream_ordering_without_host_sync(rt):
+    """The pool orders its own operations on the device (kb_pool.cu
+    pool_enter / pool_meta_begin): grows, appends, drops, releases and a
+    compaction issued on three streams with no host synchronization give
+    the same block tables and bytes as the serialized run."""
+    from paper_2412_18169_b200 import runtime
+    model = TINY.spec()
+    a = rt.create_pool(0, model, model.param_bytes + MIB, TINY)
+    b = rt.create_pool(1, model, model.param_bytes + MIB, TINY)
+    orc = oracle_for(a)
+    gen = torch.Generator().manual_seed(5)
+    ctx = 300
+    pages = (ctx + 63) // 64
+    k = rand_bf16((ctx, 1, 128), gen).cuda()
+    v = rand_bf16((ctx, 1, 128), gen).cuda()
+    slots_t = torch.full((ctx,), 2, dtype=torch.int32, device="cuda")
+    pos_t = torch.arange(ctx, dtype=torch.int32, device="cuda")
+    big = torch.empty(1 << 29, dtype=torch.uint8, device="cuda")
+    big2 = torch.empty_like(big)
+    torch.cuda.synchronize()
+    s1, s2, s3 = (torch.cuda.Stream() for _ in range(3))
+    # s1 is busy for a while: everything it queues lands late
+    for _ in range(4):
+        runtime.copy_bytes(big2.data_ptr(), big.data_ptr(), big.numel(), stream=s1)
+    a.drop_layers(1, 2)
+    assert a.grow([(5, 0, 1, 190)], stream=s1)
+    assert a.grow([(2, 0, 1, pages)], stream=s1)
+    runtime.kv_append(a, 0, k, v, slots_t, pos_t, stream=s2)  # after the grows
+    assert b.grow([(7, 0, 1, pages)], stream=s3)
+    s3.wait_stream(s2)  # data -> data dependencies stay the caller's
+    runtime.copy_pages(b, a, [(2, 7, 0, 1, pages, 0, pages)], stream=s3)
+    a.release([5], 0, 1, stream=s1)      # after every stream's reader
+    a.restore_begin(1, 2, stream=s2)     # compaction after the release
+    orc.drop(1, 2)
+    assert orc.grow([(5, 0, 1, 190)]) and orc.grow([(2, 0, 1, pages)])
+    orc.release([5], 0, 1)
+    assert orc.restore(1, 2) == a.last_moved_pages > 0
+    a.restore_complete(1, 2)
+    torch.cuda.synchronize()
+    assert_same_state(a, orc, [2, 5])
+    ka, va = device_gather(a, 2, 0, ctx, 1, 64)
+    kb_, vb_ = device_gather(b, 7, 0, ctx, 1, 64)
+    want_k = k.cpu().view(torch.int16).numpy().view(np.uint16)
+    assert (ka == want_k).all() and (kb_ == want_k).all()
+    assert (va == vb_).all()
     a.close()
     b.close()
 

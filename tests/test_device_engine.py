@@ -53,3 +53,5 @@ def test_device_engine_overload_cycle(built, policy):
     st = collect(res.log_lines)
     assert len(st.ttfts()) == len(trace)
     assert eng.stage_samples and all(s[-1] >= 1 for s in eng.stage_samples)
+    for pool in eng.pools.values():
+        pool.close()
