@@ -462,7 +462,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                          "traffic": _traffic("copy_flat_kernel"),
-                         "traffic_algorithmic": 2 * cyc.param_chunk,
+                         "traffic_algorithmic": 2 * pbytes // max(1, sum(r.param_launches for r in reps)),
                          "kernel": "copy_flat_kernel (peer slab pull; same-GPU replicas: "
                                    "read+write HBM)", "peak_source": peak_src},
             "paged_decode": dec,

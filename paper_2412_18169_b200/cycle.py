@@ -57,6 +57,7 @@ class CycleReport:
     kv_kernel_ms: float = 0.0      # device time of the KV page-copy launches
     host_ms: dict = field(default_factory=dict)  # host enqueue time per phase
     tid_marks: list = field(default_factory=list)  # first tid of restore / consolidation
+    param_launches: int = 0        # parameter-pull launches (coalesced runs)
 
     @property
     def bytes_moved(self) -> int:
@@ -198,6 +199,7 @@ class OverloadCycle:
         L = self.L
         ev["t0"].record(st)
         h0 = time.perf_counter()
+        rep.param_launches = self.te.stats.param_launches  # baseline; a delta at the end
         # ---- plan (engine.py:616-648): a queued burst that outgrows every
         # replica's free KV by a quarter of one parameter copy
         groups = [Group(i, [i], {i: (0, L)}) for i in sorted(self.instances)]
@@ -382,6 +384,7 @@ class OverloadCycle:
         rep.kv_kernel_ms += _span_ms([p for p in done if p.task.kind is TaskKind.KVCACHE_CHUNK])
         rep.param_kernel_ms += _span_ms([p for p in done if p.task.kind is TaskKind.PARAM_SHARD])
         rep.pages_compacted = sum(self.pools[iid].last_moved_pages for iid in restored)
+        rep.param_launches = self.te.stats.param_launches - rep.param_launches
         rep.bytes_compaction = rep.pages_compacted * self.shape.page_bytes
         # ---- refill: the next burst re-admits the transient residents
         if self.auto_refill:

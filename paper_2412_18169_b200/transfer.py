@@ -89,6 +89,7 @@ class TransferStats:
     param_bytes: int = 0
     act_bytes: int = 0
     tasks: int = 0
+    param_launches: int = 0
 
 
 class TransferEngine:
@@ -242,6 +243,7 @@ class TransferEngine:
             runtime.copy_pages(self.pools[d], self.pools[s], moves, stream=stream)
         for (src, dst, layers), a, b in runs:
             self._copy_param(src, dst, layers, a, b, stream)
+        self.stats.param_launches += len(runs)
         ev = torch.cuda.Event(enable_timing=self.timing)
         ev.record(stream)
         self.stats.tasks += len(tasks)
@@ -278,6 +280,7 @@ class TransferEngine:
     def _run_param_shard(self, task: TransferTask, stream) -> int:
         off = self.param_off.pop(task.tid)
         self._copy_param(task.src, task.dst, task.layers, off, off + task.size_bytes, stream)
+        self.stats.param_launches += 1
         return task.size_bytes
 
     def _copy_param(self, src: int, dst_iid: int, layers: tuple[int, int], a: int, b: int,
