@@ -292,6 +292,36 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
             "launches_per_step": launches}
 
 
+def nvlink_measure(rt, shape, args) -> dict:
+    """BASELINE configs[2]/[3]: one replica per GPU (rank r owns instance r),
+    plan_drop merges (0,1), (2,3), ... into PP-2 groups spanning two GPUs;
+    a step is drop -> KV exchange -> restore -> consolidation where every
+    byte a rank receives is pulled from its peer's pool through a peer view
+    (dist_cycle.DistCycle) -- NVLink traffic.  value = payload summed over
+    ranks / max-over-ranks step time."""
+    import torch
+    from paper_2412_18169_b200 import dist_cycle
+    ws = torch.distributed.get_world_size()
+    out = dist_cycle.run(rt, shape, int(args.kv_gib * (1 << 30)), steps=args.steps,
+                         warmup=args.warmup, key="bench")
+    ms = out["ms_total_max"]
+    gbs = out["bytes_total"] / (ms / 1e3) / 1e9
+    peer_gbs_per_gpu = out["bytes_peer"] / ws / (out["peer_kernel_ms_max"] / 1e3) / 1e9 \
+        if out["peer_kernel_ms_max"] else 0.0
+    last = out["last"]
+    return {"value": round(gbs, 1), "unit": "GB/s", "n_gpus": ws,
+            "workload": f"llama3_8b bf16, {ws} replicas on {ws} GPUs -> {ws // 2} PP-2 groups "
+                        f"spanning GPU pairs; exchange + restore + consolidation over NVLink",
+            "ms_per_step": round(ms / args.steps, 3),
+            "peer_bytes_per_step": int(out["bytes_peer"] / args.steps),
+            "roofline": {"bound": "nvlink", "achieved": round(peer_gbs_per_gpu, 1),
+                         "peak": 900.0, "unit": "GB/s per GPU per direction",
+                         "frac": round(peer_gbs_per_gpu / 900.0, 4),
+                         "kernel": "copy_pages_kernel + copy_flat_kernel pulling from peer views"},
+            "rank0_ms": {k: round(v, 3) for k, v in last.ms.items()},
+            "parity_bit_exact": out["parity_fail"] == 0}
+
+
 def _traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the committed ncu capture
     (profiles/ncu_traffic.json), or None."""
@@ -422,6 +452,12 @@ def main():
         from paper_2412_18169_b200.ttft import measure
         ttft = measure(kv_gib=1.25, base_rps=3.0, output_mean=128)
 
+    # configs[2] across GPUs: replica r on GPU r, PP-2 groups spanning GPU
+    # pairs, every exchange / restore / consolidation byte pulled over NVLink
+    nvl = None
+    if ws > 1:
+        nvl = nvlink_measure(rt, shape, args)
+
     line = None
     if rank == 0:
         cpu = None
@@ -469,6 +505,7 @@ def main():
             "paged_prefill": prefill,
             "copy_sweep": sweep,
             "p99_ttft": ttft,
+            "nvlink_cycle": nvl,
             "parity": parity,
             "e2e": {"value": round(e_moved / e2e_s / 1e9, 1), "unit": "GB/s",
                     "h2d_bytes_per_step": tok.numel() * 4, "d2h_bytes_per_step": res.numel() * 4},

@@ -166,6 +166,41 @@ int kb_read_bitmap(kb_pool* pool, uint32_t* out, int64_t n_words);
 int kb_read_owner(kb_pool* pool, int32_t* out, int64_t n);
 int64_t kb_pages_per_layer_count(kb_pool* pool, int32_t slot, int32_t layer);
 
+/* ---- N1 across processes: peer views over NVLink ------------------------ */
+/* One process per GPU (torchrun): a pool is exported once as POSIX file
+ * descriptors of its VMM handles (head segment, then slab 0..L-1) plus CUDA
+ * IPC handles of its block table and page counts; a peer process imports
+ * them as a read-only VIEW mapped into its own VA with access for its own
+ * device, so kb_copy_pages / kb_copy_slabs with the view as `src` pull the
+ * owner's pages and slabs over NVLink (plan_exchange / plan_restore_transfers
+ * flows whose source lives on another rank, exchange.py:146-249).  A view
+ * refuses every mutating call (grow, release, drop, restore, append,
+ * attention); the owner performs those, and the two processes order them
+ * (a view's copies complete before the owner releases or compacts).
+ * kb_pool_export fills `fds[0 .. 1+L)` with new descriptors the caller
+ * passes on (SCM_RIGHTS) and closes. */
+typedef struct kb_export_desc {
+    kb_model_desc model;
+    int64_t hbm_bytes;
+    int64_t head_bytes;      /* KV VA head segment (slack + residual), bytes */
+    int64_t slack_pages;
+    int32_t device;          /* owner's device ordinal */
+    int32_t max_slots;
+    int32_t max_pages_per_seq;
+    int32_t n_handles;       /* 1 + num_layers */
+    uint8_t bt_ipc[64];      /* cudaIpcMemHandle_t of block_table */
+    uint8_t np_ipc[64];      /* cudaIpcMemHandle_t of npages */
+} kb_export_desc;
+int kb_pool_export(kb_pool* pool, kb_export_desc* out, int32_t* fds, int32_t cap);
+int kb_pool_import(int32_t device, const kb_export_desc* desc, const int32_t* fds,
+                   int32_t n_fds, kb_pool** out);
+/* Refresh a view's host mirrors before planning against it: page counts
+ * from the owner's device array (synchronizing), layer states from the
+ * caller's mirror of the owner's segment table (1 = held). */
+int kb_pool_view_refresh(kb_pool* view, const uint8_t* layer_held, int32_t n_layers);
+/* 1 if `pool` is an imported view, 0 if this process owns it. */
+int kb_pool_is_view(kb_pool* pool);
+
 /* ---- N4/N5/N7: NVLink peer copy kernels --------------------------------- */
 /* KV exchange / consolidation (exchange.py:146-205, engine.py:690-726,
  * 1211-1239): copy whole pages named by the two pools' block tables. */

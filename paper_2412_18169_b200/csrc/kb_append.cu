@@ -57,6 +57,7 @@ using namespace kb;
 extern "C" int kb_kv_append(kb_pool* p, int32_t layer, uint64_t k, uint64_t v, uint64_t slots,
                             uint64_t pos, int32_t ntok, uintptr_t stream) {
   if (!p) return fail(KB_EINVAL, "null pool");
+  if (p->view) return refuse_view();
   if (p->m.head_dim != 128) return fail(KB_EINVAL, "head_dim must be 128");
   if (layer < 0 || layer >= p->m.num_layers) return fail(KB_EINVAL, "bad layer");
   if (ntok <= 0) return KB_OK;

@@ -28,6 +28,8 @@ struct Driver {
   PFN_cuMemGetAllocationGranularity MemGetAllocationGranularity = nullptr;
   PFN_cuTensorMapEncodeTiled TensorMapEncodeTiled = nullptr;
   PFN_cuGetErrorString GetErrorString = nullptr;
+  PFN_cuMemExportToShareableHandle MemExport = nullptr;
+  PFN_cuMemImportFromShareableHandle MemImport = nullptr;
   bool ready = false;
 };
 Driver& drv();
@@ -133,10 +135,15 @@ struct kb_pool {
   // TMA descriptor over the whole KV VA viewed as [rows][head_dim] bf16
   // (row = one token of one kv head of K or V), box = [block_tokens][64].
   alignas(64) CUtensorMap kv_tmap;
+  // Imported from another process (kb_pool_import): slabs mapped from the
+  // owner's exported handles, block table / page counts opened through CUDA
+  // IPC.  Only a copy source; every mutating entry point refuses a view.
+  bool view = false;
 };
 
 namespace kb {
 int ensure_scratch(kb_pool* p, int64_t bytes);
+int refuse_view();
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 inline int grid_for(int64_t work, int per_block, int max_blocks) {

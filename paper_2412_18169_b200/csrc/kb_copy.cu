@@ -138,6 +138,7 @@ using namespace kb;
 extern "C" int kb_copy_pages(kb_pool* dst, kb_pool* src, const kb_move* moves, int32_t n,
                              uintptr_t stream) {
   if (!dst || !src) return fail(KB_EINVAL, "null pool");
+  if (dst->view) return fail(KB_EINVAL, "copy destination must be a pool this process owns (pull from views)");
   if (n <= 0) return KB_OK;
   if (dst->m.page_bytes != src->m.page_bytes || dst->m.num_layers != src->m.num_layers)
     return fail(KB_EINVAL, "pools disagree on page geometry");
@@ -189,6 +190,7 @@ extern "C" int kb_copy_pages(kb_pool* dst, kb_pool* src, const kb_move* moves, i
 extern "C" int kb_copy_slabs(kb_pool* dst, kb_pool* src, int32_t lo, int32_t hi, int64_t byte_lo,
                              int64_t byte_hi, uintptr_t stream) {
   if (!dst || !src) return fail(KB_EINVAL, "null pool");
+  if (dst->view) return fail(KB_EINVAL, "copy destination must be a pool this process owns (pull from views)");
   if (dst->m.slab_bytes != src->m.slab_bytes) return fail(KB_EINVAL, "pools disagree on slab size");
   const int64_t slab = src->m.slab_bytes;
   if (hi <= lo || byte_lo < 0 || byte_hi < byte_lo || byte_hi > (int64_t)(hi - lo) * slab)
@@ -213,6 +215,7 @@ extern "C" int kb_copy_slabs(kb_pool* dst, kb_pool* src, int32_t lo, int32_t hi,
 extern "C" int kb_copy_slabs_from_host(kb_pool* dst, const void* host_src, int32_t lo, int32_t hi,
                                        int64_t byte_lo, int64_t byte_hi, uintptr_t stream) {
   if (!dst || !host_src) return fail(KB_EINVAL, "null argument");
+  if (dst->view) return refuse_view();
   const int64_t slab = dst->m.slab_bytes;
   if (hi <= lo || byte_lo < 0 || byte_hi < byte_lo || byte_hi > (int64_t)(hi - lo) * slab)
     return fail(KB_EINVAL, "bad slab byte range");

@@ -127,6 +127,7 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
                                float scale, uint64_t out, uint64_t workspace, int32_t max_splits,
                                int32_t flags, uintptr_t stream) {
   if (!p) return fail(KB_EINVAL, "null pool");
+  if (p->view) return refuse_view();
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
   if (p->m.head_dim != 128) return fail(KB_EINVAL, "head_dim must be 128");
   if (n_q_heads % Hkv || n_q_heads / Hkv > 8) return fail(KB_EINVAL, "GQA group must be <= 8");

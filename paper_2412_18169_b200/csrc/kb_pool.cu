@@ -60,10 +60,16 @@ int ensure_driver() {
             get("cuMemAddressFree", (void**)&d.MemAddressFree) &&
             get("cuMemGetAllocationGranularity", (void**)&d.MemGetAllocationGranularity) &&
             get("cuTensorMapEncodeTiled", (void**)&d.TensorMapEncodeTiled) &&
-            get("cuGetErrorString", (void**)&d.GetErrorString);
+            get("cuGetErrorString", (void**)&d.GetErrorString) &&
+            get("cuMemExportToShareableHandle", (void**)&d.MemExport) &&
+            get("cuMemImportFromShareableHandle", (void**)&d.MemImport);
   if (!ok) return fail(KB_ECUDA, "cannot resolve CUDA driver entry points");
   d.ready = true;
   return KB_OK;
+}
+
+int refuse_view() {
+  return fail(KB_EINVAL, "pool is a read-only peer view: its owner process performs this operation");
 }
 
 int ensure_scratch(kb_pool* p, int64_t bytes) {
@@ -626,8 +632,13 @@ extern "C" int kb_pool_destroy(kb_pool* p) {
   if (p->kva) drv().MemAddressFree(p->kva, p->kva_size);
   if (p->d_bitmap) cudaFree(p->d_bitmap);
   if (p->d_owner) cudaFree(p->d_owner);
-  if (p->d_bt) cudaFree(p->d_bt);
-  if (p->d_np) cudaFree(p->d_np);
+  if (p->view) {
+    if (p->d_bt) cudaIpcCloseMemHandle(p->d_bt);
+    if (p->d_np) cudaIpcCloseMemHandle(p->d_np);
+  } else {
+    if (p->d_bt) cudaFree(p->d_bt);
+    if (p->d_np) cudaFree(p->d_np);
+  }
   if (p->d_scratch) cudaFree(p->d_scratch);
   if (p->h_pinned) cudaFreeHost(p->h_pinned);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
@@ -677,6 +688,7 @@ static int collect_counts(kb_pool* p) {
 
 extern "C" int kb_drop_layers(kb_pool* p, int32_t lo, int32_t hi, int64_t* remap_ns) {
   if (!p) return fail(KB_EINVAL, "null pool");
+  if (p->view) return refuse_view();
   if (hi <= lo) return fail(KB_EINVAL, "empty layer range");
   for (int l = lo; l < hi; ++l) {
     if (l < 0 || l >= p->m.num_layers) return fail(KB_EINVAL, "layer " + std::to_string(l) + " absent from segment table");
@@ -705,6 +717,7 @@ extern "C" int kb_drop_layers(kb_pool* p, int32_t lo, int32_t hi, int64_t* remap
 extern "C" int kb_restore_begin(kb_pool* p, int32_t lo, int32_t hi, uintptr_t stream,
                                 int64_t* moved_pages, int64_t* remap_ns) {
   if (!p) return fail(KB_EINVAL, "null pool");
+  if (p->view) return refuse_view();
   if (hi <= lo) return fail(KB_EINVAL, "empty layer range");
   for (int l = lo; l < hi; ++l) {
     if (l < 0 || l >= p->m.num_layers) return fail(KB_EINVAL, "layer " + std::to_string(l) + " absent from segment table");
@@ -767,6 +780,7 @@ extern "C" int kb_pool_last_moved(kb_pool* p, int64_t* moved_pages) {
 
 extern "C" int kb_restore_complete(kb_pool* p, int32_t lo, int32_t hi) {
   if (!p) return fail(KB_EINVAL, "null pool");
+  if (p->view) return refuse_view();
   for (int l = lo; l < hi; ++l) {
     if (l < 0 || l >= p->m.num_layers || p->layer_state[l] != kLayerRestoring)
       return fail(KB_ESTATE, "layer " + std::to_string(l) + " not awaiting restore");
@@ -777,6 +791,7 @@ extern "C" int kb_restore_complete(kb_pool* p, int32_t lo, int32_t hi) {
 
 extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr_t stream) {
   if (!p) return fail(KB_EINVAL, "null pool");
+  if (p->view) return refuse_view();
   if (n <= 0) return KB_OK;
   const int L = p->m.num_layers;
   int64_t total = 0;
@@ -834,6 +849,7 @@ extern "C" int kb_pages_grow(kb_pool* p, const kb_grow* reqs, int32_t n, uintptr
 extern "C" int kb_pages_release(kb_pool* p, const int32_t* slots, int32_t n, int32_t lo,
                                 int32_t hi, uintptr_t stream) {
   if (!p) return fail(KB_EINVAL, "null pool");
+  if (p->view) return refuse_view();
   const int L = p->m.num_layers;
   if (n <= 0 || hi <= lo) return KB_OK;
   if (lo < 0 || hi > L) return fail(KB_EINVAL, "bad layer range");
@@ -885,6 +901,7 @@ extern "C" int kb_read_block_table(kb_pool* p, int32_t slot, int32_t layer, int3
 
 extern "C" int kb_read_bitmap(kb_pool* p, uint32_t* out, int64_t n_words) {
   if (!p || n_words > p->n_words) return fail(KB_EINVAL, "bad bitmap read");
+  if (p->view) return refuse_view();
   KB_RT(cudaSetDevice(p->device));
   KB_RT(cudaDeviceSynchronize());
   KB_RT(cudaMemcpy(out, p->d_bitmap, (size_t)n_words * 4, cudaMemcpyDeviceToHost));
@@ -893,8 +910,149 @@ extern "C" int kb_read_bitmap(kb_pool* p, uint32_t* out, int64_t n_words) {
 
 extern "C" int kb_read_owner(kb_pool* p, int32_t* out, int64_t n) {
   if (!p || n > p->max_pages) return fail(KB_EINVAL, "bad owner read");
+  if (p->view) return refuse_view();
   KB_RT(cudaSetDevice(p->device));
   KB_RT(cudaDeviceSynchronize());
   KB_RT(cudaMemcpy(out, p->d_owner, (size_t)n * 4, cudaMemcpyDeviceToHost));
   return KB_OK;
 }
+
+// ------------------------------------------------------- cross-process views
+// One process per GPU: the owner exports its VMM handles as POSIX file
+// descriptors and its block table / page counts as CUDA IPC handles; a peer
+// imports them as a read-only view in its own VA with access for its own
+// device, and pulls pages and slabs over NVLink with the same copy kernels.
+
+extern "C" int kb_pool_export(kb_pool* p, kb_export_desc* o, int32_t* fds, int32_t cap) {
+  if (!p || !o || !fds) return fail(KB_EINVAL, "null argument");
+  if (p->view) return refuse_view();
+  const int n = 1 + p->m.num_layers;
+  if (cap < n) return fail(KB_EINVAL, "fd buffer holds " + std::to_string(cap) + " < " +
+                                          std::to_string(n) + " handles");
+  KB_RT(cudaSetDevice(p->device));
+  std::memset(o, 0, sizeof(*o));
+  o->model = p->m;
+  o->hbm_bytes = p->hbm_bytes;
+  o->head_bytes = p->kv_segs.empty() ? 0 : p->kv_segs[0].bytes;
+  o->slack_pages = p->slack_pages;
+  o->device = p->device;
+  o->max_slots = p->max_slots;
+  o->max_pages_per_seq = p->maxp;
+  o->n_handles = n;
+  static_assert(sizeof(cudaIpcMemHandle_t) <= 64, "ipc handle size");
+  cudaIpcMemHandle_t hb, hn;
+  KB_RT(cudaIpcGetMemHandle(&hb, p->d_bt));
+  KB_RT(cudaIpcGetMemHandle(&hn, p->d_np));
+  std::memcpy(o->bt_ipc, &hb, sizeof(hb));
+  std::memcpy(o->np_ipc, &hn, sizeof(hn));
+  for (int i = 0; i < n; ++i) fds[i] = -1;
+  for (int i = 0; i < n; ++i) {
+    CUmemGenericAllocationHandle h = i == 0 ? p->kv_segs[0].h : p->layer_handle[i - 1];
+    int fd = -1;
+    CUresult r = drv().MemExport(&fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
+    if (r != CUDA_SUCCESS) return fail(KB_ECUDA, "cuMemExportToShareableHandle failed for handle " +
+                                                     std::to_string(i));
+    fds[i] = fd;
+  }
+  return KB_OK;
+}
+
+extern "C" int kb_pool_import(int32_t device, const kb_export_desc* d, const int32_t* fds,
+                              int32_t n_fds, kb_pool** out) {
+  if (!d || !fds || !out) return fail(KB_EINVAL, "null argument");
+  *out = nullptr;
+  const kb_model_desc m = d->model;
+  if (m.num_layers < 1 || m.slab_bytes < 1 || m.page_bytes < 1 || d->head_bytes < 0)
+    return fail(KB_EINVAL, "bad export descriptor");
+  if (n_fds != 1 + m.num_layers || d->n_handles != n_fds)
+    return fail(KB_EINVAL, "export carries " + std::to_string(n_fds) + " handles, want " +
+                               std::to_string(1 + m.num_layers));
+  int rc = set_device(device);
+  if (rc) return rc;
+  kb_pool* p = new kb_pool();
+  p->view = true;
+  p->device = device;
+  p->m = m;
+  p->hbm_bytes = d->hbm_bytes;
+  p->access.push_back(device);
+  p->max_slots = d->max_slots;
+  p->maxp = d->max_pages_per_seq;
+  auto bail = [&](int code) {
+    kb_pool_destroy(p);
+    return code;
+  };
+  int64_t gran = 0;
+  if ((rc = kb_vmm_granularity(device, &gran))) return bail(rc);
+  p->gran = gran;
+  const int64_t param = (int64_t)m.num_layers * m.slab_bytes;
+  const int64_t head = d->head_bytes;
+  p->wva_size = (size_t)param;
+  p->kva_size = (size_t)(head + param);
+  if (drv().MemAddressReserve(&p->wva, p->wva_size, (size_t)gran, 0, 0) != CUDA_SUCCESS ||
+      drv().MemAddressReserve(&p->kva, p->kva_size, (size_t)gran, 0, 0) != CUDA_SUCCESS)
+    return bail(fail(KB_ECUDA, "cuMemAddressReserve(view) failed"));
+  auto import = [&](int32_t fd, CUmemGenericAllocationHandle* h) -> int {
+    CUresult r = drv().MemImport(h, reinterpret_cast<void*>((uintptr_t)fd),
+                                 CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    if (r != CUDA_SUCCESS) return fail(KB_ECUDA, "cuMemImportFromShareableHandle failed");
+    return KB_OK;
+  };
+  {
+    CUmemGenericAllocationHandle h;
+    if ((rc = import(fds[0], &h))) return bail(rc);
+    p->kv_segs.push_back({h, head, false});
+    if ((rc = map_at(p, p->kva, head, h))) return bail(rc);
+  }
+  p->layer_handle.assign(m.num_layers, 0);
+  p->layer_state.assign(m.num_layers, kLayerHeld);
+  for (int l = 0; l < m.num_layers; ++l) {
+    CUmemGenericAllocationHandle h;
+    if ((rc = import(fds[1 + l], &h))) return bail(rc);
+    p->layer_handle[l] = h;
+    if ((rc = map_at(p, p->wva + (CUdeviceptr)l * m.slab_bytes, m.slab_bytes, h))) return bail(rc);
+    if ((rc = map_at(p, p->kva + head + (CUdeviceptr)l * m.slab_bytes, m.slab_bytes, h)))
+      return bail(rc);
+  }
+  p->head_pages = head / m.page_bytes;
+  p->slack_pages = d->slack_pages;
+  p->max_pages = (int64_t)p->kva_size / m.page_bytes;
+  p->usable_pages = p->head_pages;
+  cudaIpcMemHandle_t hb, hn;
+  std::memcpy(&hb, d->bt_ipc, sizeof(hb));
+  std::memcpy(&hn, d->np_ipc, sizeof(hn));
+  void* bt = nullptr;
+  void* np = nullptr;
+  if (cudaIpcOpenMemHandle(&bt, hb, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return bail(fail(KB_ECUDA, "cudaIpcOpenMemHandle(block table) failed"));
+  p->d_bt = static_cast<int32_t*>(bt);
+  if (cudaIpcOpenMemHandle(&np, hn, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return bail(fail(KB_ECUDA, "cudaIpcOpenMemHandle(page counts) failed"));
+  p->d_np = static_cast<int32_t*>(np);
+  p->h_np.assign((size_t)p->max_slots * m.num_layers, 0);
+  if (cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->meta_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->counts_ev, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(KB_ECUDA, "view stream/event creation failed"));
+  *out = p;
+  return KB_OK;
+}
+
+extern "C" int kb_pool_view_refresh(kb_pool* p, const uint8_t* layer_held, int32_t n_layers) {
+  if (!p || !layer_held) return fail(KB_EINVAL, "null argument");
+  if (!p->view) return fail(KB_EINVAL, "not a peer view");
+  if (n_layers != p->m.num_layers) return fail(KB_EINVAL, "layer count mismatch");
+  KB_RT(cudaSetDevice(p->device));
+  KB_RT(cudaMemcpy(p->h_np.data(), p->d_np, p->h_np.size() * 4, cudaMemcpyDeviceToHost));
+  int64_t live = 0, usable = p->head_pages;
+  const int64_t sp = p->m.slab_bytes / p->m.page_bytes;
+  for (auto c : p->h_np) live += c;
+  for (int l = 0; l < n_layers; ++l) {
+    p->layer_state[l] = layer_held[l] ? kLayerHeld : kLayerDropped;
+    if (!layer_held[l]) usable += sp;
+  }
+  p->live_pages = live;
+  p->usable_pages = usable;
+  return KB_OK;
+}
+
+extern "C" int kb_pool_is_view(kb_pool* p) { return p && p->view ? 1 : 0; }

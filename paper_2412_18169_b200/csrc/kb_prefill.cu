@@ -358,6 +358,7 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
                                 int32_t nseq, int32_t max_q_len, float scale, uint64_t out,
                                 uintptr_t stream) {
   if (!p) return fail(KB_EINVAL, "null pool");
+  if (p->view) return refuse_view();
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
   if (p->m.head_dim != 128) return fail(KB_EINVAL, "head_dim must be 128");
   if (n_q_heads % Hkv) return fail(KB_EINVAL, "n_q_heads must be a multiple of n_kv_heads");

@@ -5,16 +5,25 @@ The drop path shards into independent groups: plan_drop
 the same plan from the same all-gathered group state and executes only the
 merges whose members it owns -- no data-path collective.  Pairs of replicas
 live on one GPU in the single-GPU configuration (rank r owns instances
-k*r .. k*r+k-1); a merge that spans ranks is reported as remote (its KV
-exchange needs the cross-process NVLink pool mapping, not built this round).
+k*r .. k*r+k-1); a merge that spans ranks is remote: its KV exchange and
+restore run through peer views (share_pools): every rank exports its pools'
+VMM handles as file descriptors, passes them to the other ranks over a
+Unix socket (SCM_RIGHTS), and imports the peers' pools as read-only views
+mapped in its own VA -- the copy kernels then pull pages and slabs over
+NVLink (dist_cycle.DistCycle).
 
 torch.distributed carries only metadata (object all-gathers, a max-reduce of
-timings); it is plumbing for the multi-process launch bench.py gets from
-torchrun, and the tests run it over gloo.
+timings, barriers between the phases whose device work crosses ranks); it is
+plumbing for the multi-process launch bench.py gets from torchrun, and the
+tests run it over gloo.
 """
 
 from __future__ import annotations
 
+import os
+import socket
+import struct
+import threading
 from dataclasses import dataclass
 
 from .core import Group, ModelSpec
@@ -81,3 +90,86 @@ def sum_over_ranks(x: float, device=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+# ---------------------------------------------------------------- fd passing
+
+_MAX_FDS = 250  # below SCM_MAX_FD (253)
+
+
+def _sock_name(key: str, rank: int) -> bytes:
+    # Linux abstract namespace: nothing on the filesystem to clean up
+    return f"\0kunserve-b200-{key}-{rank}".encode()
+
+
+def exchange_fds(payloads: dict, key: str) -> dict:
+    """All-to-all of (descriptor bytes, file descriptors) between the ranks
+    of the default process group.  payloads: local id -> (bytes, [fd]);
+    returns every other rank's entries as id -> (bytes, [fd]) with fds
+    valid in this process (the caller owns and closes them).  File
+    descriptors cannot travel through torch.distributed, so each rank serves
+    its payloads on a Unix SEQPACKET socket (SCM_RIGHTS, one message per
+    entry) and connects to every other rank's socket."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    srv = socket.socket(socket.AF_UNIX, socket.SOCK_SEQPACKET)
+    srv.bind(_sock_name(key, rank))
+    srv.listen(world)
+    for k, (_, fds) in payloads.items():
+        if len(fds) > _MAX_FDS:
+            raise ValueError(f"entry {k}: {len(fds)} fds exceed one SCM_RIGHTS message")
+
+    def serve():
+        for _ in range(world - 1):
+            conn, _ = srv.accept()
+            with conn:
+                conn.sendall(struct.pack("<q", len(payloads)))
+                for k, (blob, fds) in sorted(payloads.items()):
+                    socket.send_fds(conn, [struct.pack("<qq", k, len(fds)) + blob], fds)
+                conn.recv(1)  # the peer holds its copies: done
+
+    th = threading.Thread(target=serve, daemon=True)
+    th.start()
+    dist.barrier()  # every listener is up
+    out = {}
+    try:
+        for peer in range(world):
+            if peer == rank:
+                continue
+            with socket.socket(socket.AF_UNIX, socket.SOCK_SEQPACKET) as c:
+                c.connect(_sock_name(key, peer))
+                n = struct.unpack("<q", c.recv(8))[0]
+                for _ in range(n):
+                    msg, fds, _flags, _addr = socket.recv_fds(c, 1 << 16, _MAX_FDS)
+                    k, nfd = struct.unpack("<qq", msg[:16])
+                    if len(fds) != nfd:
+                        raise RuntimeError(f"entry {k}: received {len(fds)} of {nfd} fds")
+                    out[k] = (msg[16:], list(fds))
+                c.sendall(b"x")
+    finally:
+        th.join(timeout=60)
+        srv.close()
+    dist.barrier()
+    return out
+
+
+def share_pools(rt, local_pools: dict, model, shape, key: str = "pools") -> dict:
+    """Export this rank's pools, import every other rank's as PeerPool views
+    on this rank's device.  local_pools: iid -> DevicePool.  Returns
+    iid -> PeerPool for the remote instances."""
+    from .runtime import PeerPool
+    mine = {iid: pool.export() for iid, pool in local_pools.items()}
+    try:
+        theirs = exchange_fds(mine, key)
+    finally:
+        for _, fds in mine.values():
+            for fd in fds:
+                os.close(fd)
+    views = {}
+    for iid, (blob, fds) in sorted(theirs.items()):
+        try:
+            views[iid] = PeerPool(rt, iid, model, shape, blob, fds)
+        finally:
+            for fd in fds:
+                os.close(fd)
+    return views

@@ -1,0 +1,420 @@
+"""The overload cycle across processes: one replica per GPU, PP-2 groups
+spanning two GPUs, KV exchange and parameter restore pulled over NVLink.
+
+BASELINE.json configs[2] ("Llama-3-8B bf16, 8 replicas on 8xB200 dropped to
+4 PP-2 groups, KV exchange + param restore at burst end").  Rank r owns
+instance r; plan_drop (pkg/src/dropsim/planner.py:70-114) pairs gids
+(0,1), (2,3), ... so every merged group spans two GPUs.
+
+Every rank runs the reference's control plane for ALL instances -- the
+same memory.* / KVAllocator / plan_exchange / plan_restore_transfers calls
+in the same order, so the host state (segment tables, token accounting,
+block-table slots) is identical everywhere -- and executes on its GPU only
+what its own instance does:
+  * drops, restores (compaction) and block-table growth of its own pool;
+  * every task whose DESTINATION is its instance, pulling from the source's
+    pool through a PeerPool view (dist.share_pools): the copy kernels read
+    the peer's pages / slabs over NVLink and write local HBM;
+  * the release of its own source pages once the peer's pulls landed.
+Cross-rank ordering is explicit: after each phase whose pulls read a peer's
+memory, every rank synchronizes its transfer stream and the ranks meet at a
+barrier before a source releases (exchange, consolidation) or compacts
+(restore) pages a peer may still read.  Timing: CUDA events on each rank's
+transfer stream (they include the barrier waits), max over ranks.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import memory
+from .core import Group, ModelShape
+from .cycle import _span_ms
+from .dist import max_over_ranks, share_pools, sum_over_ranks
+from .exchange import HOST, TaskKind, TransferTask, plan_exchange, plan_restore_transfers, share_bytes
+from .planner import compute_demand, member_moves, plan_drop
+from .traceio import synth_burst
+from .transfer import SlotTable, TransferEngine
+
+
+@dataclass
+class DistReport:
+    bytes_pulled: int = 0          # payload this rank pulled (all phases)
+    bytes_pulled_peer: int = 0     # ... of it from another rank's GPU (NVLink)
+    bytes_kv_exchange: int = 0
+    bytes_param: int = 0
+    bytes_kv_consolidate: int = 0
+    bytes_compaction: int = 0
+    kv_kernel_ms: float = 0.0
+    param_kernel_ms: float = 0.0
+    ms: dict = field(default_factory=dict)
+
+
+class DistCycle:
+    def __init__(self, rt, shape: ModelShape, kv_budget_bytes: int, fill: float = 0.9,
+                 seed: int = 3, kv_chunk_bytes: int = 64 << 20,
+                 param_chunk_bytes: int = 256 << 20, input_mean: int = 1660,
+                 key: str = "cycle"):
+        import torch
+        import torch.distributed as dist
+        self.torch = torch
+        self.dist = dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.me = self.rank
+        self.shape = shape
+        self.model = shape.spec()
+        self.L = self.model.num_layers
+        self.kv_chunk = kv_chunk_bytes
+        self.param_chunk = param_chunk_bytes
+        self.device = rt.device
+        hbm = self.model.param_bytes + kv_budget_bytes
+        self.instances = {}
+        for iid in range(self.world):
+            local = iid == self.me
+            self.instances[iid] = memory.build_instance(
+                iid, self.model, hbm, 900_000_000_000,
+                device=rt if local else None, shape=shape if local else None)
+        self.pool = self.instances[self.me].pool
+        self.slots = {iid: SlotTable(rt.max_slots) for iid in self.instances}
+        trace = synth_burst(10_000.0, 4.0, 16.0, 0.0, 10_000.0, input_mean, 373, seed=seed)
+        self.tokens: dict[int, int] = {}
+        self.home: dict[int, int] = {}
+        full = {i: False for i in self.instances}
+        rid = 0
+        for rec in trace:
+            if all(full.values()):
+                break
+            iid = rid % self.world
+            rid += 1
+            if full[iid]:
+                continue
+            inst = self.instances[iid]
+            if inst.kv.used_tokens + rec.input_len > fill * inst.kv.capacity_tokens:
+                full[iid] = True
+                continue
+            self.tokens[rid] = rec.input_len
+            self.home[rid] = iid
+            self._admit(rid)
+        # every other resident of each home is transient (finishes in the drain)
+        self.transient = set()
+        for iid in self.instances:
+            self.transient |= set(sorted(r for r, h in self.home.items() if h == iid)[1::2])
+        g = torch.Generator(device=f"cuda:{self.device}").manual_seed(77 + self.me)
+        head = self.pool.info().extent_pages * self.pool.page_bytes
+        kv = self.pool.kv_bytes()[:head].view(torch.int32)
+        kv.copy_(torch.randint(-2**31, 2**31 - 1, (kv.numel(),), dtype=torch.int32,
+                               device=kv.device, generator=g))
+        n = self.shape.layer_weight_bytes // 2
+        for l in range(self.L):
+            gl = torch.Generator(device=f"cuda:{self.device}").manual_seed(1000 + l)
+            slab = self.pool.weight_bytes(l)
+            slab[2 * n:].zero_()
+            w = slab[:2 * n].view(torch.bfloat16)
+            w.copy_((torch.randn(n, device=w.device, generator=gl) * 0.02).to(torch.bfloat16))
+        torch.cuda.synchronize(self.device)
+        self.views = share_pools(rt, {self.me: self.pool}, self.model, shape,
+                                 key=f"{key}-{self._job_key()}")
+        self.pools = {self.me: self.pool, **self.views}
+        self.te = TransferEngine(self.pools, self.slots, timing=True)
+        self._sync_views()
+
+    @staticmethod
+    def _job_key() -> str:
+        import os
+        return os.environ.get("MASTER_PORT", "0")
+
+    # ---------------------------------------------------------------- helpers
+    def _admit(self, rid: int) -> None:
+        iid = self.home[rid]
+        inst = self.instances[iid]
+        assert inst.kv.alloc(rid, self.tokens[rid])
+        slot = self.slots[iid].get(rid)
+        if iid == self.me:
+            assert self.pool.grow([(slot, 0, self.L, -(-self.tokens[rid] // self.shape.block_tokens))])
+
+    def _sync_views(self) -> None:
+        """Phase boundary: this rank's device work is done, every rank is
+        here, and the views reflect the owners' page counts / layer states."""
+        self.torch.cuda.synchronize(self.device)
+        self.dist.barrier()
+        for iid, v in self.views.items():
+            v.refresh(self.instances[iid].table.layers_held())
+
+    def _submit_local(self, tasks: list[TransferTask]) -> None:
+        """Mirror the slot assignment of every destination (the owners do the
+        same get() calls in the same order), then run the tasks whose
+        destination is this rank; drop the bookkeeping of the others."""
+        for t in tasks:
+            if t.kind is TaskKind.KVCACHE_CHUNK:
+                key, _ = self.te.chunk_of[t.tid]
+                fl = self.te.flows[key]
+                self.slots[fl.dst].get(fl.rid)
+        mine = [t for t in tasks if t.dst == self.me]
+        for t in tasks:
+            if t.dst != self.me:
+                self.te.chunk_of.pop(t.tid, None)
+                self.te.param_off.pop(t.tid, None)
+        if mine:
+            self.te.submit_many(mine)
+
+    def _release_sources(self) -> None:
+        """After the barrier: free this rank's source pages of every flow
+        (all flows' chunks were submitted by their destinations and have
+        landed -- every rank synchronized before the barrier)."""
+        batches: dict[tuple[int, int], list[int]] = {}
+        for key, fl in list(self.te.flows.items()):
+            if fl.src == self.me:
+                slot = self.slots[fl.src].of.get(fl.rid)
+                if slot is not None:
+                    batches.setdefault(fl.layers, []).append(slot)
+            del self.te.flows[key]
+        for (lo, hi), slots in batches.items():
+            self.pool.release(slots, lo, hi, stream=self.te.bulk)
+
+    # ------------------------------------------------------------------ checks
+    def weight_checksums(self) -> list[int]:
+        torch = self.torch
+        return [int(self.pool.weight_bytes(l).view(torch.int32).to(torch.int64).sum().item())
+                for l in range(self.L)]
+
+    def kv_checksums(self) -> dict:
+        """This rank's long-lived home residents: per-page int32 sums."""
+        torch = self.torch
+        inf = self.pool.info()
+        from .runtime import device_bytes
+        bt = device_bytes(inf.block_table, inf.max_slots * self.L * inf.max_pages_per_seq * 4)
+        bt = bt.view(torch.int32).view(inf.max_slots, self.L, inf.max_pages_per_seq)
+        kv = self.pool.kv_bytes().view(torch.int32).view(-1, self.pool.page_bytes // 4)
+        out = {}
+        for rid, home in self.home.items():
+            if home != self.me or rid in self.transient:
+                continue
+            npg = -(-self.tokens[rid] // self.shape.block_tokens)
+            pages = bt[self.slots[self.me].of[rid], :, :npg].reshape(-1).long()
+            out[rid] = kv.index_select(0, pages).to(torch.int64).sum(dim=1).cpu()
+        return out
+
+    # ------------------------------------------------------------------- cycle
+    def step(self) -> DistReport:
+        torch = self.torch
+        rep = DistReport()
+        st = self.te.bulk
+        L = self.L
+        kvbpt = self.model.kv_bytes_per_token
+        ev = {k: torch.cuda.Event(enable_timing=True) for k in
+              ("t0", "exch", "drain", "restore", "cons")}
+        self.dist.barrier()
+        ev["t0"].record(st)
+        # ---- plan: every replica's queued burst outgrows its free KV by just
+        # under half a parameter copy, so plan_drop merges every pair
+        groups = [Group(i, [i], {i: (0, L)}) for i in sorted(self.instances)]
+        demand = 0
+        for i, inst in sorted(self.instances.items()):
+            free = inst.kv.free_tokens * kvbpt
+            pending = (free + self.model.param_bytes // 2 - kvbpt) // kvbpt
+            demand += compute_demand(pending, free, kvbpt)
+        plan = plan_drop(groups, demand, self.model)
+        assert plan.merges and not plan.fallback, plan.to_text()
+        orig_map = {rid: {h: (0, L)} for rid, h in self.home.items()}
+        live = {g.gid: g for g in groups}
+        for m in plan.merges:
+            live.pop(m.gid_a)
+            live.pop(m.gid_b)
+            new = Group(m.gid, list(m.members), dict(m.stage_layer_map))
+            new.validate_coverage(L)
+            for iid in m.members:
+                drops, fetches = member_moves(self.instances[iid].table.held_ranges(),
+                                              m.stage_layer_map[iid])
+                assert not fetches
+                for lo, hi in drops:
+                    memory.drop_layers(self.instances[iid], (lo, hi), new)
+            live[m.gid] = new
+        final = {iid: g for g in live.values() for iid in g.member_instances}
+        # ---- exchange (engine.py:690-726): pulls into this rank's pool
+        tid = 0
+        all_tasks = []
+        for g in sorted(live.values(), key=lambda g: g.gid):
+            cohorts: dict[tuple, list[int]] = {}
+            for rid in sorted(self.tokens):
+                if final[self.home[rid]] is g:
+                    cohorts.setdefault(tuple(sorted(orig_map[rid].items())), []).append(rid)
+            for key in sorted(cohorts):
+                old_map = dict(key)
+                toks = {rid: self.tokens[rid] for rid in cohorts[key]}
+                tasks = plan_exchange(toks, old_map, g.stage_layer_map, L, kvbpt, self.kv_chunk,
+                                      tid_start=tid)
+                tid += len(tasks)
+                self.te.register_exchange(tasks, old_map, g.stage_layer_map, toks)
+                all_tasks += tasks
+        self._submit_local(all_tasks)
+        self._sync_views()            # every pull landed
+        self._release_sources()       # now the sources may free
+        for rid, tok in self.tokens.items():
+            g = final[self.home[rid]]
+            for iid in g.member_instances:
+                self.instances[iid].kv.free(rid)
+            for iid in g.member_instances:
+                lo, hi = g.stage_layer_map[iid]
+                share = memory.stage_share(tok, lo, hi, L)
+                if share:
+                    assert self.instances[iid].kv.alloc(rid, share)
+        ev["exch"].record(st)
+        x_end = tid
+        # ---- drain (untimed): the transient residents finish
+        gone = []
+        for rid in sorted(self.transient):
+            for iid, inst in self.instances.items():
+                inst.kv.free(rid)
+                slot = self.slots[iid].drop(rid)
+                if slot is not None and iid == self.me:
+                    gone.append(slot)
+        self.pool.release(gone, 0, L, stream=st)
+        self._sync_views()
+        ev["drain"].record(st)
+        # ---- restore (engine.py:1093-1157): compaction here, pulls from holders
+        restored = False
+        for g in sorted(live.values(), key=lambda g: g.gid):
+            missing, holders = {}, {}
+            for iid in g.member_instances:
+                holders[iid] = self.instances[iid].table.held_ranges()
+                _, need = member_moves(holders[iid], (0, L))
+                if need:
+                    missing[iid] = need
+            for iid in sorted(missing):
+                for rng in missing[iid]:
+                    memory.restore_layers(self.instances[iid], rng, -1, tid=0, stream=st)
+                    restored |= iid == self.me
+            flat = {iid: rng for iid, rngs in missing.items() for rng in rngs}
+            tasks = plan_restore_transfers(flat, holders, self.model.bytes_per_layer,
+                                           self.param_chunk, tid_start=tid)
+            assert all(t.src != HOST for t in tasks)
+            tid += len(tasks)
+            self.te.register_restore(tasks, self.model.bytes_per_layer)
+            self._submit_local(tasks)
+            for iid, rngs in missing.items():
+                for rng in rngs:
+                    memory.complete_restore(self.instances[iid], rng)
+        r_end = tid
+        self._sync_views()  # compactions done before a peer reads our block tables
+        ev["restore"].record(st)
+        # ---- dissolve + consolidation (engine.py:1159-1254)
+        cons = []
+        for rid in sorted(self.tokens):
+            if rid in self.transient:
+                continue
+            home = self.home[rid]
+            g = final[home]
+            for iid in g.member_instances:
+                if iid == home:
+                    continue
+                lo, hi = g.stage_layer_map[iid]
+                left = share_bytes(self.tokens[rid], lo, hi, L, kvbpt)
+                chunks = []
+                while left > 0:
+                    take = min(self.kv_chunk, left)
+                    left -= take
+                    chunks.append(TransferTask(tid, TaskKind.KVCACHE_CHUNK, iid, home, take,
+                                               rid=rid))
+                    tid += 1
+                self.te.register_chunked_kv(chunks, (lo, hi), {rid: self.tokens[rid]})
+                cons += chunks
+        self._submit_local(cons)
+        self._sync_views()
+        self._release_sources()
+        for rid, tok in self.tokens.items():
+            if rid in self.transient:
+                continue
+            home = self.home[rid]
+            for iid, inst in self.instances.items():
+                if iid != home:
+                    inst.kv.free(rid)
+                    self.slots[iid].drop(rid)
+            inst = self.instances[home]
+            extra = tok - inst.kv.allocated_tokens.get(rid, 0)
+            if extra:
+                assert inst.kv.alloc(rid, extra)
+        ev["cons"].record(st)
+        # ---- accounting
+        done = self.te.drain()
+        for p in done:
+            k = p.task.tid
+            if k < x_end:
+                rep.bytes_kv_exchange += p.bytes_moved
+            elif k < r_end:
+                rep.bytes_param += p.bytes_moved
+            else:
+                rep.bytes_kv_consolidate += p.bytes_moved
+            rep.bytes_pulled += p.bytes_moved
+            if p.task.src != self.me:
+                rep.bytes_pulled_peer += p.bytes_moved
+        rep.kv_kernel_ms = _span_ms([p for p in done if p.task.kind is TaskKind.KVCACHE_CHUNK])
+        rep.param_kernel_ms = _span_ms([p for p in done if p.task.kind is TaskKind.PARAM_SHARD])
+        if restored:
+            rep.bytes_compaction = self.pool.last_moved_pages * self.shape.page_bytes
+        ev["cons"].synchronize()
+        parts = {"exchange": ev["t0"].elapsed_time(ev["exch"]),
+                 "restore": ev["drain"].elapsed_time(ev["restore"]),
+                 "consolidate": ev["restore"].elapsed_time(ev["cons"])}
+        parts["total"] = sum(parts.values())
+        parts["drain_untimed"] = ev["exch"].elapsed_time(ev["drain"])
+        rep.ms = parts
+        self.refill()
+        return rep
+
+    def refill(self) -> None:
+        torch = self.torch
+        for rid in sorted(self.transient):
+            self._admit(rid)
+        inf = self.pool.info()
+        from .runtime import device_bytes
+        bt = device_bytes(inf.block_table, inf.max_slots * self.L * inf.max_pages_per_seq * 4)
+        bt = bt.view(torch.int32).view(inf.max_slots, self.L, inf.max_pages_per_seq)
+        rows = []
+        for rid in sorted(self.transient):
+            if self.home[rid] == self.me:
+                npg = -(-self.tokens[rid] // self.shape.block_tokens)
+                rows.append(bt[self.slots[self.me].of[rid], :, :npg].reshape(-1))
+        if rows:
+            kv = self.pool.kv_bytes().view(torch.int32).view(-1, self.pool.page_bytes // 4)
+            kv.index_fill_(0, torch.cat(rows).long(), 0x5A5A5A5A)
+        self._sync_views()
+
+    def close(self) -> None:
+        self.torch.cuda.synchronize(self.device)
+        self.dist.barrier()
+        for v in self.views.values():
+            v.close()
+        self.dist.barrier()
+        self.pool.close()
+
+
+def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, **kw) -> dict:
+    """Warm-up + timed steps; whole-job numbers (sum of bytes over ranks,
+    max of step time over ranks) and the parity verdict."""
+    import torch.distributed as dist
+    cyc = DistCycle(rt, shape, kv_budget_bytes, **kw)
+    dev = f"cuda:{rt.device}" if dist.get_backend() == "nccl" else None
+    w0 = cyc.weight_checksums()
+    k0 = cyc.kv_checksums()
+    for _ in range(warmup):
+        cyc.step()
+    reps = [cyc.step() for _ in range(steps)]
+    ms = sum(r.ms["total"] for r in reps)
+    w_ok = cyc.weight_checksums() == w0
+    k1 = cyc.kv_checksums()
+    kv_ok = set(k0) == set(k1) and all(bool((k0[r] == k1[r]).all()) for r in k0)
+    out = {
+        "ms_total_max": max_over_ranks(ms, device=dev),
+        "bytes_total": sum_over_ranks(sum(r.bytes_pulled + r.bytes_compaction for r in reps),
+                                      device=dev),
+        "bytes_peer": sum_over_ranks(sum(r.bytes_pulled_peer for r in reps),
+                                     device=dev),
+        "peer_kernel_ms_max": max_over_ranks(sum(r.kv_kernel_ms + r.param_kernel_ms for r in reps),
+                                             device=dev),
+        "parity_fail": sum_over_ranks(0.0 if (w_ok and kv_ok) else 1.0,
+                                      device=dev),
+        "residents_local": len(k0),
+        "last": reps[-1],
+    }
+    cyc.close()
+    return out

@@ -47,6 +47,13 @@ class PoolInfo(C.Structure):
                 ("max_slots", C.c_int32), ("max_pages_per_seq", C.c_int32)]
 
 
+class ExportDesc(C.Structure):
+    _fields_ = [("model", ModelDesc), ("hbm_bytes", C.c_int64), ("head_bytes", C.c_int64),
+                ("slack_pages", C.c_int64), ("device", C.c_int32), ("max_slots", C.c_int32),
+                ("max_pages_per_seq", C.c_int32), ("n_handles", C.c_int32),
+                ("bt_ipc", C.c_uint8 * 64), ("np_ipc", C.c_uint8 * 64)]
+
+
 class Grow(C.Structure):
     _fields_ = [("slot", C.c_int32), ("layer_lo", C.c_int32), ("layer_hi", C.c_int32),
                 ("add_pages", C.c_int32)]
@@ -73,6 +80,11 @@ _sigs = {
                                  C.c_int32, C.c_int32, _I32P, C.c_int32, C.POINTER(_P)]),
     "kb_pool_destroy": (C.c_int, [_P]),
     "kb_pool_query": (C.c_int, [_P, C.POINTER(PoolInfo)]),
+    "kb_pool_export": (C.c_int, [_P, C.POINTER(ExportDesc), _I32P, C.c_int32]),
+    "kb_pool_import": (C.c_int, [C.c_int32, C.POINTER(ExportDesc), _I32P, C.c_int32,
+                                 C.POINTER(_P)]),
+    "kb_pool_view_refresh": (C.c_int, [_P, C.POINTER(C.c_uint8), C.c_int32]),
+    "kb_pool_is_view": (C.c_int, [_P]),
     "kb_drop_layers": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P]),
     "kb_restore_begin": (C.c_int, [_P, C.c_int32, C.c_int32, _S, _I64P, _I64P]),
     "kb_restore_complete": (C.c_int, [_P, C.c_int32, C.c_int32]),
@@ -228,6 +240,17 @@ class DevicePool:
     def slab_pages(self) -> int:
         return self.model.bytes_per_layer // self.shape.page_bytes
 
+    # -- cross-process export (one process per GPU; see PeerPool)
+    def export(self) -> tuple[bytes, list[int]]:
+        """(descriptor bytes, file descriptors of the head segment and every
+        layer slab).  The caller sends the fds to the peer (SCM_RIGHTS) and
+        closes its copies."""
+        desc = ExportDesc()
+        n = 1 + self.model.num_layers
+        fds = (C.c_int32 * n)()
+        _check(_lib.kb_pool_export(self.h, C.byref(desc), fds, n))
+        return bytes(desc), list(fds)
+
     # -- N1 / N3: drop and restore (memory.drop_layers / restore_layers)
     def drop_layers(self, lo: int, hi: int) -> int:
         ns = C.c_int64()
@@ -311,6 +334,77 @@ class DevicePool:
         buf = (C.c_int32 * n_pages)()
         _check(_lib.kb_read_owner(self.h, buf, n_pages))
         return np.frombuffer(bytes(buf), dtype=np.int32).copy()
+
+
+class PeerPool:
+    """Read-only view, in this process, of a pool another process owns
+    (possibly on another GPU): its slabs and pages mapped into this process's
+    VA from the owner's exported VMM handles, its block table and page
+    counts opened through CUDA IPC.  Usable as the `src` of copy_pages /
+    copy_slabs -- the pull travels over NVLink when the owner's GPU is a
+    different one.  Every mutating call is the owner's job and the library
+    refuses it on a view."""
+
+    def __init__(self, rt: Runtime, iid: int, model: ModelSpec, shape: ModelShape,
+                 desc: bytes, fds: Sequence[int]):
+        d = ExportDesc.from_buffer_copy(desc)
+        if d.model.num_layers != model.num_layers or d.model.page_bytes != shape.page_bytes:
+            raise ValueError("exported pool disagrees with the model shape")
+        self.rt = rt
+        self.iid = iid
+        self.model = model
+        self.shape = shape
+        self.owner_device = d.device
+        h = _P()
+        _check(_lib.kb_pool_import(rt.device, C.byref(d), _i32arr(list(fds)), len(fds),
+                                   C.byref(h)))
+        self.h = h
+        self.last_remap_ns = 0
+
+    def close(self) -> None:
+        if self.h:
+            _lib.kb_pool_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def refresh(self, layers_held: Sequence[int]) -> None:
+        """Re-read the owner's page counts (synchronizing) and take its layer
+        states from the caller's mirror of the owner's segment table."""
+        L = self.model.num_layers
+        held = set(layers_held)
+        arr = (C.c_uint8 * L)(*[1 if l in held else 0 for l in range(L)])
+        _check(_lib.kb_pool_view_refresh(self.h, arr, L))
+
+    def info(self) -> PoolInfo:
+        out = PoolInfo()
+        _check(_lib.kb_pool_query(self.h, C.byref(out)))
+        return out
+
+    @property
+    def page_bytes(self) -> int:
+        return self.shape.page_bytes
+
+    def npages(self, slot: int, layer: int) -> int:
+        return int(_lib.kb_pages_per_layer_count(self.h, slot, layer))
+
+    def weight_bytes(self, layer: int):
+        ptr = int(_lib.kb_weight_ptr(self.h, layer))
+        if not ptr:
+            raise DeviceError(f"layer {layer} is not held by pool {self.iid}'s owner")
+        return device_bytes(ptr, self.model.bytes_per_layer)
+
+    def kv_bytes(self):
+        inf = self.info()
+        return device_bytes(inf.kv_base, inf.max_pages * self.page_bytes)
+
+
+def is_view(pool) -> bool:
+    return bool(_lib.kb_pool_is_view(pool.h))
 
 
 # -- N4 / N5 / N7 copies ------------------------------------------------------

@@ -60,3 +60,68 @@ def test_two_ranks_share_one_plan_and_split_merges():
     assert mine0 == [(0, 1)] and mine1 == [(2, 3)]  # pairs stay on their GPU
     assert rem0 == [] and rem1 == []
     assert t0 == t1 == 2.0 and s0 == s1 == 20.0
+
+
+def _fd_worker(rank, world, port, q):
+    import tempfile
+
+    import torch.distributed as dist
+
+    from paper_2412_18169_b200.dist import exchange_fds
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # two entries per rank, each a descriptor blob plus three open files
+        mine, files = {}, []
+        for k in range(2):
+            iid = 10 * rank + k
+            fds = []
+            for j in range(3):
+                f = tempfile.TemporaryFile()
+                f.write(f"rank{rank}-entry{iid}-file{j}".encode())
+                f.flush()
+                files.append(f)
+                fds.append(os.dup(f.fileno()))
+            mine[iid] = (f"desc-{iid}".encode() * 5, fds)
+        got = exchange_fds(mine, f"t{port}")
+        for _, fds in mine.values():
+            for fd in fds:
+                os.close(fd)
+        seen = {}
+        for iid, (blob, fds) in sorted(got.items()):
+            texts = []
+            for fd in fds:
+                # received fds share the sender's file offset with every
+                # other receiver: positional reads only
+                texts.append(os.pread(fd, 100, 0).decode())
+                os.close(fd)
+            seen[iid] = (blob.decode(), texts)
+        q.put((rank, seen))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fd_exchange_passes_descriptors_between_ranks():
+    """share_pools' transport: every rank receives every other rank's
+    descriptor blobs and working file descriptors (SCM_RIGHTS)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 3
+    procs = [ctx.Process(target=_fd_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in range(world):
+        want = {}
+        for peer in range(world):
+            if peer == rank:
+                continue
+            for k in range(2):
+                iid = 10 * peer + k
+                want[iid] = (f"desc-{iid}" * 5, [f"rank{peer}-entry{iid}-file{j}" for j in range(3)])
+        assert res[rank] == want
