@@ -187,7 +187,7 @@ def copy_sweep(rt, iters: int = 5) -> dict:
 
 
 def prefill_measure(rt, tensor_peak: float, ctx: int = 32768, chunk: int = 2048,
-                    iters: int = 3) -> dict:
+                    iters: int = 3, kv_splits=None) -> dict:
     """Config 4 attention: one Qwen2.5-14B layer, a 32k-token prompt prefilled
     in 2048-token chunks over the paged pool (each chunk attends to its
     prefix + itself causally).  FLOPs = 4*Hq*d*(p*c + c(c+1)/2) per chunk
@@ -214,11 +214,13 @@ def prefill_measure(rt, tensor_peak: float, ctx: int = 32768, chunk: int = 2048,
     calls = []
     for p in range(0, ctx, chunk):
         flops += 4 * Hq * 128 * (p * chunk + chunk * (chunk + 1) // 2)
-        calls.append((dev([0]), dev([0]), dev([chunk]), dev([p])))
+        calls.append((dev([0]), dev([0]), dev([chunk]), dev([p]), p + chunk))
 
     def run():
-        for sl, off, ln, pre in calls:
-            runtime.paged_prefill(pool, 0, q, sl, off, ln, pre, chunk, out, 128 ** -0.5)
+        for sl, off, ln, pre, kvl in calls:
+            runtime.paged_prefill(pool, 0, q, sl, off, ln, pre, chunk, out, 128 ** -0.5,
+                                  max_kv_len=kvl if kv_splits is None else None,
+                                  kv_splits=kv_splits)
     run()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -314,10 +316,14 @@ def nvlink_measure(rt, shape, args) -> dict:
                         f"spanning GPU pairs; exchange + restore + consolidation over NVLink",
             "ms_per_step": round(ms / args.steps, 3),
             "peer_bytes_per_step": int(out["bytes_peer"] / args.steps),
-            "roofline": {"bound": "nvlink", "achieved": round(peer_gbs_per_gpu, 1),
-                         "peak": 900.0, "unit": "GB/s per GPU per direction",
-                         "frac": round(peer_gbs_per_gpu / 900.0, 4),
-                         "kernel": "copy_pages_kernel + copy_flat_kernel pulling from peer views"},
+            "roofline": ({"bound": "nvlink", "achieved": round(peer_gbs_per_gpu, 1),
+                          "peak": 900.0, "unit": "GB/s per GPU per direction",
+                          "frac": round(peer_gbs_per_gpu / 900.0, 4),
+                          "kernel": "copy_pages_kernel + copy_flat_kernel pulling from peer views"}
+                         if not out["peers_on_same_gpu"] else
+                         {"bound": "hbm", "note": "ranks share one GPU (KB_BENCH_BACKEND=gloo "
+                          "test mode): peer pulls read the same HBM, no NVLink",
+                          "achieved": round(peer_gbs_per_gpu, 1), "unit": "GB/s payload"}),
             "rank0_ms": {k: round(v, 3) for k, v in last.ms.items()},
             "parity_bit_exact": out["parity_fail"] == 0}
 
@@ -352,10 +358,18 @@ def main():
 
     import torch
     ws, rank, local = dist_env()
+    # one GPU per rank; KB_BENCH_BACKEND=gloo lets several ranks share one
+    # GPU to exercise the multi-rank path on a single-GPU box (NCCL refuses
+    # two ranks on one device)
+    backend = os.environ.get("KB_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     hbm_peak, _, peak_src = load_peaks()
 
     from paper_2412_18169_b200 import build as _build

@@ -240,11 +240,16 @@ int kb_paged_decode(kb_pool* pool, int32_t layer, int32_t n_q_heads, uint64_t q,
 /* Chunked prefill: for sequence i, q rows [q_off[i], q_off[i]+q_len[i]) are
  * positions [prefix[i], prefix[i]+q_len[i]) of slot slots[i]; they attend
  * causally over pages [0, prefix[i]+q_len[i]) (the chunk's K/V must be
- * appended first).  q/out: [total_q][n_q_heads][head_dim] bf16. */
+ * appended first).  q/out: [total_q][n_q_heads][head_dim] bf16.
+ * kv_splits > 1 splits every (sequence, 256-row tile, head) unit's key range
+ * into that many CTAs (wave balance on 148 SMs) whose partials a combine
+ * kernel merges; it needs kb_prefill_workspace_bytes() of device scratch. */
+int64_t kb_prefill_workspace_bytes(int32_t nseq, int32_t n_q_heads, int32_t max_q_len,
+                                   int32_t kv_splits);
 int kb_paged_prefill(kb_pool* pool, int32_t layer, int32_t n_q_heads, uint64_t q,
                      uint64_t slots, uint64_t q_off, uint64_t q_len, uint64_t prefix,
                      int32_t nseq, int32_t max_q_len, float scale, uint64_t out,
-                     uintptr_t stream);
+                     uint64_t workspace, int32_t kv_splits, uintptr_t stream);
 
 #ifdef __cplusplus
 }

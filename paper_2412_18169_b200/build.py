@@ -29,7 +29,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 
 # per-source extra flags: the prefill kernel runs 320 threads (1 CTA/SM) and
 # wants the full 200-register budget for the softmax warpgroups
-EXTRA = {"kb_prefill.cu": ["--maxrregcount=200"]}
+EXTRA = {}
 
 
 def _sources():
@@ -48,9 +48,10 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA.get(os.path.basename(src), []), "-c", src, "-o", obj]
+def _compile(src: str, verbose: bool, defines=(), obj_dir: str = OBJ) -> str:
+    obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA.get(os.path.basename(src), []), *defines, "-c", src,
+           "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -74,6 +75,19 @@ def build(verbose: bool = False, force: bool = False) -> str:
         raise RuntimeError(f"link failed:\n{res.stderr}")
     os.replace(tmp, OUT)
     return OUT
+
+
+def build_variant(out: str, defines: list[str]) -> str:
+    """A side build of the same library with extra -D flags (kernel A/B
+    experiments, loaded through KB_LIB_PATH); never the product path."""
+    obj_dir = os.path.join(ROOT, "build", "var_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(obj_dir, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, False, defines, obj_dir), _sources()))
+    res = subprocess.run([NVCC, *ARCH, "-shared", "-o", out, *objs], capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr}")
+    return out
 
 
 if __name__ == "__main__":

@@ -20,10 +20,14 @@
 // softmax runs.  O is rescaled lazily, only when a row max grows by more
 // than 2^8 (the probabilities stay bounded by 256, exact in bf16 / fp32).
 //
-// Warp roles (320 threads): 0-3 softmax tile 0, 4-7 softmax tile 1, 8 TMA
-// producer (K/V pages named by the block table), 9 MMA issuer + TMEM owner.
+// Warp roles (384 threads): 0-3 softmax tile 0, 4-7 softmax tile 1, 8 TMA
+// producer (K/V pages named by the block table), 9 MMA issuer + TMEM owner,
+// 10-11 idle; warpgroup 2 gives its registers to the softmax warpgroups
+// (setmaxnreg) so a thread holds its full 128-column S row.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+
+#include <type_traits>
 
 #include "kb_common.cuh"
 #include "kb_sm100.cuh"
@@ -31,7 +35,7 @@
 namespace kb {
 
 constexpr int kPfStages = 2;
-constexpr int kPfThreads = 320;
+constexpr int kPfThreads = 384;  // 2 softmax warpgroups + 1 producer/MMA warpgroup
 constexpr int kPfTile = 128;
 constexpr int kPfHalf = 16384;                     // 128 rows x 64 el x 2 B
 constexpr int kPfKV = 4 * kPfHalf;                 // K + V for one 128-key tile
@@ -39,12 +43,65 @@ constexpr int kPfQ = 2 * kPfHalf;                  // one 128-row Q tile
 constexpr int kPfSmem = kPfStages * kPfKV + 2 * kPfQ + 1024 + 1024;
 constexpr uint32_t kPfTmemCols = 512;              // S0 | S1 | O0 | O1
 constexpr float kRescaleLog2 = 8.0f;               // lazy-rescale threshold
+#ifndef KB_PF_REGS_SOFTMAX
+#define KB_PF_REGS_SOFTMAX 216
+#endif
+// per SMSP: 2 softmax warps x 216 + 1 warpgroup-2 warp x 64 = 496 regs/lane
+// (the full 512 deadlocks the setmaxnreg.inc on B200)
+constexpr int kPfRegsSoftmax = KB_PF_REGS_SOFTMAX;
+constexpr int kPfRegsProducer = 64;
 
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// Packed f32x2 FMA / add (sm_100a): two softmax elements per instruction.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// exp2 on the FMA pipe (FA4's trick): the MUFU unit does 16 ex2 per clock
+// per SM -- exactly the tensor pipe's pace for a 128x128 tile -- so a share
+// of the exponentials is computed as 2^j * p(f), j = round(x),
+// f = x - j in [-0.5, 0.5], p a degree-3 fit of 2^f (max rel. error 7.5e-5,
+// below the fp16 rounding of P), 2^j added into the exponent bits.
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+  const float kMagic = 12582912.0f;  // 1.5 * 2^23: round-to-nearest
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
+  const float2 jf = fadd2(t, make_float2(-kMagic, -kMagic));
+  const float2 f = fadd2(x, make_float2(-jf.x, -jf.y));
+  float2 p = ffma2(make_float2(0.0551716685f, 0.0551716685f), f,
+                   make_float2(0.2426111549f, 0.2426111549f));
+  p = ffma2(p, f, make_float2(0.6932609677f, 0.6932609677f));
+  p = ffma2(p, f, make_float2(0.9999280572f, 0.9999280572f));
+  // bits(t) << 23 == j << 23 (mod 2^32): the magic's low 9 bits are zero
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+// pairs i with i % kEmuEvery == kEmuEvery - 1 use exp2_fma2
+#ifndef KB_PF_EMU_EVERY
+#define KB_PF_EMU_EVERY 6
+#endif
+constexpr int kEmuEvery = KB_PF_EMU_EVERY;
 
 struct PrefillMisc {
   uint64_t full[kPfStages];
@@ -63,18 +120,34 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
                   const int32_t* __restrict__ q_off, const int32_t* __restrict__ q_len,
                   const int32_t* __restrict__ prefix, int mtiles,
                   __nv_bfloat16* __restrict__ out, int Hkv, int Hq, int L, int maxp, int layer,
-                  float scale_log2) {
+                  float scale_log2, float* __restrict__ part) {
   using namespace sm100;
   constexpr int kPPT = kPfTile / kB;
   const int hq = blockIdx.y;
   const int seq = blockIdx.x / mtiles, mt = blockIdx.x % mtiles;  // mt: 256-row CTA tile
+  const int split = blockIdx.z, splits = gridDim.z;
   const int h = hq / (Hq / Hkv);
   const int qlen = q_len[seq], pre = prefix[seq], qo = q_off[seq];
   const int row0 = mt * 2 * kPfTile;
   if (row0 >= qlen) return;  // grid is sized for the longest chunk
   const int rows = min(2 * kPfTile, qlen - row0);
   const int kv_len = pre + row0 + rows;  // keys visible to the last row
-  const int nt = (kv_len + kPfTile - 1) / kPfTile;
+  const int nt_all = (kv_len + kPfTile - 1) / kPfTile;
+  // KV split (flash-decoding style, for wave balance): this CTA takes key
+  // tiles [j0, j0 + nt); the partial (O, m, l) goes to `part` and
+  // prefill_combine_kernel merges the splits
+  const int j0 = (int)((int64_t)split * nt_all / splits);
+  const int nt = (int)((int64_t)(split + 1) * nt_all / splits) - j0;
+  if (nt <= 0) {
+    if (splits > 1 && threadIdx.x < 2 * kPfTile) {  // empty split: l = 0
+      const int64_t u = ((int64_t)blockIdx.x * Hq + hq) * splits + split;
+      float* ml = part + (int64_t)gridDim.x * Hq * splits * 2 * kPfTile * 128 +
+                  (u * 2 * kPfTile + threadIdx.x) * 2;
+      ml[0] = -INFINITY;
+      ml[1] = 0.f;
+    }
+    return;
+  }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   extern __shared__ uint8_t smem_raw[];
@@ -106,8 +179,15 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
   tc_fence_after();
   const uint32_t tmem = misc->tmem_base;
   const int32_t* bt_row = bt + ((int64_t)slots[seq] * L + layer) * maxp;
-
-  if (warp == 8) {
+  // register rebalancing (per SMSP: 2 softmax warps + 1 warp of warpgroup 2):
+  // the softmax rows keep all 128 S values in registers
+  if (warp >= 8) {
+#ifndef KB_PF_NO_SETMAXNREG
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kPfRegsProducer));
+#endif
+  if (warp >= 10) {
+    // spare warps of warpgroup 2: nothing to do until the final barrier
+  } else if (warp == 8) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       for (int j = 0; j < nt; ++j) {
@@ -117,7 +197,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         int npg = 0;
 #pragma unroll
         for (int k = 0; k < kPPT; ++k) {
-          const int pi = j * kPPT + k;
+          const int pi = (j0 + j) * kPPT + k;
           pages[k] = (pi * kB < kv_len) ? bt_row[pi] : -1;
           npg += pages[k] >= 0;
         }
@@ -189,8 +269,12 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       issue_pv(1, j);
       if (j + 1 < nt) issue_qk(1, j + 1);
     }
+  }
   } else {
     // ------------------------------------------------ softmax warpgroup t
+#ifndef KB_PF_NO_SETMAXNREG
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPfRegsSoftmax));
+#endif
     const int t = warp >> 2;              // query tile of this warpgroup
     const int r = tid & 127;              // row within the tile (= TMEM lane)
     const int qrow = row0 + t * kPfTile + r;  // row within the chunk
@@ -212,38 +296,59 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
     const uint32_t s_addr = tmem + lane_base + t * 128;
     const uint32_t o_addr = tmem + lane_base + 256 + t * 128;
     float m_ref = -INFINITY, l_run = 0.f;
+#ifdef KB_PF_TIMING
+    long long t_wait = 0, t_soft = 0, t_a = 0, t_b = 0, t_c = 0;
+#endif
     for (int j = 0; j < nt; ++j) {
+#ifdef KB_PF_TIMING
+      const long long tw0 = clock64();
+#endif
       mbar_wait(&misc->s_full[t], j & 1);
+#ifdef KB_PF_TIMING
+      const long long tw1 = clock64();
+      t_wait += tw1 - tw0;
+      t_a -= tw1; t_b -= tw1; t_c -= tw1;
+#endif
       tc_fence_after();
-      const int kbase = j * kPfTile;
+      const int kbase = (j0 + j) * kPfTile;
       // Tiles wholly below the warp's first query position need no mask
       // (warp-uniform); diagonal / tail tiles take the masked path.
       const int warp_q0 = pre + row0 + t * kPfTile + (warp & 3) * 32;
       const bool full_tile = kbase + kPfTile - 1 <= warp_q0 &&
                              row0 + t * kPfTile + (warp & 3) * 32 + 31 < qlen;
-      // S row in two halves of 64 columns (two loads, one wait each)
-      float mraw = -INFINITY;
+      // the whole S row (128 columns) in registers: one TMEM round trip per
+      // tile, the max and the exponentials both read the registers
+      uint32_t sr[4][32];
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t sr[2][32];
-        tmem_ld_32x32b_x32_async(s_addr + hh * 64, sr[0]);
-        tmem_ld_32x32b_x32_async(s_addr + hh * 64 + 32, sr[1]);
-        tmem_ld_wait();
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32_async(s_addr + c * 32, sr[c]);
+      tmem_ld_wait();
+#ifdef KB_PF_TIMING
+      t_a += clock64();
+#endif
+      float mr8[8];  // eight independent 3-input max chains
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          if (full_tile) {
+      for (int k = 0; k < 8; ++k) mr8[k] = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) mraw = fmaxf(mraw, __uint_as_float(sr[c][i]));
-          } else {
+      for (int c = 0; c < 4; ++c) {
+        if (full_tile) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const bool ok = row_ok && (kbase + hh * 64 + c * 32 + i) <= qpos;
-              mraw = fmaxf(mraw, ok ? __uint_as_float(sr[c][i]) : -INFINITY);
-            }
+          for (int i = 0; i < 32; i += 2)
+            mr8[(i >> 1) & 7] = fmaxf(mr8[(i >> 1) & 7],
+                                      fmaxf(__uint_as_float(sr[c][i]), __uint_as_float(sr[c][i + 1])));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const bool ok = row_ok && (kbase + c * 32 + i) <= qpos;
+            mr8[i & 7] = fmaxf(mr8[i & 7], ok ? __uint_as_float(sr[c][i]) : -INFINITY);
           }
         }
       }
+      const float mraw = fmaxf(fmaxf(fmaxf(mr8[0], mr8[1]), fmaxf(mr8[2], mr8[3])),
+                               fmaxf(fmaxf(mr8[4], mr8[5]), fmaxf(mr8[6], mr8[7])));
       const float mx = mraw * scale_log2;
+#ifdef KB_PF_TIMING
+      t_b += clock64();
+#endif
       // lazy rescale: move the reference max only when it grows by > 2^8.
       // TMEM ld/st are warp-collective, so the whole warp rescales when any
       // of its rows needs it (alpha = 1 for the others).
@@ -286,56 +391,98 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       // pass 2: P = exp2(S*scale - m_ref) as fp16 pairs (the V cache is
       // fp16, kb_append.cu), written over S: the 64 keys of S half hh land in
       // P columns [32hh, 32hh + 32) -- columns whose S values were consumed.
-      float rs = 0.f;
+      float2 rs2[4] = {};  // four partial sums: no 64-long dependent add chain
       const bool live = m_ref != -INFINITY;
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t sr[2][32];
-        tmem_ld_32x32b_x32_async(s_addr + hh * 64, sr[0]);
-        tmem_ld_32x32b_x32_async(s_addr + hh * 64 + 32, sr[1]);
-        tmem_ld_wait();
-        uint32_t w[32];
+      const float2 sc2 = make_float2(scale_log2, scale_log2);
+      const float2 nm2 = make_float2(-m_ref, -m_ref);
+      // one straight-line body per case: unmasked tiles carry no selects
+      auto p_half = [&](auto masked, auto half, uint32_t (&w)[32]) {
+        constexpr bool kMasked = decltype(masked)::value;
+        constexpr int hh = decltype(half)::value;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          float x[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = 2 * i + e;  // 0..63 within the half
-            float v = fast_exp2(fmaf(__uint_as_float(sr[col >> 5][col & 31]), scale_log2, -m_ref));
-            if (!full_tile) {
-              const int key = kbase + hh * 64 + col;
-              v = (row_ok && key <= qpos && live) ? v : 0.f;
-            }
-            x[e] = v;
+          const int col = 2 * i;  // 0..63 within the half
+          const float2 sv = make_float2(__uint_as_float(sr[2 * hh + (col >> 5)][col & 31]),
+                                        __uint_as_float(sr[2 * hh + (col >> 5)][(col & 31) + 1]));
+          const float2 xv = ffma2(sv, sc2, nm2);
+          float2 v;
+          if (i % kEmuEvery == kEmuEvery - 1) {
+            v = exp2_fma2(xv);
+          } else {
+            v.x = fast_exp2(xv.x);
+            v.y = fast_exp2(xv.y);
           }
-          rs += x[0] + x[1];
-          const __half2 hp = __floats2half2_rn(x[0], x[1]);
+          if (kMasked) {
+            const int key = kbase + hh * 64 + col;
+            v.x = (row_ok && key <= qpos && live) ? v.x : 0.f;
+            v.y = (row_ok && key + 1 <= qpos && live) ? v.y : 0.f;
+          }
+          rs2[i & 3] = fadd2(rs2[i & 3], v);
+          const __half2 hp = __floats2half2_rn(v.x, v.y);
           w[i] = *reinterpret_cast<const uint32_t*>(&hp);
         }
-        tmem_st_32x32b_x32(s_addr + hh * 32, w);
+      };
+      {
+        uint32_t w[32];
+        if (full_tile) p_half(std::false_type{}, std::integral_constant<int, 0>{}, w);
+        else p_half(std::true_type{}, std::integral_constant<int, 0>{}, w);
+        tmem_st_32x32b_x32(s_addr, w);
+        if (full_tile) p_half(std::false_type{}, std::integral_constant<int, 1>{}, w);
+        else p_half(std::true_type{}, std::integral_constant<int, 1>{}, w);
+        tmem_st_32x32b_x32(s_addr + 32, w);
       }
       tmem_st_wait();
-      l_run += rs;
+#ifdef KB_PF_TIMING
+      t_c += clock64();
+#endif
+      l_run += (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y) + (rs2[2].x + rs2[2].y) +
+               (rs2[3].x + rs2[3].y);
       tc_fence_before();
       mbar_arrive(&misc->p_ready[t]);
+#ifdef KB_PF_TIMING
+      t_soft += clock64() - tw1;
+#endif
     }
-    // epilogue: O_t / l -> bf16 rows
+#ifdef KB_PF_TIMING
+    if (lane == 0 && blockIdx.x == 7 && blockIdx.y == 0 && blockIdx.z == 0)
+      printf("pf-timing warp %d tiles %d wait %lld soft %lld | ld %lld max %lld exp+st %lld\n",
+             warp, nt, t_wait / nt, t_soft / nt, t_a / nt, t_b / nt, t_c / nt);
+#endif
+    // epilogue: O_t / l -> bf16 rows, or the split's partial (O, m, l)
     mbar_wait(&misc->o_done[t], 0);
     tc_fence_after();
-    {
+    if (splits > 1) {
+      const int64_t u = ((int64_t)blockIdx.x * Hq + hq) * splits + split;
+      const int prow = t * kPfTile + r;  // row within the CTA's 256
+      float4* po = reinterpret_cast<float4*>(part + (u * 2 * kPfTile + prow) * 128);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float part_o[32];
+        tmem_ld_32x32b_x32(o_addr + c * 32, part_o);  // warp-collective
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          po[c * 8 + q4] = make_float4(part_o[4 * q4], part_o[4 * q4 + 1], part_o[4 * q4 + 2],
+                                       part_o[4 * q4 + 3]);
+      }
+      float* ml = part + (int64_t)gridDim.x * Hq * splits * 2 * kPfTile * 128 +
+                  (u * 2 * kPfTile + prow) * 2;
+      ml[0] = l_run > 0.f ? m_ref : -INFINITY;
+      ml[1] = l_run;
+    } else {
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       int4* dst = reinterpret_cast<int4*>(out + ((int64_t)(qo + qrow) * Hq + hq) * 128);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        float part[32];
-        tmem_ld_32x32b_x32(o_addr + c * 32, part);  // warp-collective: every lane
+        float part_o[32];
+        tmem_ld_32x32b_x32(o_addr + c * 32, part_o);  // warp-collective: every lane
         if (!row_ok) continue;
 #pragma unroll
         for (int q8 = 0; q8 < 4; ++q8) {
           __nv_bfloat162 pk[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            pk[e] = __floats2bfloat162_rn(part[q8 * 8 + 2 * e] * inv, part[q8 * 8 + 2 * e + 1] * inv);
+            pk[e] = __floats2bfloat162_rn(part_o[q8 * 8 + 2 * e] * inv,
+                                          part_o[q8 * 8 + 2 * e + 1] * inv);
           dst[c * 4 + q8] = *reinterpret_cast<int4*>(pk);
         }
       }
@@ -349,14 +496,77 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
   }
 }
 
+// Merge the KV splits of every (sequence, 256-row tile, q head) unit:
+// O = sum_i O_i 2^(m_i - M) / sum_i l_i 2^(m_i - M), M = max_i m_i.
+__global__ void __launch_bounds__(256)
+prefill_combine_kernel(const float* __restrict__ part, const int32_t* __restrict__ q_off,
+                       const int32_t* __restrict__ q_len, int mtiles, int Hq, int splits,
+                       __nv_bfloat16* __restrict__ out) {
+  constexpr int kRows = 2 * kPfTile;
+  __shared__ float s_w[kRows][8];
+  __shared__ float s_inv[kRows];
+  const int unit = blockIdx.x;  // (seq * mtiles + mt) * Hq + hq
+  const int hq = unit % Hq, cta = unit / Hq;
+  const int seq = cta / mtiles, mt = cta % mtiles;
+  const int qlen = q_len[seq], qo = q_off[seq];
+  const int row0 = mt * kRows;
+  if (row0 >= qlen) return;
+  const int64_t units = (int64_t)gridDim.x;
+  const float* ml = part + units * splits * kRows * 128;
+  {
+    const int r = threadIdx.x;
+    float m = -INFINITY;
+    for (int s = 0; s < splits; ++s)
+      m = fmaxf(m, ml[(((int64_t)unit * splits + s) * kRows + r) * 2]);
+    float lsum = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float* e = ml + (((int64_t)unit * splits + s) * kRows + r) * 2;
+      const float w = (m == -INFINITY || e[0] == -INFINITY) ? 0.f : exp2f(e[0] - m);
+      s_w[r][s] = w;
+      lsum += e[1] * w;
+    }
+    s_inv[r] = lsum > 0.f ? 1.f / lsum : 0.f;
+  }
+  __syncthreads();
+  const int rows = min(kRows, qlen - row0);
+  for (int i = threadIdx.x; i < rows * 32; i += blockDim.x) {
+    const int r = i >> 5, c4 = i & 31;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < splits; ++s) {
+      const float w = s_w[r][s];
+      if (w == 0.f) continue;
+      const float4 v = reinterpret_cast<const float4*>(
+          part + (((int64_t)unit * splits + s) * kRows + r) * 128)[c4];
+      acc.x += v.x * w;
+      acc.y += v.y * w;
+      acc.z += v.z * w;
+      acc.w += v.w * w;
+    }
+    const float inv = s_inv[r];
+    __nv_bfloat162 a = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    __nv_bfloat162 b = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&a);
+    pk.y = *reinterpret_cast<uint32_t*>(&b);
+    reinterpret_cast<uint2*>(out + ((int64_t)(qo + row0 + r) * Hq + hq) * 128)[c4] = pk;
+  }
+}
+
 }  // namespace kb
 
 using namespace kb;
 
+extern "C" int64_t kb_prefill_workspace_bytes(int32_t nseq, int32_t n_q_heads, int32_t max_q_len,
+                                              int32_t kv_splits) {
+  if (kv_splits <= 1 || nseq <= 0 || max_q_len <= 0) return 0;
+  const int64_t units = (int64_t)nseq * ceil_div(max_q_len, 2 * kPfTile) * n_q_heads * kv_splits;
+  return units * 2 * kPfTile * (128 + 2) * 4;
+}
+
 extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, uint64_t q,
                                 uint64_t slots, uint64_t q_off, uint64_t q_len, uint64_t prefix,
                                 int32_t nseq, int32_t max_q_len, float scale, uint64_t out,
-                                uintptr_t stream) {
+                                uint64_t workspace, int32_t kv_splits, uintptr_t stream) {
   if (!p) return fail(KB_EINVAL, "null pool");
   if (p->view) return refuse_view();
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
@@ -372,7 +582,10 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
   // their sequence's chunk exit at once, so no host copy of q_len is needed
   const int mtiles = (int)ceil_div(max_q_len, 2 * kPfTile);
   const float scale_log2 = scale * 1.4426950408889634f;
-  dim3 grid((unsigned)(nseq * mtiles), n_q_heads);
+  const int splits = kv_splits < 1 ? 1 : kv_splits;
+  if (splits > 8) return fail(KB_EINVAL, "kv_splits must be <= 8");
+  if (splits > 1 && !workspace) return fail(KB_EINVAL, "kv_splits > 1 needs a workspace");
+  dim3 grid((unsigned)(nseq * mtiles), n_q_heads, splits);
   auto launch = [&](auto kernel) -> int {
     static bool attr = false;
     if (!attr) {
@@ -384,7 +597,7 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(q_off),
         reinterpret_cast<const int32_t*>(q_len), reinterpret_cast<const int32_t*>(prefix), mtiles,
         reinterpret_cast<__nv_bfloat16*>(out), Hkv, n_q_heads, p->m.num_layers, p->maxp, layer,
-        scale_log2);
+        scale_log2, reinterpret_cast<float*>(workspace));
     KB_LAUNCH_CHECK();
     return KB_OK;
   };
@@ -392,5 +605,12 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
   if (rc) return rc;
   rc = B == 64 ? launch(prefill_tc_kernel<64>) : launch(prefill_tc_kernel<128>);
   if (rc) return rc;
+  if (splits > 1) {
+    prefill_combine_kernel<<<nseq * mtiles * n_q_heads, 256, 0, st>>>(
+        reinterpret_cast<const float*>(workspace), reinterpret_cast<const int32_t*>(q_off),
+        reinterpret_cast<const int32_t*>(q_len), mtiles, n_q_heads, splits,
+        reinterpret_cast<__nv_bfloat16*>(out));
+    KB_LAUNCH_CHECK();
+  }
   return pool_leave(p, st);
 }

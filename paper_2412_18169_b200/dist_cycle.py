@@ -414,6 +414,7 @@ def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, **kw) -> dict:
         "parity_fail": sum_over_ranks(0.0 if (w_ok and kv_ok) else 1.0,
                                       device=dev),
         "residents_local": len(k0),
+        "peers_on_same_gpu": any(v.owner_device == rt.device for v in cyc.views.values()),
         "last": reps[-1],
     }
     cyc.close()

@@ -22,7 +22,8 @@ from typing import Optional, Sequence
 from .core import ModelShape, ModelSpec
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_kb.so")
+# KB_LIB_PATH: load a variant build of the same ABI (kernel A/B runs in tools/)
+LIB_PATH = os.environ.get("KB_LIB_PATH") or os.path.join(_HERE, "_kb.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with "
@@ -105,8 +106,9 @@ _sigs = {
     "kb_decode_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "kb_paged_decode": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, C.c_int32, C.c_int32,
                                   C.c_float, _U, _U, C.c_int32, C.c_int32, _S]),
+    "kb_prefill_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "kb_paged_prefill": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, _U, _U, C.c_int32,
-                                   C.c_int32, C.c_float, _U, _S]),
+                                   C.c_int32, C.c_float, _U, _U, C.c_int32, _S]),
 }
 for _name, (_res, _args) in _sigs.items():
     _fn = getattr(_lib, _name)
@@ -463,10 +465,62 @@ def paged_decode(pool: DevicePool, layer: int, q, slots, ctx_lens, max_ctx: int,
                                 _stream(stream)), launches=2 if reuse_plan else 3)
 
 
+def prefill_splits(nseq: int, n_q_heads: int, max_q_len: int, max_kv_len: int,
+                   n_sm: int = 148) -> int:
+    """KV splits for one prefill launch: the split count (1..8) whose grid
+    fills the last wave of CTAs best (one 256-row CTA per SM), keeping at
+    least 16 key tiles per split so the pipeline ramp stays amortised; a
+    split costs a combine pass, so it must win by 3%."""
+    units = nseq * -(-max_q_len // 256) * n_q_heads
+    tiles = -(-max_kv_len // 128)
+    best, best_eff = 1, units / (n_sm * -(-units // n_sm))
+    for s in range(2, 9):
+        if tiles < 16 * s:
+            break
+        eff = units * s / (n_sm * -(-(units * s) // n_sm))
+        if eff > best_eff + 0.03:
+            best, best_eff = s, eff
+    return best
+
+
+def prefill_workspace_bytes(nseq: int, n_q_heads: int, max_q_len: int, kv_splits: int) -> int:
+    return int(_lib.kb_prefill_workspace_bytes(nseq, n_q_heads, max_q_len, kv_splits))
+
+
 def paged_prefill(pool: DevicePool, layer: int, q, slots, q_off, q_len, prefix, max_q_len: int,
-                  out, scale: float, stream=None) -> None:
-    """q/out: [total_q, n_q_heads, 128] bf16; per-sequence int32 vectors (device)."""
-    _check(_lib.kb_paged_prefill(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
+                  out, scale: float, max_kv_len: Optional[int] = None,
+                  kv_splits: Optional[int] = None, workspace=None, stream=None) -> None:
+    """q/out: [total_q, n_q_heads, 128] bf16; per-sequence int32 vectors (device).
+    max_kv_len (host-known longest prefix + chunk) enables KV splits chosen
+    by prefill_splits; the workspace is cached on the pool when not given."""
+    nseq, hq = slots.shape[0], q.shape[1]
+    if kv_splits is None:
+        kv_splits = 1 if max_kv_len is None else prefill_splits(
+            nseq, hq, max_q_len, max_kv_len, _sm_count(pool.rt.device))
+    ws_ptr = 0
+    if kv_splits > 1:
+        need = prefill_workspace_bytes(nseq, hq, max_q_len, kv_splits)
+        if workspace is None:
+            import torch
+            ws = getattr(pool, "_prefill_ws", None)
+            if ws is None or ws.numel() < need:
+                ws = torch.empty(need, dtype=torch.uint8, device=f"cuda:{pool.rt.device}")
+                pool._prefill_ws = ws
+            workspace = ws
+        elif workspace.numel() < need:
+            raise ValueError(f"prefill workspace holds {workspace.numel()} < {need} bytes")
+        ws_ptr = workspace.data_ptr()
+    _check(_lib.kb_paged_prefill(pool.h, layer, hq, q.data_ptr(), slots.data_ptr(),
                                  q_off.data_ptr(), q_len.data_ptr(), prefix.data_ptr(),
-                                 slots.shape[0], max_q_len, scale, out.data_ptr(),
-                                 _stream(stream)), launches=1)
+                                 nseq, max_q_len, scale, out.data_ptr(), ws_ptr, kv_splits,
+                                 _stream(stream)), launches=2 if kv_splits > 1 else 1)
+
+
+_SMS: dict = {}
+
+
+def _sm_count(device: int) -> int:
+    if device not in _SMS:
+        import torch
+        _SMS[device] = torch.cuda.get_device_properties(device).multi_processor_count
+    return _SMS[device]

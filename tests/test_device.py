@@ -292,8 +292,9 @@ def test_paged_decode_matches_oracle(rt, shape):
     pool.close()
 
 
+@pytest.mark.parametrize("kv_splits", [1, 3, 8])
 @pytest.mark.parametrize("shape", ATTN_SHAPES[:2], ids=lambda s: s.name)
-def test_paged_prefill_matches_oracle(rt, shape):
+def test_paged_prefill_matches_oracle(rt, shape, kv_splits):
     from paper_2412_18169_b200 import runtime
     model = shape.spec()
     pool = rt.create_pool(0, model, model.param_bytes + 64 * MIB, shape)
@@ -320,7 +321,7 @@ def test_paged_prefill_matches_oracle(rt, shape):
     scale = 128 ** -0.5
     runtime.paged_prefill(pool, 0, q, dev(list(range(len(cases)))), dev(offs),
                           dev([c for _, c in cases]), dev([p for p, _ in cases]),
-                          max(c for _, c in cases), out, scale)
+                          max(c for _, c in cases), out, scale, kv_splits=kv_splits)
     torch.cuda.synchronize()
     got = out.float().cpu().numpy()
     for i, (pre, c) in enumerate(cases):
@@ -328,5 +329,5 @@ def test_paged_prefill_matches_oracle(rt, shape):
                            pre, scale)
         want = bf16_to_f32(f32_to_bf16(want))
         ma, mr = check_close(got[offs[i]:offs[i] + c], want)
-        assert ma <= 2e-2 and mr <= 1e-3, (shape.name, pre, c, ma, mr)
+        assert ma <= 2e-2 and mr <= 1e-3, (shape.name, kv_splits, pre, c, ma, mr)
     pool.close()
