@@ -120,7 +120,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
                   const int32_t* __restrict__ q_off, const int32_t* __restrict__ q_len,
                   const int32_t* __restrict__ prefix, int mtiles,
                   __nv_bfloat16* __restrict__ out, int Hkv, int Hq, int L, int maxp, int layer,
-                  float scale_log2, float* __restrict__ part) {
+                  float scale_log2, uint8_t* __restrict__ part) {
   using namespace sm100;
   constexpr int kPPT = kPfTile / kB;
   const int hq = blockIdx.y;
@@ -141,7 +141,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
   if (nt <= 0) {
     if (splits > 1 && threadIdx.x < 2 * kPfTile) {  // empty split: l = 0
       const int64_t u = ((int64_t)blockIdx.x * Hq + hq) * splits + split;
-      float* ml = part + (int64_t)gridDim.x * Hq * splits * 2 * kPfTile * 128 +
+      float* ml = reinterpret_cast<float*>(part + (int64_t)gridDim.x * Hq * splits * 2 * kPfTile * 256) +
                   (u * 2 * kPfTile + threadIdx.x) * 2;
       ml[0] = -INFINITY;
       ml[1] = 0.f;
@@ -454,17 +454,24 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
     if (splits > 1) {
       const int64_t u = ((int64_t)blockIdx.x * Hq + hq) * splits + split;
       const int prow = t * kPfTile + r;  // row within the CTA's 256
-      float4* po = reinterpret_cast<float4*>(part + (u * 2 * kPfTile + prow) * 128);
+      // partial O normalised by its own l, as fp16 (|O/l| <= max |v|; the
+      // combine re-weights by l * 2^(m - M))
+      int4* po = reinterpret_cast<int4*>(part + (u * 2 * kPfTile + prow) * 256);
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float part_o[32];
         tmem_ld_32x32b_x32(o_addr + c * 32, part_o);  // warp-collective
 #pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4)
-          po[c * 8 + q4] = make_float4(part_o[4 * q4], part_o[4 * q4 + 1], part_o[4 * q4 + 2],
-                                       part_o[4 * q4 + 3]);
+        for (int q8 = 0; q8 < 4; ++q8) {
+          __half2 pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            pk[e] = __floats2half2_rn(part_o[q8 * 8 + 2 * e] * inv, part_o[q8 * 8 + 2 * e + 1] * inv);
+          po[c * 4 + q8] = *reinterpret_cast<int4*>(pk);
+        }
       }
-      float* ml = part + (int64_t)gridDim.x * Hq * splits * 2 * kPfTile * 128 +
+      float* ml = reinterpret_cast<float*>(part + (int64_t)gridDim.x * Hq * splits * 2 * kPfTile * 256) +
                   (u * 2 * kPfTile + prow) * 2;
       ml[0] = l_run > 0.f ? m_ref : -INFINITY;
       ml[1] = l_run;
@@ -499,12 +506,11 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 // Merge the KV splits of every (sequence, 256-row tile, q head) unit:
 // O = sum_i O_i 2^(m_i - M) / sum_i l_i 2^(m_i - M), M = max_i m_i.
 __global__ void __launch_bounds__(256)
-prefill_combine_kernel(const float* __restrict__ part, const int32_t* __restrict__ q_off,
+prefill_combine_kernel(const uint8_t* __restrict__ part, const int32_t* __restrict__ q_off,
                        const int32_t* __restrict__ q_len, int mtiles, int Hq, int splits,
                        __nv_bfloat16* __restrict__ out) {
   constexpr int kRows = 2 * kPfTile;
   __shared__ float s_w[kRows][8];
-  __shared__ float s_inv[kRows];
   const int unit = blockIdx.x;  // (seq * mtiles + mt) * Hq + hq
   const int hq = unit % Hq, cta = unit / Hq;
   const int seq = cta / mtiles, mt = cta % mtiles;
@@ -512,43 +518,46 @@ prefill_combine_kernel(const float* __restrict__ part, const int32_t* __restrict
   const int row0 = mt * kRows;
   if (row0 >= qlen) return;
   const int64_t units = (int64_t)gridDim.x;
-  const float* ml = part + units * splits * kRows * 128;
+  const float* ml = reinterpret_cast<const float*>(part + units * splits * kRows * 256);
   {
     const int r = threadIdx.x;
     float m = -INFINITY;
     for (int s = 0; s < splits; ++s)
       m = fmaxf(m, ml[(((int64_t)unit * splits + s) * kRows + r) * 2]);
-    float lsum = 0.f;
+    float wsum = 0.f;
     for (int s = 0; s < splits; ++s) {
       const float* e = ml + (((int64_t)unit * splits + s) * kRows + r) * 2;
-      const float w = (m == -INFINITY || e[0] == -INFINITY) ? 0.f : exp2f(e[0] - m);
+      const float w = (m == -INFINITY || e[0] == -INFINITY) ? 0.f : e[1] * exp2f(e[0] - m);
       s_w[r][s] = w;
-      lsum += e[1] * w;
+      wsum += w;
     }
-    s_inv[r] = lsum > 0.f ? 1.f / lsum : 0.f;
+    const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+    for (int s = 0; s < splits; ++s) s_w[r][s] *= inv;
   }
   __syncthreads();
   const int rows = min(kRows, qlen - row0);
-  for (int i = threadIdx.x; i < rows * 32; i += blockDim.x) {
-    const int r = i >> 5, c4 = i & 31;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  // 16 threads per row, 8 fp16 (16 B) each
+  for (int i = threadIdx.x; i < rows * 16; i += blockDim.x) {
+    const int r = i >> 4, c8 = i & 15;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int s = 0; s < splits; ++s) {
       const float w = s_w[r][s];
       if (w == 0.f) continue;
-      const float4 v = reinterpret_cast<const float4*>(
-          part + (((int64_t)unit * splits + s) * kRows + r) * 128)[c4];
-      acc.x += v.x * w;
-      acc.y += v.y * w;
-      acc.z += v.z * w;
-      acc.w += v.w * w;
+      const int4 v = reinterpret_cast<const int4*>(
+          part + (((int64_t)unit * splits + s) * kRows + r) * 256)[c8];
+      const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(h[e]);
+        acc[2 * e] += f.x * w;
+        acc[2 * e + 1] += f.y * w;
+      }
     }
-    const float inv = s_inv[r];
-    __nv_bfloat162 a = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-    __nv_bfloat162 b = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&a);
-    pk.y = *reinterpret_cast<uint32_t*>(&b);
-    reinterpret_cast<uint2*>(out + ((int64_t)(qo + row0 + r) * Hq + hq) * 128)[c4] = pk;
+    __nv_bfloat162 pk[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) pk[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+    reinterpret_cast<int4*>(out + ((int64_t)(qo + row0 + r) * Hq + hq) * 128)[c8] =
+        *reinterpret_cast<int4*>(pk);
   }
 }
 
@@ -560,7 +569,7 @@ extern "C" int64_t kb_prefill_workspace_bytes(int32_t nseq, int32_t n_q_heads, i
                                               int32_t kv_splits) {
   if (kv_splits <= 1 || nseq <= 0 || max_q_len <= 0) return 0;
   const int64_t units = (int64_t)nseq * ceil_div(max_q_len, 2 * kPfTile) * n_q_heads * kv_splits;
-  return units * 2 * kPfTile * (128 + 2) * 4;
+  return units * 2 * kPfTile * (128 * 2 + 2 * 4);  // fp16 O/l + (m, l) per row
 }
 
 extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, uint64_t q,
@@ -597,7 +606,7 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(q_off),
         reinterpret_cast<const int32_t*>(q_len), reinterpret_cast<const int32_t*>(prefix), mtiles,
         reinterpret_cast<__nv_bfloat16*>(out), Hkv, n_q_heads, p->m.num_layers, p->maxp, layer,
-        scale_log2, reinterpret_cast<float*>(workspace));
+        scale_log2, reinterpret_cast<uint8_t*>(workspace));
     KB_LAUNCH_CHECK();
     return KB_OK;
   };
@@ -607,7 +616,7 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
   if (rc) return rc;
   if (splits > 1) {
     prefill_combine_kernel<<<nseq * mtiles * n_q_heads, 256, 0, st>>>(
-        reinterpret_cast<const float*>(workspace), reinterpret_cast<const int32_t*>(q_off),
+        reinterpret_cast<const uint8_t*>(workspace), reinterpret_cast<const int32_t*>(q_off),
         reinterpret_cast<const int32_t*>(q_len), mtiles, n_q_heads, splits,
         reinterpret_cast<__nv_bfloat16*>(out));
     KB_LAUNCH_CHECK();

@@ -150,15 +150,23 @@ class OverloadCycle:
         page on its home pool after the cycle (the step's result, read back
         by bench.py's end-to-end leg); -1 for transient residents."""
         torch = self.torch
-        rows = []
-        for rid in sorted(self.tokens):
+        order = sorted(self.tokens)
+        out = torch.full((len(order),), -1, dtype=torch.int32, device="cuda")
+        per_pool: dict[int, tuple[list[int], list[int]]] = {}
+        for k, rid in enumerate(order):
             if rid in self.transient:
-                rows.append(torch.full((1,), -1, dtype=torch.int32, device="cuda"))
                 continue
             iid = self.home[rid]
-            bt = self._bt_view(iid)
-            rows.append(bt[self.slots[iid].of[rid], 0, :1])
-        return torch.cat(rows)
+            pos, cell = per_pool.setdefault(iid, ([], []))
+            pos.append(k)
+            cell.append(self.slots[iid].of[rid] * self.L * self._maxp(iid))  # layer 0, page 0
+        for iid, (pos, cell) in per_pool.items():
+            bt = self._bt_view(iid).reshape(-1)
+            out[torch.tensor(pos, device="cuda")] = bt[torch.tensor(cell, device="cuda")]
+        return out
+
+    def _maxp(self, iid) -> int:
+        return self.pools[iid].rt.max_pages_per_seq
 
     def _bt_view(self, iid):
         torch = self.torch

@@ -164,7 +164,7 @@ class StageRunner:
                 op = torch.empty_like(qp)
                 runtime.paged_prefill(self.pool, l, qp, batch["p_slots"], batch["p_off"],
                                       batch["p_len"], batch["p_prefix"], batch["p_max"], op,
-                                      self.scale)
+                                      self.scale, max_kv_len=batch.get("p_kv_max"))
                 o.index_copy_(0, batch["p_rows"], op)
             if batch["nd"]:
                 qd = q.index_select(0, batch["d_rows"]).contiguous()
@@ -346,6 +346,7 @@ class DeviceEngine(Engine):
                 "np": len(p_slots), "p_rows": i64(p_rows), "p_slots": i32(p_slots),
                 "p_off": i32(p_off), "p_len": i32(p_len), "p_prefix": i32(p_prefix),
                 "p_max": max(p_len) if p_len else 0,
+                "p_kv_max": max((a + b for a, b in zip(p_prefix, p_len)), default=0),
                 "nd": len(d_slots), "d_rows": i64(d_rows), "d_slots": i32(d_slots),
                 "d_ctx": i32(d_ctx), "d_max": max(d_ctx) if d_ctx else 0,
                 "last": i64(last_rows),

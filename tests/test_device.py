@@ -245,6 +245,33 @@ def test_slab_restore_pull_bit_exact(rt):
     b.close()
 
 
+def test_host_replica_restore_through_the_plan(rt):
+    """exchange.HOST (exchange.py:18, 224-233): when no live instance holds a
+    layer, plan_restore_transfers sources it from the host replica; the
+    transfer engine pulls it from pinned host memory into the vacated slab."""
+    from paper_2412_18169_b200 import memory
+    from paper_2412_18169_b200.exchange import HOST, plan_restore_transfers
+    from paper_2412_18169_b200.transfer import SlotTable, TransferEngine
+    model = TINY.spec()
+    inst = memory.build_instance(0, model, model.param_bytes + MIB, 25_000_000_000,
+                                 device=rt, shape=TINY)
+    host = torch.randint(0, 256, (model.param_bytes,), dtype=torch.uint8).pin_memory()
+    memory.drop_layers(inst, (0, 2))
+    task = memory.restore_layers(inst, (0, 2), HOST)
+    tasks = plan_restore_transfers({0: (0, 2)}, {0: []}, model.bytes_per_layer, 1 << 20)
+    assert tasks and all(t.src == HOST and t.dst == 0 for t in tasks)
+    assert sum(t.size_bytes for t in tasks) == task.size_bytes
+    te = TransferEngine({0: inst.pool}, {0: SlotTable(rt.max_slots)}, host_replica=host)
+    te.register_restore(tasks, model.bytes_per_layer)
+    te.submit_many(tasks)
+    te.drain()
+    memory.complete_restore(inst, (0, 2))
+    for l in range(2):
+        lo = l * model.bytes_per_layer
+        assert torch.equal(inst.pool.weight_bytes(l).cpu(), host[lo:lo + model.bytes_per_layer])
+    inst.pool.close()
+
+
 ATTN_SHAPES = [
     ModelShape("g2", num_layers=2, hidden=256, n_q_heads=2, n_kv_heads=1, head_dim=128,
                ffn=768, vocab=1024, block_tokens=64),
