@@ -18,8 +18,10 @@ metric   drop/restore GB/s = payload bytes moved per step / step device time
 paged_decode   tcgen05 paged-decode attention over the merged (enlarged)
          pools, all 32 layers per token, tok/s
 p99_ttft  the reference's scheduler on real Llama-3-8B pools with measured
-         stage times (serving.DeviceEngine), KunServe vs recompute on one 4x
-         ShareGPT-shaped burst (ttft.py)
+         stage times (serving.DeviceEngine), KunServe vs the reference's three
+         baselines -- recompute, swap (pages to pinned host memory over PCIe)
+         and migrate (pages to the other replica) -- on one 4x ShareGPT-shaped
+         burst (ttft.py)
 With --gpus N each rank runs its own pair of replicas on its GPU (the path
 shards into independent groups: scaling "weak", no data-path collective).
 """

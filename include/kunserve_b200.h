@@ -213,6 +213,12 @@ int kb_copy_slabs(kb_pool* dst, kb_pool* src, int32_t lo, int32_t hi, int64_t by
 /* HOST replica source (exchange.py:18, 224-233): pinned host -> weight VA. */
 int kb_copy_slabs_from_host(kb_pool* dst, const void* host_src, int32_t lo, int32_t hi,
                             int64_t byte_lo, int64_t byte_hi, uintptr_t stream);
+/* Swap baseline (engine.py:906-970, KV to / from the HOST pseudo instance):
+ * the pages of move->src_slot, layers [layer_lo, layer_hi), flattened pages
+ * [flat_lo, flat_hi) to (to_host = 1) or from (0) a pinned host buffer
+ * holding flattened page f at host + f * page_bytes (dst_slot unused). */
+int kb_copy_pages_host(kb_pool* pool, const kb_move* move, void* host, int32_t to_host,
+                       uintptr_t stream);
 /* Activation hand-off between pipeline stages (engine.py:428-448) and any
  * other flat device-to-device (peer) copy: 16-byte vector kernel. */
 int kb_copy_bytes(uint64_t dst, uint64_t src, int64_t nbytes, uintptr_t stream);

@@ -93,6 +93,28 @@ copy_pages_kernel(PoolView dst, PoolView src, const __grid_constant__ MoveBatch 
   }
 }
 
+// Pages of one (slot, layer range) <-> a flat host buffer (pinned, mapped
+// into the device VA): flattened page f = (layer - lo) * npages + i sits at
+// host + f * page_bytes.  The SMs drive the PCIe / C2C transfer with 16-byte
+// loads and stores, like the peer copies.
+__global__ void __launch_bounds__(kThreads)
+copy_pages_host_kernel(PoolView pool, uint8_t* __restrict__ host, kb_move mv, int64_t total_pages,
+                       int64_t page_bytes, int64_t pieces, int to_host) {
+  const int64_t piece_bytes = page_bytes / pieces;
+  for (int64_t job = blockIdx.x; job < total_pages * pieces; job += gridDim.x) {
+    const int64_t f = mv.flat_lo + job / pieces, pc = job % pieces;
+    const int layer = mv.layer_lo + (int)(f / mv.npages);
+    const int idx = (int)(f % mv.npages);
+    const int32_t pg = pool.bt[((int64_t)mv.src_slot * pool.L + layer) * pool.maxp + idx];
+    uint8_t* dev = pool.kv + (int64_t)pg * page_bytes + pc * piece_bytes;
+    uint8_t* hst = host + f * page_bytes + pc * piece_bytes;
+    if (to_host)
+      block_copy(reinterpret_cast<int4*>(hst), reinterpret_cast<const int4*>(dev), piece_bytes / 16);
+    else
+      block_copy(reinterpret_cast<int4*>(dev), reinterpret_cast<const int4*>(hst), piece_bytes / 16);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
 copy_flat_kernel(int4* __restrict__ d, const int4* __restrict__ s, int64_t nvec) {
   // grid-stride over 32 KiB pieces
@@ -235,4 +257,35 @@ extern "C" int kb_copy_slabs_from_host(kb_pool* dst, const void* host_src, int32
 extern "C" int kb_copy_bytes(uint64_t dst, uint64_t src, int64_t nbytes, uintptr_t stream) {
   if (nbytes < 0) return fail(KB_EINVAL, "negative size");
   return launch_flat(dst, src, nbytes, (cudaStream_t)stream);
+}
+
+extern "C" int kb_copy_pages_host(kb_pool* p, const kb_move* mv, void* host, int32_t to_host,
+                                  uintptr_t stream) {
+  if (!p || !mv || !host) return fail(KB_EINVAL, "null argument");
+  if (p->view) return refuse_view();
+  const int L = p->m.num_layers;
+  if (mv->layer_lo < 0 || mv->layer_hi > L || mv->layer_hi <= mv->layer_lo || mv->npages < 0 ||
+      mv->flat_lo < 0 || mv->flat_hi < mv->flat_lo ||
+      mv->flat_hi > (mv->layer_hi - mv->layer_lo) * mv->npages || mv->src_slot < 0 ||
+      mv->src_slot >= p->max_slots)
+    return fail(KB_EINVAL, "bad host move");
+  for (int l = mv->layer_lo; l < mv->layer_hi; ++l)
+    if (p->h_np[(int64_t)mv->src_slot * L + l] < mv->npages)
+      return fail(KB_EINVAL, "host move names pages that are not allocated");
+  const int64_t total = mv->flat_hi - mv->flat_lo;
+  if (total == 0) return KB_OK;
+  KB_RT(cudaSetDevice(p->device));
+  void* dhost = nullptr;
+  // pinned host memory is mapped into the device VA (UVA): same address
+  KB_RT(cudaHostGetDevicePointer(&dhost, host, 0));
+  if ((reinterpret_cast<uintptr_t>(dhost) & 15) != 0) return fail(KB_EINVAL, "host buffer must be 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t pieces = p->m.page_bytes > kPiece ? p->m.page_bytes / kPiece : 1;
+  PoolView pv{p->d_bt, reinterpret_cast<uint8_t*>(p->kva), L, p->maxp};
+  int rc = pool_enter(p, st);
+  if (rc) return rc;
+  copy_pages_host_kernel<<<grid_for(total * pieces, 1, 148 * 4), kThreads, 0, st>>>(
+      pv, static_cast<uint8_t*>(dhost), *mv, total, p->m.page_bytes, pieces, to_host);
+  KB_LAUNCH_CHECK();
+  return pool_leave(p, st);
 }

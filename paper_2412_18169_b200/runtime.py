@@ -102,6 +102,7 @@ _sigs = {
     "kb_copy_slabs_from_host": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int64,
                                           C.c_int64, _S]),
     "kb_copy_bytes": (C.c_int, [_U, _U, C.c_int64, _S]),
+    "kb_copy_pages_host": (C.c_int, [_P, C.POINTER(Move), _P, C.c_int32, _S]),
     "kb_kv_append": (C.c_int, [_P, C.c_int32, _U, _U, _U, _U, C.c_int32, _S]),
     "kb_decode_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "kb_paged_decode": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, C.c_int32, C.c_int32,
@@ -431,6 +432,20 @@ def copy_slabs_from_host(dst: DevicePool, host_ptr: int, lo: int, hi: int, byte_
                          byte_hi: int, stream=None) -> None:
     _check(_lib.kb_copy_slabs_from_host(dst.h, C.c_void_p(host_ptr), lo, hi, byte_lo, byte_hi,
                                         _stream(stream)))
+
+
+def copy_pages_host(pool: DevicePool, slot: int, layer_lo: int, layer_hi: int, npages: int,
+                    host, to_host: bool, flat_lo: int = 0, flat_hi: Optional[int] = None,
+                    stream=None) -> None:
+    """Pages of `slot` (layers [lo, hi), npages each, flattened layer-major)
+    to / from the pinned host tensor `host` (swap baseline)."""
+    if flat_hi is None:
+        flat_hi = (layer_hi - layer_lo) * npages
+    if host.numel() * host.element_size() < flat_hi * pool.page_bytes:
+        raise ValueError("host buffer too small for the pages")
+    mv = Move(slot, slot, layer_lo, layer_hi, npages, flat_lo, flat_hi, 0)
+    _check(_lib.kb_copy_pages_host(pool.h, C.byref(mv), C.c_void_p(host.data_ptr()),
+                                   1 if to_host else 0, _stream(stream)), launches=1)
 
 
 def copy_bytes(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:

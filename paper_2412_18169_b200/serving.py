@@ -20,8 +20,11 @@ and replaces the emulated device with real work:
 Link times (activations, KV exchange, restores) stay on the reference's link
 model with the configured bandwidth (NVLink-5 in bench.py), because the
 replicas of a one-GPU run share one HBM rather than an NVLink.
-Supported policies: kunserve and recompute (the others move KV to host /
-between groups outside the drop path).
+Supported policies: kunserve and the reference's three baselines
+(engine.py:863-1047) -- recompute (evict + re-prefill), swap (the victim's
+pages to pinned host memory and back, SM-driven over PCIe:
+kb_copy_pages_host) and migrate (the victim's pages to another replica's
+pool: kb_copy_pages).
 """
 
 from __future__ import annotations
@@ -187,8 +190,8 @@ class DeviceEngine(Engine):
         import torch
         self.torch = torch
         pol = policy or cfg.policy.kind
-        if pol not in ("kunserve", "recompute"):
-            raise ValueError(f"device mode supports kunserve and recompute, not {pol}")
+        if pol not in ("kunserve", "recompute", "swap", "migrate"):
+            raise ValueError(f"unknown policy {pol}")
         if runtimes is None:
             runtimes = {d: runtime.Runtime(d, max_slots=cfg.device.max_slots,
                                            max_pages_per_seq=cfg.device.max_pages_per_seq)
@@ -262,7 +265,25 @@ class DeviceEngine(Engine):
     def _run_task(self, task: TransferTask) -> None:
         if task.kind is TaskKind.ACTIVATION:
             return  # the stage inputs were handed over when the round executed
+        if task.kind is TaskKind.KVCACHE_CHUNK and task.tid not in self.te.chunk_of:
+            # a baseline's whole-request move (swap out / in, migrate): the
+            # request's pages of every layer, destination pages already allocated
+            self.te.register_request_move(task, (0, self.model.num_layers),
+                                          self.requests[task.rid].context_len)
         self.te.submit(task)
+
+    def _swap_in_done(self, gid, task, when) -> None:
+        self.te.drain()             # the host copy has been read
+        self.te.release_host(task.rid)
+        super()._swap_in_done(gid, task, when)
+
+    def _migrate_done(self, src_gid, dst_gid, task, tokens, when) -> None:
+        # the source pages free behind the copy (same stream, device-ordered)
+        slot = self.slots[task.src].of.get(task.rid)
+        if slot is not None:
+            self.pools[task.src].release([slot], 0, self.model.num_layers, stream=self.te.bulk)
+            self.slots[task.src].drop(task.rid)
+        super()._migrate_done(src_gid, dst_gid, task, tokens, when)
 
     def _on_exchange_planned(self, tasks, old_map, new_map, tokens) -> None:
         self.te.register_exchange(tasks, old_map, new_map, tokens)
@@ -400,15 +421,18 @@ class DeviceEngine(Engine):
 
 def device_config(shape, instances: int = 2, kv_bytes: int = 8 << 30, devices=(0,),
                   nvlink_bandwidth: int = 900_000_000_000, link_latency_us: int = 5,
+                  host_bandwidth: int = 50_000_000_000,
                   map_latency_us: int = 0):
     """SimConfig for `instances` replicas of `shape` with `kv_bytes` of KV
-    budget each, NVLink-5 links and the aliased-slab remap cost."""
+    budget each, NVLink-5 links, a PCIe Gen5 x16 host link (swap baseline)
+    and the aliased-slab remap cost."""
     from .config import SimConfig
     cfg = SimConfig()
     cfg.model = shape.spec()
     cfg.cluster.instances = instances
     cfg.cluster.hbm_bytes = cfg.model.param_bytes + kv_bytes
     cfg.cluster.nic_bandwidth = nvlink_bandwidth
+    cfg.cluster.host_bandwidth = host_bandwidth
     cfg.cluster.link_base_latency_us = link_latency_us
     cfg.cluster.map_latency_us = map_latency_us
     cfg.device.shape = shape

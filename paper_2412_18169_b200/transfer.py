@@ -68,6 +68,7 @@ class KVFlow:
     done_chunks: int = 0
     submitted: int = 0
     grown: bool = False
+    release_src: bool = True  # False: the engine frees the source itself (baseline moves)
 
     @property
     def total(self) -> int:
@@ -115,6 +116,8 @@ class TransferEngine:
         self.pending: list[Pending] = []
         self.stats = TransferStats()
         self.timing = timing
+        # swapped-out KV (HOST endpoint): rid -> (pinned tensor, layers, npages)
+        self.host_kv: dict[int, tuple] = {}
 
     # -------------------------------------------------------------- planning
     def register_exchange(self, tasks: list[TransferTask], old_map: dict, new_map: dict,
@@ -165,6 +168,57 @@ class TransferEngine:
             self.flows[key] = KVFlow(rid, j, key[2], layers, npages, len(chunks))
             for idx, t in enumerate(chunks):
                 self.chunk_of[t.tid] = (key, idx)
+
+    def register_request_move(self, task: TransferTask, layers: tuple[int, int],
+                              context_tokens: int) -> None:
+        """A baseline policy's whole-request KV move as one task (swap out /
+        swap in / migrate, engine.py:906-1047): every page of `layers`.  The
+        destination's pages already exist (the engine allocated them before
+        enqueueing), so the flow is not grown here; a HOST destination gets
+        a pinned buffer, a HOST source is the buffer of the swap-out."""
+        rid, j, k = task.rid, task.src, task.dst
+        if j == HOST:
+            buf, hl, npages = self.host_kv[rid]
+            if hl != layers:
+                raise ValueError(f"rid {rid}: swapped out layers {hl}, swap-in asks {layers}")
+        else:
+            npages = self._flow_pages(j, rid, context_tokens, layers[0])
+        key = (rid, j, k)
+        self.flows[key] = KVFlow(rid, j, k, layers, npages, 1, grown=True, release_src=False)
+        self.chunk_of[task.tid] = (key, 0)
+
+    def _run_host_flow(self, fl: KVFlow, stream) -> int:
+        """Swap out (device -> pinned host) or swap in (host -> device)."""
+        lo, hi = fl.layers
+        if fl.dst == HOST:
+            pool = self.pools[fl.src]
+            buf = self.torch.empty((hi - lo) * fl.npages * pool.page_bytes, dtype=self.torch.uint8,
+                                   pin_memory=True)
+            self.host_kv[fl.rid] = (buf, fl.layers, fl.npages)
+            if fl.npages:
+                runtime.copy_pages_host(pool, self.slots[fl.src].get(fl.rid), lo, hi, fl.npages,
+                                        buf, True, stream=stream)
+            return (hi - lo) * fl.npages * pool.page_bytes
+        pool = self.pools[fl.dst]
+        buf, _, npages = self.host_kv[fl.rid]
+        slot = self.slots[fl.dst].get(fl.rid)
+        have = min(pool.npages(slot, l) for l in range(lo, hi))
+        if have >= npages:
+            if npages:
+                runtime.copy_pages_host(pool, slot, lo, hi, npages, buf, False, stream=stream)
+        else:  # fewer pages re-allocated than swapped out: per layer, the first `have`
+            per = npages * pool.page_bytes
+            for l in range(lo, hi):
+                view = buf[(l - lo) * per:(l - lo + 1) * per]
+                if have:
+                    runtime.copy_pages_host(pool, slot, l, l + 1, have, view, False,
+                                            stream=stream)
+            npages = have
+        return (hi - lo) * npages * pool.page_bytes
+
+    def release_host(self, rid: int) -> None:
+        """Drop a swapped-in request's host copy (after its copy landed)."""
+        self.host_kv.pop(rid, None)
 
     # -------------------------------------------------------------- execution
     def submit(self, task: TransferTask, cb: Optional[Callable] = None) -> None:
@@ -262,6 +316,8 @@ class TransferEngine:
         key, idx = self.chunk_of.pop(task.tid)
         fl = self.flows[key]
         fl.submitted += 1
+        if fl.src == HOST or fl.dst == HOST:
+            return self._run_host_flow(fl, stream)
         src, dst = self.pools[fl.src], self.pools[fl.dst]
         s_slot = self.slots[fl.src].get(fl.rid)
         d_slot = self.slots[fl.dst].get(fl.rid)
@@ -307,7 +363,7 @@ class TransferEngine:
         batches: dict[tuple[int, tuple[int, int]], list[int]] = {}
         for key, fl in list(self.flows.items()):
             if fl.done_chunks == fl.n_chunks or (ordered and fl.submitted == fl.n_chunks):
-                slot = self.slots[fl.src].of.get(fl.rid)
+                slot = self.slots[fl.src].of.get(fl.rid) if fl.release_src else None
                 if slot is not None:
                     batches.setdefault((fl.src, fl.layers), []).append(slot)
                 del self.flows[key]

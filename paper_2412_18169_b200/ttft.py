@@ -78,7 +78,8 @@ def fit_stage_samples(samples, num_layers: int) -> dict:
             "reference_defaults": {"alpha": 6.6e-9, "beta": 2.8e-6, "gamma": 9.6e-3}}
 
 
-def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b", **trace_kw) -> dict:
+def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b",
+            policies=("kunserve", "recompute", "swap", "migrate"), **trace_kw) -> dict:
     shape = SHAPES[shape_name]
     trace = burst_trace(**trace_kw)
     # warm-up: load every kernel / cuBLAS heuristic and walk one drop cycle
@@ -87,17 +88,30 @@ def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b", **trace_kw) -> d
     run_policy("kunserve", warm, shape, int(0.25 * (1 << 30)))
     res = {}
     samples_all = []
-    for pol in ("kunserve", "recompute"):
+    for pol in policies:
         r, samples = run_policy(pol, trace, shape, int(kv_gib * (1 << 30)))
         res[pol] = r
         samples_all += samples
     k, r = res["kunserve"], res["recompute"]
     ratio = (r["p99_ttft_s"] / k["p99_ttft_s"]) if k["p99_ttft_s"] and r["p99_ttft_s"] else None
+    # the reference's acceptance criterion 4 (tests/test_acceptance.py:146-163)
+    # on hardware: P99 TTFT ratio vs EVERY baseline, P50 TPOT ratio vs the best
+    base = [p for p in policies if p != "kunserve"]
+    ttft_ratio = min((res[p]["p99_ttft_s"] or 0) / k["p99_ttft_s"] for p in base) \
+        if k["p99_ttft_s"] else None
+    tpot_ratio = k["p50_tpot_s"] / min(res[p]["p50_tpot_s"] for p in base) \
+        if k["p50_tpot_s"] else None
     return {"value": k["p99_ttft_all_s"], "unit": "s",
             "baseline_recompute_s": r["p99_ttft_all_s"],
             "baseline_recompute_served_only_s": r["p99_ttft_s"],
             "p99_ratio_recompute_over_kunserve_served_only": round(ratio, 2) if ratio else None,
-            "kunserve": k, "recompute": r,
+            "criterion_4": {"p99_ttft_ratio_min_over_baselines": round(ttft_ratio, 2)
+                            if ttft_ratio else None,
+                            "p50_tpot_ratio_vs_best_baseline": round(tpot_ratio, 3)
+                            if tpot_ratio else None,
+                            "bounds": "ttft ratio >= 5, tpot ratio <= 1.35 "
+                                      "(reference desk config; this is a different model/trace)"},
+            **{p: res[p] for p in policies},
             "trace": {"requests": len(trace), "input_mean": trace_kw.get("input_mean", 1660),
                       "output_mean": trace_kw.get("output_mean", 64), "burst": "4x",
                       "kv_budget_gib_per_replica": kv_gib},

@@ -245,6 +245,33 @@ def test_slab_restore_pull_bit_exact(rt):
     b.close()
 
 
+def test_swap_pages_round_trip_bit_exact(rt):
+    """Swap baseline (engine.py:906-970): a request's pages to pinned host
+    memory, its device pages released and re-grown elsewhere, then back --
+    every byte returns."""
+    from paper_2412_18169_b200 import runtime
+    model = TINY.spec()
+    pool = rt.create_pool(0, model, model.param_bytes + 4 * MIB, TINY)
+    pb = pool.page_bytes
+    assert pool.grow([(0, 0, 2, 5)])
+    kv = pool.kv_bytes().view(torch.uint8).view(-1, pb)
+    pages = [pool.block_table(0, l) for l in range(2)]
+    want = torch.randint(0, 256, (10, pb), dtype=torch.uint8, device="cuda")
+    kv[torch.tensor(pages[0] + pages[1], device="cuda")] = want
+    host = torch.empty(10 * pb, dtype=torch.uint8).pin_memory()
+    runtime.copy_pages_host(pool, 0, 0, 2, 5, host, True)
+    pool.release([0], 0, 2)
+    assert pool.grow([(1, 0, 2, 3)])   # occupy the freed pages with another slot
+    assert pool.grow([(0, 0, 2, 5)])   # the request comes back on other pages
+    runtime.copy_pages_host(pool, 0, 0, 2, 5, host, False)
+    torch.cuda.synchronize()
+    assert torch.equal(host.view(10, pb), want.cpu())
+    back = [pool.block_table(0, l) for l in range(2)]
+    assert back != pages
+    assert torch.equal(kv[torch.tensor(back[0] + back[1], device="cuda")], want)
+    pool.close()
+
+
 def test_host_replica_restore_through_the_plan(rt):
     """exchange.HOST (exchange.py:18, 224-233): when no live instance holds a
     layer, plan_restore_transfers sources it from the host replica; the

@@ -30,7 +30,7 @@ def built():
     build.build()
 
 
-@pytest.mark.parametrize("policy", ["kunserve", "recompute"])
+@pytest.mark.parametrize("policy", ["kunserve", "recompute", "swap", "migrate"])
 def test_device_engine_overload_cycle(built, policy):
     from paper_2412_18169_b200.serving import DeviceEngine, device_config
     shape = SHAPES["tiny"]
@@ -45,6 +45,11 @@ def test_device_engine_overload_cycle(built, policy):
         assert k.get("PLAN", 0) >= 1 and k.get("EXCHANGE", 0) >= 1
         assert k.get("RESTORE_DONE", 0) >= 1 and k.get("DISSOLVE", 0) >= 1
         assert res.evictions == 0
+    if policy == "swap":
+        assert k.get("SWAP_OUT", 0) >= 1 and k.get("SWAP_IN", 0) == k.get("SWAP_OUT", 0)
+        assert eng.te.host_kv == {}
+    if policy == "migrate":
+        assert k.get("MIGRATE", 0) + k.get("MIGRATE_NOOP", 0) >= 1
     for iid, inst in eng.instances.items():
         assert inst.table.layers_held() == list(range(shape.num_layers))
         assert inst.kv.allocated_tokens == {} and inst.kv.reserved_bytes == 0
