@@ -223,6 +223,17 @@ int kb_copy_pages_host(kb_pool* pool, const kb_move* move, void* host, int32_t t
  * other flat device-to-device (peer) copy: 16-byte vector kernel. */
 int kb_copy_bytes(uint64_t dst, uint64_t src, int64_t nbytes, uintptr_t stream);
 
+/* ---- N7 across processes: activation hand-off buffers ------------------- */
+/* The receiving stage of a pipeline group (engine.py:428-448) allocates its
+ * activation slots with kb_device_alloc and exports them (CUDA IPC); the
+ * sending stage maps them (kb_ipc_mem_import) and writes each microbatch's
+ * rows with kb_copy_bytes -- stores over NVLink into the peer's HBM. */
+int kb_device_alloc(int32_t device, int64_t nbytes, uint64_t* ptr);
+int kb_device_free(uint64_t ptr);
+int kb_ipc_mem_export(uint64_t ptr, uint8_t* handle /* 64 bytes */);
+int kb_ipc_mem_import(int32_t device, const uint8_t* handle, uint64_t* ptr);
+int kb_ipc_mem_close(uint64_t ptr);
+
 /* ---- N8: paged attention over the pool --------------------------------- */
 /* Write the new tokens' K/V into their pages.  k, v: [ntok][n_kv_heads][head_dim]
  * bf16; token t belongs to slot slots[t] at position pos[t]; its page must

@@ -15,6 +15,8 @@
 // with cuMemSetAccess for all peers, so a plain ld.global/st.global on the
 // peer VA travels over NVLink.  All kernels move 16-byte vectors with 8
 // loads in flight per thread and a grid of 148 x k blocks.
+#include <cstring>
+
 #include "kb_common.cuh"
 
 namespace kb {
@@ -288,4 +290,50 @@ extern "C" int kb_copy_pages_host(kb_pool* p, const kb_move* mv, void* host, int
       pv, static_cast<uint8_t*>(dhost), *mv, total, p->m.page_bytes, pieces, to_host);
   KB_LAUNCH_CHECK();
   return pool_leave(p, st);
+}
+
+// ------------------------------------------------ cross-process activation buffers
+// The stage s -> s+1 hand-off of a pipeline group whose members live in
+// different processes (engine.py:428-448): the receiving stage owns a
+// device buffer, the sending stage maps it through CUDA IPC and writes the
+// activation rows into it with the copy kernel above (NVLink stores).
+
+extern "C" int kb_device_alloc(int32_t device, int64_t nbytes, uint64_t* ptr) {
+  if (!ptr || nbytes <= 0) return fail(KB_EINVAL, "bad allocation request");
+  KB_RT(cudaSetDevice(device));
+  void* p = nullptr;
+  KB_RT(cudaMalloc(&p, (size_t)nbytes));
+  *ptr = reinterpret_cast<uint64_t>(p);
+  return KB_OK;
+}
+
+extern "C" int kb_device_free(uint64_t ptr) {
+  if (ptr) KB_RT(cudaFree(reinterpret_cast<void*>(ptr)));
+  return KB_OK;
+}
+
+extern "C" int kb_ipc_mem_export(uint64_t ptr, uint8_t* handle) {
+  if (!ptr || !handle) return fail(KB_EINVAL, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) <= 64, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  KB_RT(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(ptr)));
+  std::memset(handle, 0, 64);
+  std::memcpy(handle, &h, sizeof(h));
+  return KB_OK;
+}
+
+extern "C" int kb_ipc_mem_import(int32_t device, const uint8_t* handle, uint64_t* ptr) {
+  if (!handle || !ptr) return fail(KB_EINVAL, "null argument");
+  KB_RT(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  KB_RT(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *ptr = reinterpret_cast<uint64_t>(p);
+  return KB_OK;
+}
+
+extern "C" int kb_ipc_mem_close(uint64_t ptr) {
+  if (ptr) KB_RT(cudaIpcCloseMemHandle(reinterpret_cast<void*>(ptr)));
+  return KB_OK;
 }

@@ -173,3 +173,129 @@ def share_pools(rt, local_pools: dict, model, shape, key: str = "pools") -> dict
             for fd in fds:
                 os.close(fd)
     return views
+
+
+# ------------------------------------------------------ activation hand-off
+
+class ActChannel:
+    """Stage s -> s+1 activation hand-off between two ranks of a pipeline
+    group (engine.py:428-448: the ACTIVATION task of every microbatch).
+
+    The receiver owns `slots` device buffers (CUDA IPC-exported); the sender
+    maps them and writes each microbatch's rows with the repo's copy kernel
+    (runtime.copy_bytes: 16-byte stores into the peer's HBM over NVLink).
+    Ordering never blocks a GPU: the sender records an interprocess CUDA
+    event after the copy and publishes the microbatch number in a shared
+    host counter; the receiver's stream waits on that event once the
+    counter shows the record happened.  The receiver acknowledges a slot the
+    same way (its event after the consuming stage), so the sender reuses a
+    slot only after the receiver is done with it.  Both sides poll the host
+    counters with a timeout instead of ever spinning on the device.
+    """
+
+    def __init__(self, rt, sender: int, receiver: int, slot_bytes: int, slots: int = 2,
+                 key: str = "act", timeout_s: float = 120.0):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        from multiprocessing import shared_memory
+        from .runtime import IpcBuffer
+        self.torch = torch
+        self.rank = dist.get_rank()
+        self.sender, self.receiver = sender, receiver
+        self.is_sender = self.rank == sender
+        assert self.rank in (sender, receiver)
+        self.slot_bytes = (slot_bytes + 255) // 256 * 256
+        self.slots = slots
+        self.timeout_s = timeout_s
+        self.device = rt.device
+        name = f"kbact_{os.environ.get('MASTER_PORT', '0')}_{key}_{sender}_{receiver}"
+        # the receiver creates the buffer, the counters and its ack event
+        info = None
+        if not self.is_sender:
+            self.buf = IpcBuffer.allocate(rt.device, self.slot_bytes * slots)
+            self.shm = shared_memory.SharedMemory(name=name, create=True, size=64)
+            self.recv_ev = torch.cuda.Event(interprocess=True)
+            info = (self.buf.export(), self.recv_ev.ipc_handle())
+        objs = [None] * dist.get_world_size()
+        dist.all_gather_object(objs, (self.rank, info))
+        theirs = dict(objs)
+        if self.is_sender:
+            mem_h, ev_h = theirs[receiver]
+            self.buf = IpcBuffer.open(rt.device, mem_h, self.slot_bytes * slots)
+            self.shm = shared_memory.SharedMemory(name=name)
+            self.recv_ev = torch.cuda.Event.from_ipc_handle(self.device, ev_h)
+            self.send_ev = torch.cuda.Event(interprocess=True)
+            h = self.send_ev.ipc_handle()
+        else:
+            h = None
+        dist.all_gather_object(objs, (self.rank, h))
+        if not self.is_sender:
+            self.send_ev = torch.cuda.Event.from_ipc_handle(self.device, dict(objs)[sender])
+        self.ctr = np.ndarray((2,), dtype=np.int64, buffer=self.shm.buf)  # [sent, acked]
+        if not self.is_sender:
+            self.ctr[:] = -1
+        dist.barrier()
+        self.n = 0
+
+    def _poll(self, idx: int, want: int) -> None:
+        import time
+        t0 = time.perf_counter()
+        while self.ctr[idx] < want:
+            if time.perf_counter() - t0 > self.timeout_s:
+                raise TimeoutError(f"activation channel {self.sender}->{self.receiver}: "
+                                   f"waited {self.timeout_s}s for counter {idx} >= {want}")
+            time.sleep(0)
+
+    def slot(self, n: int):
+        off = (n % self.slots) * self.slot_bytes
+        return self.buf.tensor()[off:off + self.slot_bytes]
+
+    def send(self, x, stream=None) -> int:
+        """Hand x (contiguous device tensor) to the receiver as microbatch
+        n = the n-th send; returns n."""
+        from .runtime import copy_bytes
+        torch = self.torch
+        st = stream or torch.cuda.current_stream()
+        n = self.n
+        nbytes = x.numel() * x.element_size()
+        if nbytes > self.slot_bytes:
+            raise ValueError(f"{nbytes} activation bytes exceed the {self.slot_bytes}-byte slot")
+        if n >= self.slots:  # the receiver is done with this slot's previous use
+            self._poll(1, n - self.slots)
+            st.wait_event(self.recv_ev)
+        copy_bytes(self.buf.ptr + (n % self.slots) * self.slot_bytes, x.data_ptr(), nbytes,
+                   stream=st)
+        self.send_ev.record(st)
+        self.ctr[0] = n
+        self.n += 1
+        return n
+
+    def recv(self, nbytes: int, stream=None):
+        """uint8 view of the next microbatch's rows; call done() after the
+        stage consumed it."""
+        torch = self.torch
+        st = stream or torch.cuda.current_stream()
+        n = self.n
+        self._poll(0, n)
+        st.wait_event(self.send_ev)
+        return self.slot(n)[:nbytes]
+
+    def done(self, stream=None) -> None:
+        torch = self.torch
+        st = stream or torch.cuda.current_stream()
+        self.recv_ev.record(st)
+        self.ctr[1] = self.n
+        self.n += 1
+
+    def close(self) -> None:
+        import torch.distributed as dist
+        self.torch.cuda.synchronize(self.device)
+        dist.barrier()
+        self.buf.close()
+        self.shm.close()
+        if not self.is_sender:
+            dist.barrier()
+            self.shm.unlink()
+        else:
+            dist.barrier()

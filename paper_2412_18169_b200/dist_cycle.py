@@ -116,6 +116,8 @@ class DistCycle:
                                  key=f"{key}-{self._job_key()}")
         self.pools = {self.me: self.pool, **self.views}
         self.te = TransferEngine(self.pools, self.slots, timing=True)
+        self.rt = rt
+        self.on_merged = None  # callback(live groups, instance -> group) in the merged state
         self._sync_views()
 
     @staticmethod
@@ -260,6 +262,8 @@ class DistCycle:
                     assert self.instances[iid].kv.alloc(rid, share)
         ev["exch"].record(st)
         x_end = tid
+        if self.on_merged is not None:  # untimed: runs between the exch and drain events
+            self.on_merged(live, final)
         # ---- drain (untimed): the transient residents finish
         gone = []
         for rid in sorted(self.transient):
@@ -361,6 +365,77 @@ class DistCycle:
         self.refill()
         return rep
 
+    # --------------------------------------------------- pipelined group decode
+    def pipeline_decode(self, final: dict, iters: int = 3, microbatches: int = 2) -> dict:
+        """One decode token for every resident of this rank's merged PP-2
+        group, executed as a real pipeline across the two ranks: the stage-0
+        rank runs its layers (cuBLAS GEMMs + this repo's kv_append and
+        tcgen05 paged decode over its pool) per microbatch and hands the
+        activation rows to the stage-1 rank through an ActChannel (the
+        copy kernel storing into the peer's HBM), which runs the remaining
+        layers.  Returns timing (CUDA events, max over ranks is the caller's)
+        and the transport checksums."""
+        import torch
+        from .dist import ActChannel
+        from .serving import StageRunner
+        g = final[self.me]
+        members = list(g.member_instances)
+        if len(members) != 2:
+            raise ValueError("pipeline_decode expects PP-2 groups")
+        stage = members.index(self.me)
+        lo, hi = g.stage_layer_map[self.me]
+        res = sorted(r for r in self.tokens if self.home[r] in members)
+        mbs = [res[k::microbatches] for k in range(microbatches)]
+        H = self.shape.hidden
+        dev = f"cuda:{self.device}"
+        runner = StageRunner(self.pool, self.shape, max_seqs=max(len(m) for m in mbs))
+        chan = ActChannel(self.rt, members[0], members[1],
+                          slot_bytes=max(len(m) for m in mbs) * H * 2, slots=2,
+                          key=f"pipe{g.gid}")
+
+        def batch(mb):
+            i32 = lambda v: torch.tensor(v, dtype=torch.int32, device=dev)  # noqa: E731
+            sl = [self.slots[self.me].of[r] for r in mb]
+            ctx = [self.tokens[r] for r in mb]
+            return {"n": len(mb), "slots": i32(sl), "pos": i32([c - 1 for c in ctx]),
+                    "np": 0, "nd": len(mb),
+                    "d_rows": torch.arange(len(mb), dtype=torch.int64, device=dev),
+                    "d_slots": i32(sl), "d_ctx": i32(ctx), "d_max": max(ctx)}
+        batches = [batch(mb) for mb in mbs]
+        gen = torch.Generator(device=dev).manual_seed(99)
+        inputs = [(torch.randn((len(mb), H), device=dev, generator=gen) * 0.5).to(torch.bfloat16)
+                  for mb in mbs]
+        sums = []
+
+        def one_pass(record):
+            for k, b in enumerate(batches):
+                if stage == 0:
+                    x = runner.run(lo, hi, inputs[k], b)
+                    chan.send(x.contiguous())
+                    if record:
+                        sums.append(x.view(torch.int16).to(torch.int64).sum())
+                else:
+                    raw = chan.recv(b["n"] * H * 2)
+                    x = raw.view(torch.bfloat16).view(b["n"], H).clone()
+                    chan.done()
+                    if record:
+                        sums.append(x.view(torch.int16).to(torch.int64).sum())
+                    runner.run(lo, hi, x, b)
+        one_pass(True)  # warm-up (cuBLAS handles, lazy attributes) + checksums
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier()
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            one_pass(False)
+        e.record()
+        e.synchronize()
+        ms = a.elapsed_time(e) / iters
+        chan.close()
+        return {"ms_per_token_step": ms, "tokens_per_step": len(res), "stage": stage,
+                "handoff_bytes_per_step": len(res) * H * 2,
+                "checksums": [int(x.item()) for x in sums], "group": g.gid}
+
     def refill(self) -> None:
         torch = self.torch
         for rid in sorted(self.transient):
@@ -388,7 +463,8 @@ class DistCycle:
         self.pool.close()
 
 
-def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, **kw) -> dict:
+def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, pipeline: bool = False,
+        **kw) -> dict:
     """Warm-up + timed steps; whole-job numbers (sum of bytes over ranks,
     max of step time over ranks) and the parity verdict."""
     import torch.distributed as dist
@@ -403,6 +479,27 @@ def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, **kw) -> dict:
     w_ok = cyc.weight_checksums() == w0
     k1 = cyc.kv_checksums()
     kv_ok = set(k0) == set(k1) and all(bool((k0[r] == k1[r]).all()) for r in k0)
+    pipe = None
+    if pipeline:
+        # after the parity checks (the decode appends K/V): one more cycle,
+        # pipelined group decode in its merged state
+        got = {}
+        cyc.on_merged = lambda live, final: got.update(cyc.pipeline_decode(final))
+        cyc.step()
+        cyc.on_merged = None
+        objs = [None] * dist.get_world_size()
+        dist.all_gather_object(objs, got)
+        by_group: dict = {}
+        for o in objs:
+            by_group.setdefault(o["group"], {})[o["stage"]] = o
+        ok = all(len(v) == 2 and v[0]["checksums"] == v[1]["checksums"]
+                 for v in by_group.values())
+        ms_max = max(o["ms_per_token_step"] for o in objs)
+        toks = sum(v[0]["tokens_per_step"] for v in by_group.values())
+        pipe = {"tokens_per_s": toks / (ms_max / 1e3), "ms_per_token_step": ms_max,
+                "handoff_bytes_per_step": sum(v[0]["handoff_bytes_per_step"]
+                                              for v in by_group.values()),
+                "groups": len(by_group), "handoff_bit_exact": ok}
     out = {
         "ms_total_max": max_over_ranks(ms, device=dev),
         "bytes_total": sum_over_ranks(sum(r.bytes_pulled + r.bytes_compaction for r in reps),
@@ -416,6 +513,7 @@ def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, **kw) -> dict:
         "residents_local": len(k0),
         "peers_on_same_gpu": any(v.owner_device == rt.device for v in cyc.views.values()),
         "last": reps[-1],
+        "pipeline": pipe,
     }
     cyc.close()
     return out

@@ -103,6 +103,11 @@ _sigs = {
                                           C.c_int64, _S]),
     "kb_copy_bytes": (C.c_int, [_U, _U, C.c_int64, _S]),
     "kb_copy_pages_host": (C.c_int, [_P, C.POINTER(Move), _P, C.c_int32, _S]),
+    "kb_device_alloc": (C.c_int, [C.c_int32, C.c_int64, C.POINTER(C.c_uint64)]),
+    "kb_device_free": (C.c_int, [_U]),
+    "kb_ipc_mem_export": (C.c_int, [_U, C.POINTER(C.c_uint8)]),
+    "kb_ipc_mem_import": (C.c_int, [C.c_int32, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64)]),
+    "kb_ipc_mem_close": (C.c_int, [_U]),
     "kb_kv_append": (C.c_int, [_P, C.c_int32, _U, _U, _U, _U, C.c_int32, _S]),
     "kb_decode_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "kb_paged_decode": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, C.c_int32, C.c_int32,
@@ -446,6 +451,40 @@ def copy_pages_host(pool: DevicePool, slot: int, layer_lo: int, layer_hi: int, n
     mv = Move(slot, slot, layer_lo, layer_hi, npages, flat_lo, flat_hi, 0)
     _check(_lib.kb_copy_pages_host(pool.h, C.byref(mv), C.c_void_p(host.data_ptr()),
                                    1 if to_host else 0, _stream(stream)), launches=1)
+
+
+class IpcBuffer:
+    """A device buffer shared across processes (CUDA IPC): the owner
+    allocates and exports it, a peer imports it into its own VA."""
+
+    def __init__(self, ptr: int, nbytes: int, owned: bool):
+        self.ptr, self.nbytes, self.owned = ptr, nbytes, owned
+
+    @classmethod
+    def allocate(cls, device: int, nbytes: int) -> "IpcBuffer":
+        p = C.c_uint64()
+        _check(_lib.kb_device_alloc(device, nbytes, C.byref(p)))
+        return cls(p.value, nbytes, True)
+
+    def export(self) -> bytes:
+        h = (C.c_uint8 * 64)()
+        _check(_lib.kb_ipc_mem_export(self.ptr, h))
+        return bytes(h)
+
+    @classmethod
+    def open(cls, device: int, handle: bytes, nbytes: int) -> "IpcBuffer":
+        h = (C.c_uint8 * 64)(*handle)
+        p = C.c_uint64()
+        _check(_lib.kb_ipc_mem_import(device, h, C.byref(p)))
+        return cls(p.value, nbytes, False)
+
+    def tensor(self):
+        return device_bytes(self.ptr, self.nbytes)
+
+    def close(self) -> None:
+        if self.ptr:
+            _check(_lib.kb_device_free(self.ptr) if self.owned else _lib.kb_ipc_mem_close(self.ptr))
+            self.ptr = 0
 
 
 def copy_bytes(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:

@@ -137,12 +137,12 @@ def _cycle_worker(rank, world, port, q, shape_name, kv_budget, chunk, input_mean
         rt = runtime.Runtime(0, max_slots=512, max_pages_per_seq=1024)
         out = dist_cycle.run(rt, SHAPES[shape_name], kv_budget, steps=2, warmup=1,
                              kv_chunk_bytes=chunk, param_chunk_bytes=chunk,
-                             input_mean=input_mean, key=f"ct{port}")
+                             input_mean=input_mean, key=f"ct{port}", pipeline=True)
         last = out["last"]
         q.put((rank, {"parity_fail": out["parity_fail"], "residents": out["residents_local"],
                       "kv": last.bytes_kv_exchange, "param": last.bytes_param,
                       "cons": last.bytes_kv_consolidate, "peer": last.bytes_pulled_peer,
-                      "pulled": last.bytes_pulled}))
+                      "pulled": last.bytes_pulled, "pipe": out["pipeline"]}))
     finally:
         dist.destroy_process_group()
 
@@ -166,3 +166,8 @@ def test_two_rank_cycle_bit_exact(shape_name, kv_budget, chunk, input_mean):
         assert d["peer"] == d["pulled"]   # every pull reads the other rank's pool
     # the two halves of the group move mirror-image byte counts
     assert res[0]["param"] == res[1]["param"]
+    # pipelined decode of the merged group across the ranks: every
+    # activation hand-off arrives bit for bit
+    pipe = res[0]["pipe"]
+    assert pipe["groups"] == 1 and pipe["handoff_bit_exact"]
+    assert pipe["tokens_per_s"] > 0 and pipe["handoff_bytes_per_step"] > 0
