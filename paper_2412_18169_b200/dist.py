@@ -224,6 +224,11 @@ class ActChannel:
             mem_h, ev_h = theirs[receiver]
             self.buf = IpcBuffer.open(rt.device, mem_h, self.slot_bytes * slots)
             self.shm = shared_memory.SharedMemory(name=name)
+            try:  # the receiver owns (and unlinks) the segment
+                from multiprocessing import resource_tracker
+                resource_tracker.unregister(self.shm._name, "shared_memory")
+            except Exception:
+                pass
             self.recv_ev = torch.cuda.Event.from_ipc_handle(self.device, ev_h)
             self.send_ev = torch.cuda.Event(interprocess=True)
             h = self.send_ev.ipc_handle()
