@@ -46,8 +46,12 @@ constexpr float kRescaleLog2 = 8.0f;               // lazy-rescale threshold
 #ifndef KB_PF_REGS_SOFTMAX
 #define KB_PF_REGS_SOFTMAX 216
 #endif
-// per SMSP: 2 softmax warps x 216 + 1 warpgroup-2 warp x 64 = 496 regs/lane
-// (the full 512 deadlocks the setmaxnreg.inc on B200)
+// per SMSP: 2 softmax warps x 216 + 1 warpgroup-2 warp x 64 = 496 regs/lane.
+// setmaxnreg.inc draws from the CTA's launch allocation (3 warps x 168 = 504
+// per SMSP), so 2 x 224 + 64 = 512 never gets its registers and hangs.
+// (A 640-thread variant -- two softmax warpgroups per Q tile splitting the
+// columns -- measured 57-58% against this version's 61%: its pool of
+// 5 x 96 per SMSP caps the softmax at 104 registers.)
 constexpr int kPfRegsSoftmax = KB_PF_REGS_SOFTMAX;
 constexpr int kPfRegsProducer = 64;
 
