@@ -118,6 +118,7 @@ class OverloadCycle:
                                    device=kv.device, generator=g))
         self._fill_weights()
         torch.cuda.synchronize()
+        self.exchange_batch = 8    # residents in the first plan_exchange / submission batch
         self.pause_merged = False  # set True to stop after the exchange (see resume())
         self.auto_refill = True    # False: the caller runs refill() between steps
         self._paused = None
@@ -247,13 +248,22 @@ class OverloadCycle:
                     cohorts.setdefault(tuple(sorted(orig_map[rid].items())), []).append(rid)
             for key in sorted(cohorts):
                 old_map = dict(key)
-                toks = {rid: self.tokens[rid] for rid in cohorts[key]}
-                tasks = plan_exchange(toks, old_map, g.stage_layer_map, L, kvbpt, self.kv_chunk,
-                                      tid_start=tid)
-                tid += len(tasks)
-                self.te.register_exchange(tasks, old_map, g.stage_layer_map, toks)
-                self.te.submit_many(tasks)
-                rep.n_tasks += len(tasks)
+                # planned and submitted in batches of residents: the first
+                # copies start while the host plans the rest (the flows, and
+                # so the bytes, are those of one plan_exchange over the cohort;
+                # only the round-robin order differs)
+                rids = cohorts[key]
+                b0, size = 0, self.exchange_batch
+                while b0 < len(rids):
+                    toks = {rid: self.tokens[rid] for rid in rids[b0:b0 + size]}
+                    b0 += size
+                    size *= 2  # first copies early, then fewer, larger batches
+                    tasks = plan_exchange(toks, old_map, g.stage_layer_map, L, kvbpt,
+                                          self.kv_chunk, tid_start=tid)
+                    tid += len(tasks)
+                    self.te.register_exchange(tasks, old_map, g.stage_layer_map, toks)
+                    self.te.submit_many(tasks)
+                    rep.n_tasks += len(tasks)
         # no host wait: source releases queue behind the copies
         self.te.finish_flow_sources(ordered=True)
         # re-share (engine.py:823-830): token accounting per member stage
