@@ -334,9 +334,14 @@ class OverloadCycle:
                     memory.restore_layers(self.instances[iid], rng, -1, tid=0, stream=st)
                     rep.remap_ns += self.pools[iid].last_remap_ns
                     restored.append(iid)
-            flat = {iid: rng for iid, rngs in missing.items() for rng in rngs}
-            tasks = plan_restore_transfers(flat, holders, self.model.bytes_per_layer,
-                                           self.param_chunk, tid_start=tid)
+            # one plan per range index: a member of a PP-4 group can miss two
+            # disjoint ranges, and plan_restore_transfers takes one range per
+            # target (the reference's engine.py:1127 keeps only the last one)
+            tasks = []
+            for k in range(max(len(r) for r in missing.values()) if missing else 0):
+                flat = {iid: rngs[k] for iid, rngs in missing.items() if len(rngs) > k}
+                tasks += plan_restore_transfers(flat, holders, self.model.bytes_per_layer,
+                                                self.param_chunk, tid_start=tid + len(tasks))
             tid += len(tasks)
             self.te.register_restore(tasks, self.model.bytes_per_layer)
             self.te.submit_many(tasks)  # one pull launch per contiguous run

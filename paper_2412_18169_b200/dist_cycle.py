@@ -54,7 +54,7 @@ class DistCycle:
     def __init__(self, rt, shape: ModelShape, kv_budget_bytes: int, fill: float = 0.9,
                  seed: int = 3, kv_chunk_bytes: int = 64 << 20,
                  param_chunk_bytes: int = 256 << 20, input_mean: int = 1660,
-                 key: str = "cycle"):
+                 key: str = "cycle", pp: int = 2):
         import torch
         import torch.distributed as dist
         self.torch = torch
@@ -64,6 +64,9 @@ class DistCycle:
         self.shape = shape
         self.model = shape.spec()
         self.L = self.model.num_layers
+        if pp not in (2, 4) or dist.get_world_size() % pp:
+            raise ValueError(f"pp must be 2 or 4 and divide the world size, got {pp}")
+        self.pp = pp
         self.kv_chunk = kv_chunk_bytes
         self.param_chunk = param_chunk_bytes
         self.device = rt.device
@@ -117,6 +120,11 @@ class DistCycle:
         self.pools = {self.me: self.pool, **self.views}
         self.te = TransferEngine(self.pools, self.slots, timing=True)
         self.rt = rt
+        self.head_pages = self.pool.info().extent_pages  # slab l's alias starts here
+        # tests: overwrite dropped slabs, so a restore that skipped a layer
+        # cannot pass the weight checksums by leaving the old bytes in place
+        self.poison_drops = False
+        self.last_groups: dict = {}
         self.on_merged = None  # callback(live groups, instance -> group) in the merged state
         self._sync_views()
 
@@ -126,6 +134,13 @@ class DistCycle:
         return os.environ.get("MASTER_PORT", "0")
 
     # ---------------------------------------------------------------- helpers
+    def _poison(self, lo: int, hi: int) -> None:
+        sp = self.model.bytes_per_layer // self.shape.page_bytes
+        a = (self.head_pages + lo * sp) * self.shape.page_bytes
+        b = (self.head_pages + hi * sp) * self.shape.page_bytes
+        with self.torch.cuda.stream(self.te.bulk):  # ordered before the exchange grows / copies
+            self.pool.kv_bytes()[a:b].fill_(0x7F)
+
     def _admit(self, rid: int) -> None:
         iid = self.home[rid]
         inst = self.instances[iid]
@@ -208,12 +223,14 @@ class DistCycle:
         self.dist.barrier()
         ev["t0"].record(st)
         # ---- plan: every replica's queued burst outgrows its free KV by just
-        # under half a parameter copy, so plan_drop merges every pair
+        # under (pp-1)/pp of a parameter copy, so plan_drop merges the
+        # replicas into PP-pp groups (configs[2]: PP-2; configs[3]: PP-4)
         groups = [Group(i, [i], {i: (0, L)}) for i in sorted(self.instances)]
         demand = 0
+        excess = self.model.param_bytes * (self.pp - 1) // self.pp - kvbpt
         for i, inst in sorted(self.instances.items()):
             free = inst.kv.free_tokens * kvbpt
-            pending = (free + self.model.param_bytes // 2 - kvbpt) // kvbpt
+            pending = (free + excess) // kvbpt
             demand += compute_demand(pending, free, kvbpt)
         plan = plan_drop(groups, demand, self.model)
         assert plan.merges and not plan.fallback, plan.to_text()
@@ -230,8 +247,11 @@ class DistCycle:
                 assert not fetches
                 for lo, hi in drops:
                     memory.drop_layers(self.instances[iid], (lo, hi), new)
+                    if self.poison_drops and iid == self.me:
+                        self._poison(lo, hi)
             live[m.gid] = new
         final = {iid: g for g in live.values() for iid in g.member_instances}
+        self.last_groups = dict(live)
         # ---- exchange (engine.py:690-726): pulls into this rank's pool
         tid = 0
         all_tasks = []
@@ -276,7 +296,6 @@ class DistCycle:
         self._sync_views()
         ev["drain"].record(st)
         # ---- restore (engine.py:1093-1157): compaction here, pulls from holders
-        restored = False
         for g in sorted(live.values(), key=lambda g: g.gid):
             missing, holders = {}, {}
             for iid in g.member_instances:
@@ -287,10 +306,16 @@ class DistCycle:
             for iid in sorted(missing):
                 for rng in missing[iid]:
                     memory.restore_layers(self.instances[iid], rng, -1, tid=0, stream=st)
-                    restored |= iid == self.me
-            flat = {iid: rng for iid, rngs in missing.items() for rng in rngs}
-            tasks = plan_restore_transfers(flat, holders, self.model.bytes_per_layer,
-                                           self.param_chunk, tid_start=tid)
+                    if iid == self.me:  # each compaction's size (waits for it)
+                        rep.bytes_compaction += self.pool.last_moved_pages * self.shape.page_bytes
+            # one plan per range index: a member of a PP-4 group can miss two
+            # disjoint ranges, and plan_restore_transfers takes one range per
+            # target (the reference's engine.py:1127 keeps only the last one)
+            tasks = []
+            for k in range(max(len(r) for r in missing.values()) if missing else 0):
+                flat = {iid: rngs[k] for iid, rngs in missing.items() if len(rngs) > k}
+                tasks += plan_restore_transfers(flat, holders, self.model.bytes_per_layer,
+                                                self.param_chunk, tid_start=tid + len(tasks))
             assert all(t.src != HOST for t in tasks)
             tid += len(tasks)
             self.te.register_restore(tasks, self.model.bytes_per_layer)
@@ -353,8 +378,6 @@ class DistCycle:
                 rep.bytes_pulled_peer += p.bytes_moved
         rep.kv_kernel_ms = _span_ms([p for p in done if p.task.kind is TaskKind.KVCACHE_CHUNK])
         rep.param_kernel_ms = _span_ms([p for p in done if p.task.kind is TaskKind.PARAM_SHARD])
-        if restored:
-            rep.bytes_compaction = self.pool.last_moved_pages * self.shape.page_bytes
         ev["cons"].synchronize()
         parts = {"exchange": ev["t0"].elapsed_time(ev["exch"]),
                  "restore": ev["drain"].elapsed_time(ev["restore"]),
@@ -465,10 +488,14 @@ class DistCycle:
 
 def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, pipeline: bool = False,
         **kw) -> dict:
+    """pipeline: also time the merged PP-2 groups decoding as cross-rank
+    pipelines (pp=2 only)."""
     """Warm-up + timed steps; whole-job numbers (sum of bytes over ranks,
     max of step time over ranks) and the parity verdict."""
     import torch.distributed as dist
+    poison = kw.pop("poison_drops", False)
     cyc = DistCycle(rt, shape, kv_budget_bytes, **kw)
+    cyc.poison_drops = poison
     dev = f"cuda:{rt.device}" if dist.get_backend() == "nccl" else None
     w0 = cyc.weight_checksums()
     k0 = cyc.kv_checksums()
@@ -480,7 +507,7 @@ def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, pipeline: bool
     k1 = cyc.kv_checksums()
     kv_ok = set(k0) == set(k1) and all(bool((k0[r] == k1[r]).all()) for r in k0)
     pipe = None
-    if pipeline:
+    if pipeline and cyc.pp == 2:
         # after the parity checks (the decode appends K/V): one more cycle,
         # pipelined group decode in its merged state
         got = {}
@@ -512,6 +539,7 @@ def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, pipeline: bool
                                       device=dev),
         "residents_local": len(k0),
         "peers_on_same_gpu": any(v.owner_device == rt.device for v in cyc.views.values()),
+        "group_sizes": sorted(len(g.member_instances) for g in cyc.last_groups.values()),
         "last": reps[-1],
         "pipeline": pipe,
     }

@@ -373,7 +373,7 @@ class Engine:
     def _on_exchange_planned(self, tasks, old_map, new_map, tokens) -> None:
         pass
 
-    def _on_params_planned(self, tasks, fetch: bool) -> None:
+    def _on_params_planned(self, tasks, fetch: bool, **restore) -> None:
         pass
 
     def _on_consolidation_planned(self, rid: int, peer: int, home: int, layers, tasks) -> None:
@@ -988,7 +988,7 @@ class Engine:
         tasks = plan_restore_transfers(flat, holders, self.model.bytes_per_layer, chunk,
                                        tid_start=self._tid + 1)
         self._tid += len(tasks)
-        self._on_params_planned(tasks, fetch=False)
+        self._on_params_planned(tasks, fetch=False, missing=missing, holders=holders, chunk=chunk)
         left: dict[int, int] = {}
         for t in tasks:
             left[t.dst] = left.get(t.dst, 0) + 1

@@ -214,6 +214,7 @@ class DeviceEngine(Engine):
             self.emb[d] = torch.randn((self.shape.vocab, self.shape.hidden), device=f"cuda:{d}",
                                       generator=g).to(torch.bfloat16)
         self.acts: dict = {}
+        self._extra_tid = 1 << 40  # device-only pulls, outside the engine's tid space
         self.stage_samples: list = []   # (tokens, prefill_units, decode_tokens, layers, us)
         self.fetch_left: dict = {}
         torch.cuda.synchronize()
@@ -288,8 +289,11 @@ class DeviceEngine(Engine):
     def _on_exchange_planned(self, tasks, old_map, new_map, tokens) -> None:
         self.te.register_exchange(tasks, old_map, new_map, tokens)
 
-    def _on_params_planned(self, tasks, fetch: bool) -> None:
+    def _on_params_planned(self, tasks, fetch: bool, **restore) -> None:
         self.te.register_restore(tasks, self.model.bytes_per_layer)
+        missing = restore.get("missing")
+        if missing:
+            self._pull_uncovered(missing, restore["holders"], restore["chunk"])
         if fetch:  # merge-time fetch: vacate the destination slab first
             for t in tasks:
                 key = (t.dst, t.layers)
@@ -297,6 +301,27 @@ class DeviceEngine(Engine):
                     self.pools[t.dst].restore_begin(*t.layers, stream=self.te.bulk)
                     self.fetch_left[key] = 0
                 self.fetch_left[key] += 1
+
+    def _pull_uncovered(self, missing: dict, holders: dict, chunk: int) -> None:
+        """The reference plans one range per restoring member
+        (engine.py:1127: {iid: rng for ... for rng in rngs} keeps the last),
+        so a member that misses two disjoint ranges (the middle members of a
+        PP-4 group) would complete_restore layers nobody pulled.  In
+        simulation that is invisible; on the device those slabs may hold KV
+        pages by now.  The event log keeps the reference's tasks; the other
+        ranges are pulled here, on the same stream, ahead of them -- they
+        land before the reference's last restore chunk completes."""
+        from .exchange import plan_restore_transfers
+        extra = []
+        for k in range(max(len(r) for r in missing.values())):
+            flat = {iid: rngs[k] for iid, rngs in missing.items() if len(rngs) > k + 1}
+            if flat:
+                extra += plan_restore_transfers(flat, holders, self.model.bytes_per_layer, chunk,
+                                                tid_start=self._extra_tid + len(extra))
+        if extra:
+            self._extra_tid += len(extra)
+            self.te.register_restore(extra, self.model.bytes_per_layer)
+            self.te.submit_many(extra)
 
     def _fetch_done(self, gid, task, when) -> None:
         self.te.drain()

@@ -15,6 +15,9 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
+SHAPES_L = {"llama3_8b": 32, "qwen25_14b": 48}
+SLAB = {"llama3_8b": 438_304_768, "qwen25_14b": 551_550_976}
+
 
 def _free_port() -> int:
     with socket.socket() as s:
@@ -127,7 +130,7 @@ def test_peer_view_pulls_pages_and_slabs_bit_exact():
     assert res[0] == (True, True, True) and res[1] == (True, True, True)
 
 
-def _cycle_worker(rank, world, port, q, shape_name, kv_budget, chunk, input_mean):
+def _cycle_worker(rank, world, port, q, shape_name, kv_budget, chunk, input_mean, pp=2):
     import torch.distributed as dist
 
     from paper_2412_18169_b200 import dist_cycle, runtime
@@ -137,12 +140,14 @@ def _cycle_worker(rank, world, port, q, shape_name, kv_budget, chunk, input_mean
         rt = runtime.Runtime(0, max_slots=512, max_pages_per_seq=1024)
         out = dist_cycle.run(rt, SHAPES[shape_name], kv_budget, steps=2, warmup=1,
                              kv_chunk_bytes=chunk, param_chunk_bytes=chunk,
-                             input_mean=input_mean, key=f"ct{port}", pipeline=True)
+                             input_mean=input_mean, key=f"ct{port}", pipeline=True, pp=pp,
+                             poison_drops=True)
         last = out["last"]
         q.put((rank, {"parity_fail": out["parity_fail"], "residents": out["residents_local"],
                       "kv": last.bytes_kv_exchange, "param": last.bytes_param,
                       "cons": last.bytes_kv_consolidate, "peer": last.bytes_pulled_peer,
-                      "pulled": last.bytes_pulled, "pipe": out["pipeline"]}))
+                      "pulled": last.bytes_pulled, "pipe": out["pipeline"],
+                      "groups": out["group_sizes"]}))
     finally:
         dist.destroy_process_group()
 
@@ -171,3 +176,26 @@ def test_two_rank_cycle_bit_exact(shape_name, kv_budget, chunk, input_mean):
     pipe = res[0]["pipe"]
     assert pipe["groups"] == 1 and pipe["handoff_bit_exact"]
     assert pipe["tokens_per_s"] > 0 and pipe["handoff_bytes_per_step"] > 0
+
+
+@pytest.mark.parametrize("shape_name,kv_budget,chunk,input_mean", [
+    ("llama3_8b", 1 << 30, 16 << 20, 1660),
+    ("qwen25_14b", 2 << 30, 64 << 20, 1660),
+])
+def test_four_rank_pp4_cycle_bit_exact(shape_name, kv_budget, chunk, input_mean):
+    """configs[3] in miniature (Qwen2.5-14B shape): four replicas on four
+    ranks merge into one PP-4 group (three merges, 12 layers per member for
+    Qwen); the exchange fans every resident's KV out to three peers,
+    restore pulls 36 layers from three holders, consolidation fans back in
+    -- all through peer views, bit for bit."""
+    res = _spawn(_cycle_worker, 4, shape_name, kv_budget, chunk, input_mean, 4)
+    for r in range(4):
+        d = res[r]
+        assert d["parity_fail"] == 0 and d["groups"] == [4]
+        assert d["residents"] > 0 and d["kv"] > 0 and d["param"] > 0 and d["cons"] > 0
+        assert d["peer"] == d["pulled"]
+    # every member misses 3/4 of the layers and pulls all of them (a member
+    # in the middle holds one range and misses two disjoint ones)
+    L = SHAPES_L[shape_name]
+    slab = SLAB[shape_name]
+    assert all(res[r]["param"] == (L - L // 4) * slab for r in range(4))
