@@ -296,7 +296,7 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
             "launches_per_step": launches}
 
 
-def nvlink_measure(rt, shape, args) -> dict:
+def nvlink_measure(rt, shape, args, pp: int = 2) -> dict:
     """BASELINE configs[2]/[3]: one replica per GPU (rank r owns instance r),
     plan_drop merges (0,1), (2,3), ... into PP-2 groups spanning two GPUs;
     a step is drop -> KV exchange -> restore -> consolidation where every
@@ -307,15 +307,15 @@ def nvlink_measure(rt, shape, args) -> dict:
     from paper_2412_18169_b200 import dist_cycle
     ws = torch.distributed.get_world_size()
     out = dist_cycle.run(rt, shape, int(args.kv_gib * (1 << 30)), steps=args.steps,
-                         warmup=args.warmup, key="bench", pipeline=True)
+                         warmup=args.warmup, key=f"bench{pp}", pipeline=pp == 2, pp=pp)
     ms = out["ms_total_max"]
     gbs = out["bytes_total"] / (ms / 1e3) / 1e9
     peer_gbs_per_gpu = out["bytes_peer"] / ws / (out["peer_kernel_ms_max"] / 1e3) / 1e9 \
         if out["peer_kernel_ms_max"] else 0.0
     last = out["last"]
     return {"value": round(gbs, 1), "unit": "GB/s", "n_gpus": ws,
-            "workload": f"llama3_8b bf16, {ws} replicas on {ws} GPUs -> {ws // 2} PP-2 groups "
-                        f"spanning GPU pairs; exchange + restore + consolidation over NVLink",
+            "workload": f"{shape.name} bf16, {ws} replicas on {ws} GPUs -> {ws // pp} PP-{pp} "
+                        f"groups spanning GPUs; exchange + restore + consolidation over NVLink",
             "ms_per_step": round(ms / args.steps, 3),
             "peer_bytes_per_step": int(out["bytes_peer"] / args.steps),
             "roofline": ({"bound": "nvlink", "achieved": round(peer_gbs_per_gpu, 1),
@@ -331,8 +331,8 @@ def nvlink_measure(rt, shape, args) -> dict:
             # the merged groups decoding as real cross-GPU pipelines: stage 0
             # on one GPU, stage 1 on its peer, activations handed over by the
             # copy kernel into the peer's IPC-mapped slots (dist.ActChannel)
-            "pipelined_decode": {k: (round(v, 3) if isinstance(v, float) else v)
-                                 for k, v in (out["pipeline"] or {}).items()}}
+            "pipelined_decode": None if out["pipeline"] is None else
+            {k: (round(v, 3) if isinstance(v, float) else v) for k, v in out["pipeline"].items()}}
 
 
 def _traffic(kernel: str):
@@ -475,9 +475,11 @@ def main():
 
     # configs[2] across GPUs: replica r on GPU r, PP-2 groups spanning GPU
     # pairs, every exchange / restore / consolidation byte pulled over NVLink
-    nvl = None
+    nvl = nvl4 = None
     if ws > 1:
         nvl = nvlink_measure(rt, shape, args)
+    if ws >= 4 and ws % 4 == 0:  # configs[3]: Qwen2.5-14B replicas into PP-4 groups
+        nvl4 = nvlink_measure(rt, SHAPES["qwen25_14b"], args, pp=4)
 
     line = None
     if rank == 0:
@@ -527,6 +529,7 @@ def main():
             "copy_sweep": sweep,
             "p99_ttft": ttft,
             "nvlink_cycle": nvl,
+            "nvlink_cycle_pp4": nvl4,
             "parity": parity,
             "e2e": {"value": round(e_moved / e2e_s / 1e9, 1), "unit": "GB/s",
                     "h2d_bytes_per_step": tok.numel() * 4, "d2h_bytes_per_step": res.numel() * 4},
