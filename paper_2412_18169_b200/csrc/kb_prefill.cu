@@ -223,45 +223,66 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
     }
   } else if (warp == 9) {
     // ------------------------------------------------ MMA issuer
+    // warp-uniform TMEM base: with the shuffle the compiler keeps the MMA
+    // operands in uniform registers (no per-MMA ELECT / R2UR.BROADCAST loop)
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     constexpr uint32_t kIdQK = idesc_bf16_f32(128, 128, false, false);
     constexpr uint32_t kIdPV = idesc_f16_f32(128, 128, false, true);  // P fp16, V fp16
+#ifdef KB_PF_TIMING
+    long long w_full = 0, w_p = 0, w_all = 0, w_iqk = 0, w_ipv = 0;
+    const long long w_start = clock64();
+#endif
     auto issue_qk = [&](int t, int j) {
       const int stage = j % kPfStages;
       if (t == 0) {
+#ifdef KB_PF_TIMING
+        const long long c0 = clock64();
+#endif
         mbar_wait(&misc->full[stage], (j / kPfStages) & 1);
+#ifdef KB_PF_TIMING
+        w_full += clock64() - c0;
+#endif
         tc_fence_after();
       }
+#ifdef KB_PF_TIMING
+      const long long ci = clock64();
+#endif
       if (lane == 0) {
-        const uint32_t q_addr = smem_u32(sQ + t * kPfQ);
-        const uint32_t k_addr = smem_u32(smem + stage * kPfKV);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t a = sw128_desc(q_addr + (kk >> 2) * kPfHalf + (kk & 3) * 32, 16, 1024);
-          const uint64_t b = sw128_desc(k_addr + (kk >> 2) * kPfHalf + (kk & 3) * 32, 16, 1024);
-          mma_f16_ss(tmem + t * 128, a, b, kIdQK, kk > 0);
-        }
+        mma_ss_k128(tm + t * 128, sw128_desc(smem_u32(sQ + t * kPfQ), 16, 1024),
+                    sw128_desc(smem_u32(smem + stage * kPfKV), 16, 1024), kIdQK);
         mma_commit(&misc->s_full[t]);
       }
       __syncwarp();
+#ifdef KB_PF_TIMING
+      w_iqk += clock64() - ci;
+#endif
     };
     auto issue_pv = [&](int t, int j) {
+#ifdef KB_PF_TIMING
+      const long long c0 = clock64();
+#endif
       mbar_wait(&misc->p_ready[t], j & 1);
+#ifdef KB_PF_TIMING
+      w_p += clock64() - c0;
+#endif
       tc_fence_after();
+#ifdef KB_PF_TIMING
+      const long long ci = clock64();
+#endif
       if (lane == 0) {
         const int stage = j % kPfStages;
-        const uint32_t v_addr = smem_u32(smem + stage * kPfKV + 2 * kPfHalf);
-        const uint32_t p_base = tmem + t * 128;
         // 16-key group m: P (fp16 pairs) at TMEM column 8m, V rows 16m..16m+15
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const uint64_t b = sw128_desc(v_addr + m * 2048, kPfHalf, 1024);  // MN-major V
-          mma_f16_ts(tmem + 256 + t * 128, p_base + 8 * m, b, kIdPV, (j > 0 || m > 0) ? 1u : 0u);
-        }
+        mma_ts_k128(tm + 256 + t * 128, tm + t * 128,
+                    sw128_desc(smem_u32(smem + stage * kPfKV + 2 * kPfHalf), kPfHalf, 1024), kIdPV,
+                    j > 0 ? 1u : 0u);
         // O_t is read only by the epilogue: signal once, after the last tile
         if (j == nt - 1) mma_commit(&misc->o_done[t]);
         if (t == 1) mma_commit(&misc->empty[stage]);
       }
       __syncwarp();
+#ifdef KB_PF_TIMING
+      w_ipv += clock64() - ci;
+#endif
     };
     mbar_wait(&misc->q_full, 0);
     tc_fence_after();
@@ -273,6 +294,13 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       issue_pv(1, j);
       if (j + 1 < nt) issue_qk(1, j + 1);
     }
+#ifdef KB_PF_TIMING
+    w_all = clock64() - w_start;
+    if (lane == 0 && blockIdx.x == 7 && blockIdx.y == 0 && blockIdx.z == 0)
+      printf("pf-timing mma: tiles %d wait-full %lld wait-p %lld issue-qk %lld issue-pv %lld "
+             "total %lld per tile\n", nt, w_full / nt, w_p / nt, w_iqk / nt, w_ipv / nt,
+             w_all / nt);
+#endif
   }
   } else {
     // ------------------------------------------------ softmax warpgroup t
