@@ -357,36 +357,13 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 #ifdef KB_PF_TIMING
       t_a += clock64();
 #endif
-      float mr8[8];  // eight independent 3-input max chains
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mr8[k] = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (full_tile) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 2)
-            mr8[(i >> 1) & 7] = fmaxf(mr8[(i >> 1) & 7],
-                                      fmaxf(__uint_as_float(sr[c][i]), __uint_as_float(sr[c][i + 1])));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const bool ok = row_ok && (kbase + c * 32 + i) <= qpos;
-            mr8[i & 7] = fmaxf(mr8[i & 7], ok ? __uint_as_float(sr[c][i]) : -INFINITY);
-          }
-        }
-      }
-      const float mraw = fmaxf(fmaxf(fmaxf(mr8[0], mr8[1]), fmaxf(mr8[2], mr8[3])),
-                               fmaxf(fmaxf(mr8[4], mr8[5]), fmaxf(mr8[6], mr8[7])));
-      const float mx = mraw * scale_log2;
-#ifdef KB_PF_TIMING
-      t_b += clock64();
-#endif
-      // lazy rescale: move the reference max only when it grows by > 2^8.
-      // TMEM ld/st are warp-collective, so the whole warp rescales when any
-      // of its rows needs it (alpha = 1 for the others).
-      const bool need = mx > m_ref + kRescaleLog2;
-      if (__any_sync(0xffffffffu, need)) {
-        const float alpha = !need ? 1.f : (m_ref == -INFINITY ? 0.f : exp2f(m_ref - mx));
+      // Once every row of the warp has a reference max, the tile goes
+      // straight to the exponentials and the row max rides along (one pass
+      // over the registers); only when some x = s*scale - m_ref exceeds the
+      // lazy-rescale bound does the warp rescale and recompute P.  The first
+      // tile of a row takes the max pass first.
+      const bool fast = __all_sync(0xffffffffu, m_ref != -INFINITY);
+      auto rescale_o = [&](float alpha) {
         if (j > 0) {
           // O_t += P.V of tile j-1 completed before QK_t(j) (in-order pipe,
           // and s_full tracks every earlier MMA of the issuer)
@@ -400,11 +377,45 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
             tmem_st_32x32b_x32(o_addr + c * 32, w);
           }
         }
-        if (need) {
-          l_run *= alpha;
-          m_ref = mx;
+      };
+      if (!fast) {
+        float mr8[8];  // eight independent 3-input max chains
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mr8[k] = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (full_tile) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2)
+              mr8[(i >> 1) & 7] = fmaxf(mr8[(i >> 1) & 7], fmaxf(__uint_as_float(sr[c][i]),
+                                                                 __uint_as_float(sr[c][i + 1])));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const bool ok = row_ok && (kbase + c * 32 + i) <= qpos;
+              mr8[i & 7] = fmaxf(mr8[i & 7], ok ? __uint_as_float(sr[c][i]) : -INFINITY);
+            }
+          }
+        }
+        const float mraw = fmaxf(fmaxf(fmaxf(mr8[0], mr8[1]), fmaxf(mr8[2], mr8[3])),
+                                 fmaxf(fmaxf(mr8[4], mr8[5]), fmaxf(mr8[6], mr8[7])));
+        const float mx = mraw * scale_log2;
+        // lazy rescale: move the reference max only when it grows by > 2^8.
+        // TMEM ld/st are warp-collective, so the whole warp rescales when any
+        // of its rows needs it (alpha = 1 for the others).
+        const bool need = mx > m_ref + kRescaleLog2;
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = !need ? 1.f : (m_ref == -INFINITY ? 0.f : exp2f(m_ref - mx));
+          rescale_o(alpha);
+          if (need) {
+            l_run *= alpha;
+            m_ref = mx;
+          }
         }
       }
+#ifdef KB_PF_TIMING
+      t_b += clock64();
+#endif
       if (kbase + kPfTile > kv_len && t == 0) {  // partial tile: zero V rows past kv_len
         const int stage = j % kPfStages;
         mbar_wait(&misc->full[stage], (j / kPfStages) & 1);
@@ -424,13 +435,15 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       // fp16, kb_append.cu), written over S: the 64 keys of S half hh land in
       // P columns [32hh, 32hh + 32) -- columns whose S values were consumed.
       float2 rs2[4] = {};  // four partial sums: no 64-long dependent add chain
+      float xm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // fast path: max of x
       const bool live = m_ref != -INFINITY;
       const float2 sc2 = make_float2(scale_log2, scale_log2);
-      const float2 nm2 = make_float2(-m_ref, -m_ref);
+      float2 nm2 = make_float2(-m_ref, -m_ref);
       // one straight-line body per case: unmasked tiles carry no selects
-      auto p_half = [&](auto masked, auto half, uint32_t (&w)[32]) {
+      auto p_half = [&](auto masked, auto half, auto track, uint32_t (&w)[32]) {
         constexpr bool kMasked = decltype(masked)::value;
         constexpr int hh = decltype(half)::value;
+        constexpr bool kTrack = decltype(track)::value;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int col = 2 * i;  // 0..63 within the half
@@ -446,22 +459,46 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
           }
           if (kMasked) {
             const int key = kbase + hh * 64 + col;
-            v.x = (row_ok && key <= qpos && live) ? v.x : 0.f;
-            v.y = (row_ok && key + 1 <= qpos && live) ? v.y : 0.f;
+            const bool ok0 = row_ok && key <= qpos && live, ok1 = row_ok && key + 1 <= qpos && live;
+            v.x = ok0 ? v.x : 0.f;
+            v.y = ok1 ? v.y : 0.f;
+            if (kTrack)
+              xm4[i & 3] = fmaxf(xm4[i & 3], fmaxf(ok0 ? xv.x : -INFINITY, ok1 ? xv.y : -INFINITY));
+          } else if (kTrack) {
+            xm4[i & 3] = fmaxf(xm4[i & 3], fmaxf(xv.x, xv.y));
           }
           rs2[i & 3] = fadd2(rs2[i & 3], v);
           const __half2 hp = __floats2half2_rn(v.x, v.y);
           w[i] = *reinterpret_cast<const uint32_t*>(&hp);
         }
       };
-      {
+      auto p_pass = [&](auto track) {
         uint32_t w[32];
-        if (full_tile) p_half(std::false_type{}, std::integral_constant<int, 0>{}, w);
-        else p_half(std::true_type{}, std::integral_constant<int, 0>{}, w);
+        if (full_tile) p_half(std::false_type{}, std::integral_constant<int, 0>{}, track, w);
+        else p_half(std::true_type{}, std::integral_constant<int, 0>{}, track, w);
         tmem_st_32x32b_x32(s_addr, w);
-        if (full_tile) p_half(std::false_type{}, std::integral_constant<int, 1>{}, w);
-        else p_half(std::true_type{}, std::integral_constant<int, 1>{}, w);
+        if (full_tile) p_half(std::false_type{}, std::integral_constant<int, 1>{}, track, w);
+        else p_half(std::true_type{}, std::integral_constant<int, 1>{}, track, w);
         tmem_st_32x32b_x32(s_addr + 32, w);
+      };
+      if (fast) {
+        p_pass(std::true_type{});
+        const float xmax = fmaxf(fmaxf(xm4[0], xm4[1]), fmaxf(xm4[2], xm4[3]));
+        const bool need = xmax > kRescaleLog2;
+        if (__any_sync(0xffffffffu, need)) {  // rare: the row max grew by > 2^8
+          const float alpha = need ? exp2f(-xmax) : 1.f;  // 2^(m_ref - (m_ref + xmax))
+          rescale_o(alpha);
+          if (need) {
+            l_run *= alpha;
+            m_ref += xmax;
+          }
+          nm2 = make_float2(-m_ref, -m_ref);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) rs2[k] = make_float2(0.f, 0.f);
+          p_pass(std::false_type{});  // P again with the new reference (overwrites)
+        }
+      } else {
+        p_pass(std::false_type{});
       }
       tmem_st_wait();
 #ifdef KB_PF_TIMING
