@@ -106,6 +106,9 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 #define KB_PF_EMU_EVERY 6
 #endif
 constexpr int kEmuEvery = KB_PF_EMU_EVERY;
+// (Strictly alternating the two tiles' exponential passes through an
+// mbarrier token measured 64.4% vs 65.7% without: the pass is latency-bound
+// per warp, not only MUFU-bound.)
 
 struct PrefillMisc {
   uint64_t full[kPfStages];
