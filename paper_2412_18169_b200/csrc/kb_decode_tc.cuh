@@ -152,6 +152,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     }
   } else if (warp == 5) {
     // ------------------------------------------------ MMA issuer
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // warp-uniform MMA operands
     constexpr uint32_t kIdQK = idesc_bf16_f32(128, 16, false, false);
     constexpr uint32_t kIdPV = idesc_f16_f32(128, 16, true, false);  // V^T fp16, P^T fp16
     const uint32_t p_base = smem_u32(sP);
@@ -170,14 +171,10 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       mbar_wait(&misc->full[stage], (qj / kDecStages) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t k_addr = smem_u32(smem + stage * kStageBytes);
-        const uint32_t q_addr = smem_u32(sQ + (qr & 1) * kQBytes);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t a = sw128_desc(k_addr + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024);
-          const uint64_t b = sw128_desc(q_addr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-          mma_f16_ss(tmem + (qj & 1) * 16, a, b, kIdQK, kk > 0);
-        }
+        // A = K tile (d-halves 16 KiB apart), B = Q (d-halves 2 KiB apart)
+        mma_ss_8<2, 4, 6, 1024, 1026, 1028, 1030, 2, 4, 6, 128, 130, 132, 134>(
+            tm + (qj & 1) * 16, sw128_desc(smem_u32(smem + stage * kStageBytes), 16, 1024),
+            sw128_desc(smem_u32(sQ + (qr & 1) * kQBytes), 16, 1024), kIdQK, 0u);
         mma_commit(&misc->s_full[qj & 1]);
       }
       __syncwarp();
@@ -195,15 +192,11 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         tc_fence_after();
         if (lane == 0) {
           const int stage = j % kDecStages;
-          const uint32_t v_addr = smem_u32(smem + stage * kStageBytes + 2 * kHalfBytes);
-          const uint32_t p_addr = p_base + (j & 1) * kPBytes;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            // A = V^T, MN-major: LBO = d-half stride, SBO = 8-token group stride
-            const uint64_t a = sw128_desc(v_addr + kk * 2048, kHalfBytes, 1024);
-            const uint64_t b = sw128_desc(p_addr + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-            mma_f16_ss(tmem + 32 + (j & 1) * 16, a, b, kIdPV, kk > 0);
-          }
+          // A = V^T, MN-major (16 tokens = 2 KiB per step); B = P^T (halves 2 KiB apart)
+          mma_ss_8<128, 256, 384, 512, 640, 768, 896, 2, 4, 6, 128, 130, 132, 134>(
+              tm + 32 + (j & 1) * 16,
+              sw128_desc(smem_u32(smem + stage * kStageBytes + 2 * kHalfBytes), kHalfBytes, 1024),
+              sw128_desc(p_base + (j & 1) * kPBytes, 16, 1024), kIdPV, 0u);
           mma_commit(&misc->o_full[j & 1]);
           mma_commit(&misc->empty[stage]);
         }

@@ -197,6 +197,35 @@ __device__ __forceinline__ void mma_ts_k128(uint32_t tmem_d, uint32_t tmem_a, ui
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc_first)
       : "memory");
 }
+// Eight K-steps of D[tmem] (+)= A[smem] * B[smem] with arbitrary per-step
+// descriptor offsets (16-byte units; step 0 at offset 0).  acc_first = 0
+// overwrites D on the first step.
+template <int A1, int A2, int A3, int A4, int A5, int A6, int A7,
+          int B1, int B2, int B3, int B4, int B5, int B6, int B7>
+__device__ __forceinline__ void mma_ss_8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t acc_first) {
+  asm volatile(
+      "{\n\t.reg .pred pf, pt;\n\t.reg .b64 a, b;\n\t"
+      "setp.ne.b32 pf, %4, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pf;\n\t"
+      "add.s64 a, %1, %5;\n\tadd.s64 b, %2, %12;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+      "add.s64 a, %1, %6;\n\tadd.s64 b, %2, %13;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+      "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %14;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+      "add.s64 a, %1, %8;\n\tadd.s64 b, %2, %15;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+      "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %16;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+      "add.s64 a, %1, %10;\n\tadd.s64 b, %2, %17;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+      "add.s64 a, %1, %11;\n\tadd.s64 b, %2, %18;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc_first), "n"(A1), "n"(A2), "n"(A3), "n"(A4),
+      "n"(A5), "n"(A6), "n"(A7), "n"(B1), "n"(B2), "n"(B3), "n"(B4), "n"(B5), "n"(B6), "n"(B7)
+      : "memory");
+}
 // Arrive (once) on an mbarrier when all prior tcgen05 ops of this thread finish.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
