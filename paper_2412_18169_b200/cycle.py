@@ -38,7 +38,7 @@ def _span_ms(done) -> float:
     """Device time of completed submissions (each (start, end) event pair once)."""
     seen = {}
     for p in done:
-        if p.start_event is not None:
+        if p.start_event is not None and id(p.event) not in seen:
             seen[id(p.event)] = p.start_event.elapsed_time(p.event)
     return sum(seen.values())
 

@@ -25,6 +25,7 @@ as in the reference; completion is a CUDA event the engine polls.
 
 from __future__ import annotations
 
+from collections import deque
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -113,7 +114,7 @@ class TransferEngine:
         self.flows: dict[tuple[int, int, int], KVFlow] = {}
         self.chunk_of: dict[int, tuple[tuple[int, int, int], int]] = {}
         self.param_off: dict[int, int] = {}
-        self.pending: list[Pending] = []
+        self.pending: deque[Pending] = deque()
         self.stats = TransferStats()
         self.timing = timing
         # swapped-out KV (HOST endpoint): rid -> (pinned tensor, layers, npages)
@@ -375,12 +376,15 @@ class TransferEngine:
     def poll(self, block: bool = False) -> list[Pending]:
         """Completed tasks in submission order; runs their callbacks."""
         out = []
+        done_ev = None  # a burst shares one event: check / wait for it once
         while self.pending:
             p = self.pending[0]
-            if not block and not p.event.query():
-                break
-            p.event.synchronize()
-            self.pending.pop(0)
+            if p.event is not done_ev:
+                if not block and not p.event.query():
+                    break
+                p.event.synchronize()
+                done_ev = p.event
+            self.pending.popleft()
             if p.task.kind is TaskKind.KVCACHE_CHUNK:
                 fl = self.flows.get((p.task.rid, p.task.src, p.task.dst))
                 if fl is not None:

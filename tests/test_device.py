@@ -272,6 +272,56 @@ def test_swap_pages_round_trip_bit_exact(rt):
     pool.close()
 
 
+def test_baseline_moves_through_the_transfer_engine(rt):
+    """The baselines' whole-request KV moves as the engine issues them
+    (engine.py:906-1047): swap out to HOST, swap back in on other pages,
+    then migrate to another instance's pool -- every byte arrives."""
+    from paper_2412_18169_b200.exchange import HOST, TaskKind, TransferTask
+    from paper_2412_18169_b200.transfer import SlotTable, TransferEngine
+    model = TINY.spec()
+    a = rt.create_pool(0, model, model.param_bytes + 4 * MIB, TINY)
+    b = rt.create_pool(1, model, model.param_bytes + 4 * MIB, TINY)
+    slots = {0: SlotTable(rt.max_slots), 1: SlotTable(rt.max_slots)}
+    te = TransferEngine({0: a, 1: b}, slots)
+    rid, tokens = 7, 5 * TINY.block_tokens - 3   # 5 pages per layer
+    sa = slots[0].get(rid)
+    assert a.grow([(sa, 0, 2, 5)])
+    kv_a = a.kv_bytes().view(-1, a.page_bytes)
+    pages = [a.block_table(sa, l) for l in range(2)]
+    want = torch.randint(0, 256, (10, a.page_bytes), dtype=torch.uint8, device="cuda")
+    kv_a[torch.tensor(pages[0] + pages[1], device="cuda")] = want
+    nbytes = tokens * model.kv_bytes_per_token
+    out = TransferTask(1, TaskKind.KVCACHE_CHUNK, 0, HOST, nbytes, rid=rid)
+    te.register_request_move(out, (0, 2), tokens)
+    te.submit(out)
+    te.drain()
+    a.release([sa], 0, 2)
+    slots[0].drop(rid)
+    assert a.grow([(slots[0].get(99), 0, 2, 2)])   # the freed pages go elsewhere
+    sa = slots[0].get(rid)
+    assert a.grow([(sa, 0, 2, 5)])
+    back = TransferTask(2, TaskKind.KVCACHE_CHUNK, HOST, 0, nbytes, rid=rid)
+    te.register_request_move(back, (0, 2), tokens)
+    te.submit(back)
+    te.drain()
+    te.release_host(rid)
+    got = [a.block_table(sa, l) for l in range(2)]
+    assert torch.equal(kv_a[torch.tensor(got[0] + got[1], device="cuda")], want)
+    # migrate 0 -> 1 (destination pages allocated first, as group_alloc does)
+    sb = slots[1].get(rid)
+    assert b.grow([(sb, 0, 2, 5)])
+    mig = TransferTask(3, TaskKind.KVCACHE_CHUNK, 0, 1, nbytes, rid=rid)
+    te.register_request_move(mig, (0, 2), tokens)
+    te.submit(mig)
+    te.drain()
+    kv_b = b.kv_bytes().view(-1, b.page_bytes)
+    pb = [b.block_table(sb, l) for l in range(2)]
+    assert torch.equal(kv_b[torch.tensor(pb[0] + pb[1], device="cuda")], want)
+    assert te.host_kv == {}
+    a.close()
+    b.close()
+
+
 def test_host_replica_restore_through_the_plan(rt):
     """exchange.HOST (exchange.py:18, 224-233): when no live instance holds a
     layer, plan_restore_transfers sources it from the host replica; the
