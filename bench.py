@@ -29,6 +29,7 @@ shards into independent groups: scaling "weak", no data-path collective).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -63,19 +64,47 @@ class Clocks:
         self.rows = []
         self._stop = threading.Event()
         self._t = None
+        try:  # initialise NVML outside the timed region (the first init is slow)
+            import pynvml
+            pynvml.nvmlInit()
+        except Exception:
+            pass
 
     def start(self):
+        # NVML when available: a query costs microseconds, so the timed region
+        # (tens of ms) gets many samples; nvidia-smi (~50 ms per call) otherwise
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = [("hw_slowdown", pynvml.nvmlClocksThrottleReasonHwSlowdown),
+                    ("hw_thermal_slowdown", pynvml.nvmlClocksThrottleReasonHwThermalSlowdown),
+                    ("sw_thermal_slowdown", pynvml.nvmlClocksThrottleReasonSwThermalSlowdown),
+                    ("sw_power_cap", pynvml.nvmlClocksThrottleReasonSwPowerCap)]
+
+            def sample():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append([str(self.device), str(sm), str(mx), "", ""] +
+                                 ["Active" if rs & b else "Not Active" for _, b in bits])
+            period = 0.005
+        except Exception:
+            def sample():
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            period = 0.2
+
         def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.device),
-                                          f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
-                                         capture_output=True, text=True, timeout=5).stdout
-                    for line in out.strip().splitlines():
-                        self.rows.append([x.strip() for x in line.split(",")])
+                    sample()
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(period)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -404,11 +433,16 @@ def main():
     torch.cuda.synchronize()
     reps = []
     launches0 = runtime.LAUNCHES[0]
+    # the collector runs between steps, not inside them (a full collection
+    # of this process's heap costs milliseconds; serving loops do the same)
+    gc.collect()
+    gc.disable()
     t_host = time.perf_counter()
     for _ in range(args.steps):
         reps.append(cyc.step())
     torch.cuda.synchronize()
     host_s = time.perf_counter() - t_host
+    gc.enable()
     launches = runtime.LAUNCHES[0] - launches0
     if ws > 1:
         torch.distributed.barrier()
@@ -447,18 +481,25 @@ def main():
     res = torch.empty(len(cyc.tokens), dtype=torch.int32).pin_memory()
     cyc.auto_refill = False
     e2e_s = 0.0
+    e2e_steps = []
+    gc.collect()
+    gc.disable()
     e_moved = 0
-    for _ in range(args.steps):
+    for i in range(args.warmup + args.steps):  # the first W steps are warm-up
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         tok_d = tok.to("cuda", non_blocking=True)
         r = cyc.step()
-        e_moved += r.bytes_moved
         res.copy_(cyc.home_first_pages(), non_blocking=True)
         torch.cuda.synchronize()
-        e2e_s += time.perf_counter() - t0
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_steps.append(round(dt * 1e3, 2))
+            e2e_s += dt
+            e_moved += r.bytes_moved
         del tok_d
         cyc.refill()  # the next burst's arrivals: not part of the cycle
+    gc.enable()
     cyc.auto_refill = True
     r_last = reps[-1]
     cyc.close()
@@ -532,7 +573,8 @@ def main():
             "nvlink_cycle_pp4": nvl4,
             "parity": parity,
             "e2e": {"value": round(e_moved / e2e_s / 1e9, 1), "unit": "GB/s",
-                    "h2d_bytes_per_step": tok.numel() * 4, "d2h_bytes_per_step": res.numel() * 4},
+                    "h2d_bytes_per_step": tok.numel() * 4, "d2h_bytes_per_step": res.numel() * 4,
+                    "ms_per_step": e2e_steps},
             "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,
