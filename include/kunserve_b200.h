@@ -230,6 +230,7 @@ int kb_copy_bytes(uint64_t dst, uint64_t src, int64_t nbytes, uintptr_t stream);
  * rows with kb_copy_bytes -- stores over NVLink into the peer's HBM. */
 int kb_device_alloc(int32_t device, int64_t nbytes, uint64_t* ptr);
 int kb_device_free(uint64_t ptr);
+/* ptr must be a kb_device_alloc pointer (CUDA IPC names whole allocations) */
 int kb_ipc_mem_export(uint64_t ptr, uint8_t* handle /* 64 bytes */);
 int kb_ipc_mem_import(int32_t device, const uint8_t* handle, uint64_t* ptr);
 int kb_ipc_mem_close(uint64_t ptr);
