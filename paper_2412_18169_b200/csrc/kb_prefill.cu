@@ -117,7 +117,9 @@ struct PrefillMisc {
   uint64_t full[kPfStages];
   uint64_t empty[kPfStages];
   uint64_t s_full[2];
-  uint64_t p_ready[2];
+  uint64_t p_lo[2];   // P of keys 0-63 of tile t stored (PV may start on them)
+  uint64_t p_hi[2];   // P of keys 64-127 stored
+  uint64_t pv_lo[2];  // the PV K-steps over keys 0-63 of tile t completed
   uint64_t o_done[2];
   uint64_t q_full;
   uint32_t tmem_base;
@@ -174,7 +176,9 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       }
       for (int t = 0; t < 2; ++t) {
         mbar_init(&misc->s_full[t], 1);
-        mbar_init(&misc->p_ready[t], 128);
+        mbar_init(&misc->p_lo[t], 128);
+        mbar_init(&misc->p_hi[t], 128);
+        mbar_init(&misc->pv_lo[t], 1);
         mbar_init(&misc->o_done[t], 1);
       }
       mbar_init(&misc->q_full, 256);
@@ -264,10 +268,14 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 #endif
     };
     auto issue_pv = [&](int t, int j) {
+      // keys 0-63 as soon as their P is stored, keys 64-127 after the rest:
+      // the first half of P.V overlaps the second half of the softmax
+      const int stage = j % kPfStages;
+      const uint64_t vdesc = sw128_desc(smem_u32(smem + stage * kPfKV + 2 * kPfHalf), kPfHalf, 1024);
 #ifdef KB_PF_TIMING
       const long long c0 = clock64();
 #endif
-      mbar_wait(&misc->p_ready[t], j & 1);
+      mbar_wait(&misc->p_lo[t], j & 1);
 #ifdef KB_PF_TIMING
       w_p += clock64() - c0;
 #endif
@@ -276,11 +284,15 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       const long long ci = clock64();
 #endif
       if (lane == 0) {
-        const int stage = j % kPfStages;
         // 16-key group m: P (fp16 pairs) at TMEM column 8m, V rows 16m..16m+15
-        mma_ts_k128(tm + 256 + t * 128, tm + t * 128,
-                    sw128_desc(smem_u32(smem + stage * kPfKV + 2 * kPfHalf), kPfHalf, 1024), kIdPV,
-                    j > 0 ? 1u : 0u);
+        mma_ts_k64(tm + 256 + t * 128, tm + t * 128, vdesc, kIdPV, j > 0 ? 1u : 0u);
+        mma_commit(&misc->pv_lo[t]);
+      }
+      __syncwarp();
+      mbar_wait(&misc->p_hi[t], j & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        mma_ts_k64(tm + 256 + t * 128, tm + t * 128 + 32, vdesc + 512, kIdPV, 1u);
         // O_t is read only by the epilogue: signal once, after the last tile
         if (j == nt - 1) mma_commit(&misc->o_done[t]);
         if (t == 1) mma_commit(&misc->empty[stage]);
@@ -478,18 +490,37 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
           w[i] = *reinterpret_cast<const uint32_t*>(&hp);
         }
       };
-      auto p_pass = [&](auto track) {
+      auto store_half = [&](auto half, auto track) {
+        constexpr int hh = decltype(half)::value;
         uint32_t w[32];
-        if (full_tile) p_half(std::false_type{}, std::integral_constant<int, 0>{}, track, w);
-        else p_half(std::true_type{}, std::integral_constant<int, 0>{}, track, w);
-        tmem_st_32x32b_x32(s_addr, w);
-        if (full_tile) p_half(std::false_type{}, std::integral_constant<int, 1>{}, track, w);
-        else p_half(std::true_type{}, std::integral_constant<int, 1>{}, track, w);
-        tmem_st_32x32b_x32(s_addr + 32, w);
+        if (full_tile) p_half(std::false_type{}, half, track, w);
+        else p_half(std::true_type{}, half, track, w);
+        tmem_st_32x32b_x32(s_addr + 32 * hh, w);
       };
+      auto take_rs = [&]() {
+        const float r = (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y) + (rs2[2].x + rs2[2].y) +
+                        (rs2[3].x + rs2[3].y);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) rs2[k] = make_float2(0.f, 0.f);
+        return r;
+      };
+      auto take_xmax = [&]() {
+        const float r = fmaxf(fmaxf(xm4[0], xm4[1]), fmaxf(xm4[2], xm4[3]));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xm4[k] = -INFINITY;
+        return r;
+      };
+      auto publish = [&](uint64_t* bar) {
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(bar);
+      };
+      using H0 = std::integral_constant<int, 0>;
+      using H1 = std::integral_constant<int, 1>;
+      // keys 0-63
       if (fast) {
-        p_pass(std::true_type{});
-        const float xmax = fmaxf(fmaxf(xm4[0], xm4[1]), fmaxf(xm4[2], xm4[3]));
+        store_half(H0{}, std::true_type{});
+        const float xmax = take_xmax();
         const bool need = xmax > kRescaleLog2;
         if (__any_sync(0xffffffffu, need)) {  // rare: the row max grew by > 2^8
           const float alpha = need ? exp2f(-xmax) : 1.f;  // 2^(m_ref - (m_ref + xmax))
@@ -499,21 +530,50 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
             m_ref += xmax;
           }
           nm2 = make_float2(-m_ref, -m_ref);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) rs2[k] = make_float2(0.f, 0.f);
-          p_pass(std::false_type{});  // P again with the new reference (overwrites)
+          take_rs();
+          store_half(H0{}, std::false_type{});  // P again with the new reference
         }
       } else {
-        p_pass(std::false_type{});
+        store_half(H0{}, std::false_type{});
       }
-      tmem_st_wait();
+      l_run += take_rs();
+      publish(&misc->p_lo[t]);
+      // keys 64-127 (the P.V of keys 0-63 may already be running)
+      if (fast) {
+        store_half(H1{}, std::true_type{});
+        const float xmax = take_xmax();
+        const bool need = xmax > kRescaleLog2;
+        if (__any_sync(0xffffffffu, need)) {
+          // rare: O already holds this tile's first-half P.V under the old
+          // reference -- let it land, then rescale everything so far
+          mbar_wait(&misc->pv_lo[t], j & 1);
+          tc_fence_after();
+          const float alpha = need ? exp2f(-xmax) : 1.f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float part[32];
+            tmem_ld_32x32b_x32(o_addr + c * 32, part);
+            uint32_t w[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(part[i] * alpha);
+            tmem_st_32x32b_x32(o_addr + c * 32, w);
+          }
+          if (need) {
+            l_run *= alpha;
+            m_ref += xmax;
+          }
+          nm2 = make_float2(-m_ref, -m_ref);
+          take_rs();
+          store_half(H1{}, std::false_type{});
+        }
+      } else {
+        store_half(H1{}, std::false_type{});
+      }
+      l_run += take_rs();
 #ifdef KB_PF_TIMING
       t_c += clock64();
 #endif
-      l_run += (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y) + (rs2[2].x + rs2[2].y) +
-               (rs2[3].x + rs2[3].y);
-      tc_fence_before();
-      mbar_arrive(&misc->p_ready[t]);
+      publish(&misc->p_hi[t]);
 #ifdef KB_PF_TIMING
       t_soft += clock64() - tw1;
 #endif
