@@ -106,6 +106,9 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 #define KB_PF_EMU_EVERY 6
 #endif
 constexpr int kEmuEvery = KB_PF_EMU_EVERY;
+// (Issuing the QK of keys 64-127 early -- those S columns never hold P --
+// as N=64 MMAs measured 52% against 67%: the half-width MMAs re-read Q for
+// every half and double the QK instruction count.)
 // (ex2.approx.f16x2 for a pair -- one MUFU op instead of two -- keeps the
 // error at 3e-4 mean-rel but costs conversions: 50-61% of peak, so the pass
 // is bound by instruction latency, not by the MUFU units.)
