@@ -47,3 +47,16 @@ def test_runtime_refuses_without_library(tmp_path, monkeypatch):
     else:
         raise AssertionError("runtime imported without _kb.so")
     importlib.reload(rt)
+
+
+def test_prefill_split_heuristic():
+    """runtime.prefill_splits: 1 for short contexts, a wave-filling count
+    for long ones, never fewer than 16 key tiles per split."""
+    from paper_2412_18169_b200.runtime import prefill_splits
+    assert prefill_splits(1, 40, 2048, 2048) == 1          # 16 tiles: no room to split
+    assert prefill_splits(1, 40, 2048, 32768) == 4         # config 4 late chunks (B200 sweep)
+    for kv in (4096, 8192, 16384, 32768):
+        s = prefill_splits(1, 32, 2048, kv)
+        assert 1 <= s <= 8 and (kv // 128) >= 16 * s or s == 1
+    # a grid that already fills whole waves stays unsplit
+    assert prefill_splits(37, 32, 256, 32768) == 1          # 37 * 32 = 8 x 148 CTAs
