@@ -269,6 +269,14 @@ int kb_paged_prefill(kb_pool* pool, int32_t layer, int32_t n_q_heads, uint64_t q
                      int32_t nseq, int32_t max_q_len, float scale, uint64_t out,
                      uint64_t workspace, int32_t kv_splits, uintptr_t stream);
 
+/* ---- decoder-layer elementwise ops for the device-backed engine --------- */
+/* Stage execution of a pipeline member (engine.py:389-397 charges its time):
+ * x (+)= res in place (res may be 0), out = rmsnorm(x) * w; bf16 rows of
+ * `hidden` elements.  And the SwiGLU: out[r, :] = silu(gu[r, :F]) * gu[r, F:]. */
+int kb_add_rmsnorm(uint64_t x, uint64_t res, uint64_t w, uint64_t out, int32_t n,
+                   int32_t hidden, float eps, uintptr_t stream);
+int kb_silu_mul(uint64_t gu, uint64_t out, int32_t n, int32_t ffn, uintptr_t stream);
+
 #ifdef __cplusplus
 }
 #endif

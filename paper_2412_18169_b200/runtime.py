@@ -103,6 +103,8 @@ _sigs = {
                                           C.c_int64, _S]),
     "kb_copy_bytes": (C.c_int, [_U, _U, C.c_int64, _S]),
     "kb_copy_pages_host": (C.c_int, [_P, C.POINTER(Move), _P, C.c_int32, _S]),
+    "kb_add_rmsnorm": (C.c_int, [_U, _U, _U, _U, C.c_int32, C.c_int32, C.c_float, _S]),
+    "kb_silu_mul": (C.c_int, [_U, _U, C.c_int32, C.c_int32, _S]),
     "kb_device_alloc": (C.c_int, [C.c_int32, C.c_int64, C.POINTER(C.c_uint64)]),
     "kb_device_free": (C.c_int, [_U]),
     "kb_ipc_mem_export": (C.c_int, [_U, C.POINTER(C.c_uint8)]),
@@ -485,6 +487,19 @@ class IpcBuffer:
         if self.ptr:
             _check(_lib.kb_device_free(self.ptr) if self.owned else _lib.kb_ipc_mem_close(self.ptr))
             self.ptr = 0
+
+
+def add_rmsnorm(x, res, w, out, eps: float = 1e-5, stream=None) -> None:
+    """x (+)= res in place (res None: no add); out = rmsnorm(x) * w (bf16 rows)."""
+    _check(_lib.kb_add_rmsnorm(x.data_ptr(), 0 if res is None else res.data_ptr(), w.data_ptr(),
+                               out.data_ptr(), x.shape[0], x.shape[1], eps, _stream(stream)),
+           launches=1)
+
+
+def silu_mul(gu, out, stream=None) -> None:
+    """out = silu(gu[:, :F]) * gu[:, F:] (bf16)."""
+    _check(_lib.kb_silu_mul(gu.data_ptr(), out.data_ptr(), gu.shape[0], out.shape[1],
+                            _stream(stream)), launches=1)
 
 
 def copy_bytes(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:

@@ -95,7 +95,14 @@ class StageRunner:
         self.scale = shape.head_dim ** -0.5
 
     def _weights(self, l):
-        return LayerWeights(self.pool.weight_bytes(l), self.shape)
+        # a layer's slab sits at a fixed weight VA (mapped once at pool
+        # creation), so its views are built once
+        if not hasattr(self, "_wcache"):
+            self._wcache = {}
+        w = self._wcache.get(l)
+        if w is None:
+            w = self._wcache[l] = LayerWeights(self.pool.weight_bytes(l), self.shape)
+        return w
 
     # -- CUDA graphs for decode-only microbatches -------------------------
     # One graph per (layers, batch size), captured on first use after an
@@ -115,7 +122,7 @@ class StageRunner:
             self._graphs = {}
         if key in self._graphs:
             return
-        self.run(lo, hi, x, batch)  # warm-up: lazy attributes, cuBLAS handles
+        self.run(lo, hi, x.clone(), batch)  # warm-up: lazy attributes, cuBLAS handles
         st = {"x": x.clone(), "slots": batch["slots"].clone(), "pos": batch["pos"].clone(),
               "d_slots": batch["d_slots"].clone(), "d_ctx": batch["d_ctx"].clone(),
               "d_rows": batch["d_rows"].clone()}
@@ -143,19 +150,18 @@ class StageRunner:
         g.replay()
         return st["out"]
 
-    @staticmethod
-    def _rmsnorm(x, w, torch):
-        xf = x.float()
-        return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5)).to(x.dtype) * w
-
     def run(self, lo: int, hi: int, x, batch: dict):
+        """Layers [lo, hi) over the microbatch rows x (bf16 [n, hidden],
+        updated in place as the residual stream)."""
         torch = self.torch
         sh = self.shape
-        Hq, Hkv, d = sh.n_q_heads, sh.n_kv_heads, sh.head_dim
+        Hq, Hkv, d, F = sh.n_q_heads, sh.n_kv_heads, sh.head_dim, sh.ffn
         n = x.shape[0]
+        h = torch.empty_like(x)
+        pending = None  # the previous layer's MLP output, added by the next norm
         for l in range(lo, hi):
             w = self._weights(l)
-            h = self._rmsnorm(x, w.n1, torch)
+            runtime.add_rmsnorm(x, pending, w.n1, h)
             qkv = h @ w.wqkv
             q = qkv[:, :Hq * d].reshape(n, Hq, d)
             k = qkv[:, Hq * d:(Hq + Hkv) * d].reshape(n, Hkv, d).contiguous()
@@ -176,11 +182,13 @@ class StageRunner:
                                      batch["d_max"], od, self.ws, self.scale,
                                      max_splits=self.max_splits, reuse_plan=l > lo)
                 o.index_copy_(0, batch["d_rows"], od)
-            x = x + o.reshape(n, Hq * d) @ w.wo
-            h2 = self._rmsnorm(x, w.n2, torch)
-            gu = h2 @ w.wgu
-            F = sh.ffn
-            x = x + (torch.nn.functional.silu(gu[:, :F]) * gu[:, F:]) @ w.wd
+            runtime.add_rmsnorm(x, o.reshape(n, Hq * d) @ w.wo, w.n2, h)  # residual + norm 2
+            gu = h @ w.wgu
+            act = torch.empty((n, F), dtype=x.dtype, device=x.device)
+            runtime.silu_mul(gu, act)
+            pending = act @ w.wd
+        if pending is not None:
+            x.add_(pending)
         return x
 
 

@@ -435,3 +435,29 @@ def test_paged_prefill_matches_oracle(rt, shape, kv_splits):
         ma, mr = check_close(got[offs[i]:offs[i] + c], want)
         assert ma <= 2e-2 and mr <= 1e-3, (shape.name, kv_splits, pre, c, ma, mr)
     pool.close()
+
+
+def test_layer_elementwise_kernels_match_torch(rt):
+    """kb_add_rmsnorm / kb_silu_mul (the device engine's stage execution)
+    against a plain PyTorch fp32 reference of the same ops."""
+    from paper_2412_18169_b200 import runtime
+    g = torch.Generator(device="cuda").manual_seed(3)
+    n, H, F = 37, 4096, 14336
+    x = torch.randn((n, H), device="cuda", generator=g).to(torch.bfloat16)
+    res = torch.randn((n, H), device="cuda", generator=g).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn((H,), device="cuda", generator=g)).to(torch.bfloat16)
+    want_x = (x.float() + res.float()).to(torch.bfloat16)
+    xf = want_x.float()
+    want = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float()
+    out = torch.empty_like(x)
+    runtime.add_rmsnorm(x, res, w, out)
+    torch.cuda.synchronize()
+    assert torch.equal(x, want_x)                      # the residual stream, in place
+    assert (out.float() - want).abs().max().item() <= 3e-2 * want.abs().max().item()
+    gu = torch.randn((n, 2 * F), device="cuda", generator=g).to(torch.bfloat16)
+    act = torch.empty((n, F), dtype=torch.bfloat16, device="cuda")
+    runtime.silu_mul(gu, act)
+    torch.cuda.synchronize()
+    want = torch.nn.functional.silu(gu[:, :F].float()) * gu[:, F:].float()
+    err = (act.float() - want).abs() / want.abs().clamp_min(1e-2)
+    assert err.mean().item() <= 1e-2
