@@ -238,9 +238,12 @@ int kb_ipc_mem_close(uint64_t ptr);
 /* ---- N8: paged attention over the pool --------------------------------- */
 /* Write the new tokens' K/V into their pages.  k, v: [ntok][n_kv_heads][head_dim]
  * bf16; token t belongs to slot slots[t] at position pos[t]; its page must
- * already be in the block table. */
+ * already be in the block table.  row_stride: elements between consecutive
+ * tokens' rows of k and v (0 = contiguous, n_kv_heads * head_dim), so the
+ * K and V column blocks of a fused QKV projection can be passed in place. */
 int kb_kv_append(kb_pool* pool, int32_t layer, uint64_t k, uint64_t v,
-                 uint64_t slots, uint64_t pos, int32_t ntok, uintptr_t stream);
+                 uint64_t slots, uint64_t pos, int32_t ntok, int64_t row_stride,
+                 uintptr_t stream);
 /* Decode: q [nseq][n_q_heads][head_dim] bf16, one query token per sequence
  * attending to ctx_lens[i] cached tokens of slot slots[i] (including its
  * own, already appended).  out [nseq][n_q_heads][head_dim] bf16.

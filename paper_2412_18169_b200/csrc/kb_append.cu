@@ -33,7 +33,7 @@ __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __rest
                                  const int4* __restrict__ k, const int4* __restrict__ v,
                                  const int32_t* __restrict__ slots, const int32_t* __restrict__ pos,
                                  int ntok, int Hkv, int B, int L, int maxp, int layer,
-                                 int64_t page_bytes) {
+                                 int64_t page_bytes, int64_t row_vec) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= ntok * Hkv) return;
@@ -42,7 +42,7 @@ __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __rest
   const int32_t page = bt[((int64_t)slot * L + layer) * maxp + p / B];
   const int row = p % B;
   const int which = lane >> 4;  // 0 = K, 1 = V
-  const int4* src = (which ? v : k) + ((int64_t)t * Hkv + h) * 16 + (lane & 15);
+  const int4* src = (which ? v : k) + (int64_t)t * row_vec + h * 16 + (lane & 15);
   const int64_t half = page_bytes / 2;
   int4* dst = reinterpret_cast<int4*>(kv + (int64_t)page * page_bytes + which * half +
                                       ((int64_t)h * B + row) * 256) + (lane & 15);
@@ -55,12 +55,14 @@ __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __rest
 using namespace kb;
 
 extern "C" int kb_kv_append(kb_pool* p, int32_t layer, uint64_t k, uint64_t v, uint64_t slots,
-                            uint64_t pos, int32_t ntok, uintptr_t stream) {
+                            uint64_t pos, int32_t ntok, int64_t row_stride, uintptr_t stream) {
   if (!p) return fail(KB_EINVAL, "null pool");
   if (p->view) return refuse_view();
   if (p->m.head_dim != 128) return fail(KB_EINVAL, "head_dim must be 128");
   if (layer < 0 || layer >= p->m.num_layers) return fail(KB_EINVAL, "bad layer");
   if (ntok <= 0) return KB_OK;
+  const int64_t stride = row_stride > 0 ? row_stride : (int64_t)p->m.n_kv_heads * 128;
+  if (stride % 8 || ((k | v) & 15)) return fail(KB_EINVAL, "K/V rows must be 16-byte aligned");
   KB_RT(cudaSetDevice(p->device));
   const int64_t warps = (int64_t)ntok * p->m.n_kv_heads;
   int rc = pool_enter(p, (cudaStream_t)stream);
@@ -69,7 +71,7 @@ extern "C" int kb_kv_append(kb_pool* p, int32_t layer, uint64_t k, uint64_t v, u
       reinterpret_cast<uint8_t*>(p->kva), p->d_bt, reinterpret_cast<const int4*>(k),
       reinterpret_cast<const int4*>(v), reinterpret_cast<const int32_t*>(slots),
       reinterpret_cast<const int32_t*>(pos), ntok, p->m.n_kv_heads, p->m.block_tokens,
-      p->m.num_layers, p->maxp, layer, p->m.page_bytes);
+      p->m.num_layers, p->maxp, layer, p->m.page_bytes, stride / 8);
   KB_LAUNCH_CHECK();
   return pool_leave(p, (cudaStream_t)stream);
 }

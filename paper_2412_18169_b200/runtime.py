@@ -110,7 +110,7 @@ _sigs = {
     "kb_ipc_mem_export": (C.c_int, [_U, C.POINTER(C.c_uint8)]),
     "kb_ipc_mem_import": (C.c_int, [C.c_int32, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64)]),
     "kb_ipc_mem_close": (C.c_int, [_U]),
-    "kb_kv_append": (C.c_int, [_P, C.c_int32, _U, _U, _U, _U, C.c_int32, _S]),
+    "kb_kv_append": (C.c_int, [_P, C.c_int32, _U, _U, _U, _U, C.c_int32, C.c_int64, _S]),
     "kb_decode_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "kb_paged_decode": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, C.c_int32, C.c_int32,
                                   C.c_float, _U, _U, C.c_int32, C.c_int32, _S]),
@@ -509,9 +509,14 @@ def copy_bytes(dst_ptr: int, src_ptr: int, nbytes: int, stream=None) -> None:
 # -- N8 attention -------------------------------------------------------------
 
 def kv_append(pool: DevicePool, layer: int, k, v, slots, pos, stream=None) -> None:
-    """k, v: [ntok, n_kv_heads, 128] bf16; slots/pos: int32 [ntok] (device)."""
+    """k, v: [ntok, n_kv_heads, 128] bf16, rows contiguous or strided views of
+    a wider row (e.g. the K / V blocks of a fused QKV output); slots/pos:
+    int32 [ntok] (device)."""
+    if k.stride()[1:] != (128, 1) or v.stride()[1:] != (128, 1) or k.stride(0) != v.stride(0):
+        k, v = k.contiguous(), v.contiguous()
     _check(_lib.kb_kv_append(pool.h, layer, k.data_ptr(), v.data_ptr(), slots.data_ptr(),
-                             pos.data_ptr(), k.shape[0], _stream(stream)), launches=1)
+                             pos.data_ptr(), k.shape[0], k.stride(0), _stream(stream)),
+           launches=1)
 
 
 def decode_workspace_bytes(nseq: int, n_q_heads: int, max_splits: int) -> int:

@@ -164,24 +164,23 @@ class StageRunner:
             runtime.add_rmsnorm(x, pending, w.n1, h)
             qkv = h @ w.wqkv
             q = qkv[:, :Hq * d].reshape(n, Hq, d)
-            k = qkv[:, Hq * d:(Hq + Hkv) * d].reshape(n, Hkv, d).contiguous()
-            v = qkv[:, (Hq + Hkv) * d:].reshape(n, Hkv, d).contiguous()
+            # K / V straight out of the fused projection (strided rows)
+            k = qkv[:, Hq * d:(Hq + Hkv) * d].view(n, Hkv, d)
+            v = qkv[:, (Hq + Hkv) * d:].view(n, Hkv, d)
             runtime.kv_append(self.pool, l, k, v, batch["slots"], batch["pos"])
+            q = q.contiguous()
             o = torch.empty((n, Hq, d), dtype=x.dtype, device=x.device)
+            # rows are ordered prefill chunks first, then decode tokens
+            # (_batch), so each kind is a contiguous row range
+            npr = batch["n_prefill_rows"]
             if batch["np"]:
-                qp = q.index_select(0, batch["p_rows"]).contiguous()
-                op = torch.empty_like(qp)
-                runtime.paged_prefill(self.pool, l, qp, batch["p_slots"], batch["p_off"],
-                                      batch["p_len"], batch["p_prefix"], batch["p_max"], op,
+                runtime.paged_prefill(self.pool, l, q[:npr], batch["p_slots"], batch["p_off"],
+                                      batch["p_len"], batch["p_prefix"], batch["p_max"], o[:npr],
                                       self.scale, max_kv_len=batch.get("p_kv_max"))
-                o.index_copy_(0, batch["p_rows"], op)
             if batch["nd"]:
-                qd = q.index_select(0, batch["d_rows"]).contiguous()
-                od = torch.empty_like(qd)
-                runtime.paged_decode(self.pool, l, qd, batch["d_slots"], batch["d_ctx"],
-                                     batch["d_max"], od, self.ws, self.scale,
+                runtime.paged_decode(self.pool, l, q[npr:], batch["d_slots"], batch["d_ctx"],
+                                     batch["d_max"], o[npr:], self.ws, self.scale,
                                      max_splits=self.max_splits, reuse_plan=l > lo)
-                o.index_copy_(0, batch["d_rows"], od)
             runtime.add_rmsnorm(x, o.reshape(n, Hq * d) @ w.wo, w.n2, h)  # residual + norm 2
             gu = h @ w.wgu
             act = torch.empty((n, F), dtype=x.dtype, device=x.device)
@@ -372,7 +371,12 @@ class DeviceEngine(Engine):
         d_rows, d_slots, d_ctx = [], [], []
         last_rows = []  # rows that produce a token: decodes, last row of each prefill chunk
         row = 0
-        for ch in mb.chunks:
+        # prefill chunks first, then decode tokens: each kind is one
+        # contiguous row range for the attention kernels (row order is free:
+        # every row's output depends only on its own request)
+        ordered = [ch for ch in mb.chunks if not ch.decode] + [ch for ch in mb.chunks if ch.decode]
+        n_prefill_rows = sum(ch.token_count for ch in mb.chunks if not ch.decode)
+        for ch in ordered:
             slot = self.slots[iid].of[ch.rid]
             if ch.decode:
                 ctx = ch.prefix_len  # context incl. the token being decoded
@@ -396,7 +400,7 @@ class DeviceEngine(Engine):
                 last_rows.append(row - 1)
         i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
         i64 = lambda xs: torch.tensor(xs, dtype=torch.int64, device=dev)  # noqa: E731
-        return {"n": row, "slots": i32(slots), "pos": i32(pos),
+        return {"n": row, "slots": i32(slots), "pos": i32(pos), "n_prefill_rows": n_prefill_rows,
                 "np": len(p_slots), "p_rows": i64(p_rows), "p_slots": i32(p_slots),
                 "p_off": i32(p_off), "p_len": i32(p_len), "p_prefix": i32(p_prefix),
                 "p_max": max(p_len) if p_len else 0,
