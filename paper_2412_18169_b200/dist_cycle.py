@@ -421,7 +421,7 @@ class DistCycle:
             sl = [self.slots[self.me].of[r] for r in mb]
             ctx = [self.tokens[r] for r in mb]
             return {"n": len(mb), "slots": i32(sl), "pos": i32([c - 1 for c in ctx]),
-                    "np": 0, "nd": len(mb),
+                    "np": 0, "nd": len(mb), "n_prefill_rows": 0,
                     "d_rows": torch.arange(len(mb), dtype=torch.int64, device=dev),
                     "d_slots": i32(sl), "d_ctx": i32(ctx), "d_max": max(ctx)}
         batches = [batch(mb) for mb in mbs]

@@ -172,7 +172,7 @@ class StageRunner:
             o = torch.empty((n, Hq, d), dtype=x.dtype, device=x.device)
             # rows are ordered prefill chunks first, then decode tokens
             # (_batch), so each kind is a contiguous row range
-            npr = batch["n_prefill_rows"]
+            npr = batch.get("n_prefill_rows", 0)
             if batch["np"]:
                 runtime.paged_prefill(self.pool, l, q[:npr], batch["p_slots"], batch["p_off"],
                                       batch["p_len"], batch["p_prefix"], batch["p_max"], o[:npr],

@@ -199,3 +199,20 @@ def test_four_rank_pp4_cycle_bit_exact(shape_name, kv_budget, chunk, input_mean)
     L = SHAPES_L[shape_name]
     slab = SLAB[shape_name]
     assert all(res[r]["param"] == (L - L // 4) * slab for r in range(4))
+
+
+def test_eight_rank_pp2_cycle_bit_exact():
+    """configs[2] with its real replica count: eight Llama-3-8B replicas on
+    eight ranks (sharing the test box's GPU) merge into four PP-2 groups;
+    every group's exchange / restore / consolidation runs concurrently
+    through peer views, and the merged groups decode as cross-rank
+    pipelines with bit-exact activation hand-offs."""
+    res = _spawn(_cycle_worker, 8, "llama3_8b", 1 << 30, 16 << 20, 1660, 2)
+    for r in range(8):
+        d = res[r]
+        assert d["parity_fail"] == 0 and d["groups"] == [2, 2, 2, 2]
+        assert d["residents"] > 0 and d["kv"] > 0 and d["param"] > 0 and d["cons"] > 0
+        assert d["peer"] == d["pulled"]
+        assert d["param"] == 16 * SLAB["llama3_8b"]
+    pipe = res[0]["pipe"]
+    assert pipe["groups"] == 4 and pipe["handoff_bit_exact"]
