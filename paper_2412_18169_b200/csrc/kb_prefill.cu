@@ -456,15 +456,13 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       // fp16, kb_append.cu), written over S: the 64 keys of S half hh land in
       // P columns [32hh, 32hh + 32) -- columns whose S values were consumed.
       float2 rs2[4] = {};  // four partial sums: no 64-long dependent add chain
-      float xm4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // fast path: max of x
       const bool live = m_ref != -INFINITY;
       const float2 sc2 = make_float2(scale_log2, scale_log2);
       float2 nm2 = make_float2(-m_ref, -m_ref);
       // one straight-line body per case: unmasked tiles carry no selects
-      auto p_half = [&](auto masked, auto half, auto track, uint32_t (&w)[32]) {
+      auto p_half = [&](auto masked, auto half, uint32_t (&w)[32]) {
         constexpr bool kMasked = decltype(masked)::value;
         constexpr int hh = decltype(half)::value;
-        constexpr bool kTrack = decltype(track)::value;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int col = 2 * i;  // 0..63 within the half
@@ -483,21 +481,17 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
             const bool ok0 = row_ok && key <= qpos && live, ok1 = row_ok && key + 1 <= qpos && live;
             v.x = ok0 ? v.x : 0.f;
             v.y = ok1 ? v.y : 0.f;
-            if (kTrack)
-              xm4[i & 3] = fmaxf(xm4[i & 3], fmaxf(ok0 ? xv.x : -INFINITY, ok1 ? xv.y : -INFINITY));
-          } else if (kTrack) {
-            xm4[i & 3] = fmaxf(xm4[i & 3], fmaxf(xv.x, xv.y));
           }
           rs2[i & 3] = fadd2(rs2[i & 3], v);
           const __half2 hp = __floats2half2_rn(v.x, v.y);
           w[i] = *reinterpret_cast<const uint32_t*>(&hp);
         }
       };
-      auto store_half = [&](auto half, auto track) {
+      auto store_half = [&](auto half) {
         constexpr int hh = decltype(half)::value;
         uint32_t w[32];
-        if (full_tile) p_half(std::false_type{}, half, track, w);
-        else p_half(std::true_type{}, half, track, w);
+        if (full_tile) p_half(std::false_type{}, half, w);
+        else p_half(std::true_type{}, half, w);
         tmem_st_32x32b_x32(s_addr + 32 * hh, w);
       };
       auto take_rs = [&]() {
@@ -507,12 +501,6 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         for (int k = 0; k < 4; ++k) rs2[k] = make_float2(0.f, 0.f);
         return r;
       };
-      auto take_xmax = [&]() {
-        const float r = fmaxf(fmaxf(xm4[0], xm4[1]), fmaxf(xm4[2], xm4[3]));
-#pragma unroll
-        for (int k = 0; k < 4; ++k) xm4[k] = -INFINITY;
-        return r;
-      };
       auto publish = [&](uint64_t* bar) {
         tmem_st_wait();
         tc_fence_before();
@@ -520,59 +508,71 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       };
       using H0 = std::integral_constant<int, 0>;
       using H1 = std::integral_constant<int, 1>;
-      // keys 0-63
-      if (fast) {
-        store_half(H0{}, std::true_type{});
-        const float xmax = take_xmax();
-        const bool need = xmax > kRescaleLog2;
-        if (__any_sync(0xffffffffu, need)) {  // rare: the row max grew by > 2^8
-          const float alpha = need ? exp2f(-xmax) : 1.f;  // 2^(m_ref - (m_ref + xmax))
-          rescale_o(alpha);
-          if (need) {
-            l_run *= alpha;
-            m_ref += xmax;
+      // max of x = s*scale - m_ref over one half's valid columns (registers)
+      auto half_xmax = [&](auto half) {
+        constexpr int hh = decltype(half)::value;
+        float m = -INFINITY;
+#pragma unroll
+        for (int c = 2 * hh; c < 2 * hh + 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const bool ok = full_tile || (row_ok && (kbase + c * 32 + i) <= qpos);
+            m = fmaxf(m, ok ? __uint_as_float(sr[c][i]) : -INFINITY);
           }
-          nm2 = make_float2(-m_ref, -m_ref);
-          take_rs();
-          store_half(H0{}, std::false_type{});  // P again with the new reference
+        return m * scale_log2 - m_ref;
+      };
+      // Fast path overflow guard: a half's row sum above 2^14 means some P
+      // may have left the lazily-rescaled range (and fp16's, at 2^16): take
+      // the real max then, rescale, and recompute.  No per-element max
+      // tracking; the comparison also catches inf / NaN sums.
+      constexpr float kSumBound = 16384.f;
+      // keys 0-63
+      store_half(H0{});
+      float rs = take_rs();
+      if (fast && __any_sync(0xffffffffu, !(rs <= kSumBound))) {  // rare
+        const float xmax = half_xmax(H0{});
+        const bool need = !(rs <= kSumBound);
+        const float alpha = need ? exp2f(-xmax) : 1.f;  // 2^(m_ref - (m_ref + xmax))
+        rescale_o(alpha);
+        if (need) {
+          l_run *= alpha;
+          m_ref += xmax;
         }
-      } else {
-        store_half(H0{}, std::false_type{});
+        nm2 = make_float2(-m_ref, -m_ref);
+        store_half(H0{});  // P again with the new reference
+        rs = take_rs();
       }
-      l_run += take_rs();
+      l_run += rs;
       publish(&misc->p_lo[t]);
       // keys 64-127 (the P.V of keys 0-63 may already be running)
-      if (fast) {
-        store_half(H1{}, std::true_type{});
-        const float xmax = take_xmax();
-        const bool need = xmax > kRescaleLog2;
-        if (__any_sync(0xffffffffu, need)) {
-          // rare: O already holds this tile's first-half P.V under the old
-          // reference -- let it land, then rescale everything so far
-          mbar_wait(&misc->pv_lo[t], j & 1);
-          tc_fence_after();
-          const float alpha = need ? exp2f(-xmax) : 1.f;
+      store_half(H1{});
+      rs = take_rs();
+      if (fast && __any_sync(0xffffffffu, !(rs <= kSumBound))) {
+        // rare: O already holds this tile's first-half P.V under the old
+        // reference -- let it land, then rescale everything so far
+        const float xmax = half_xmax(H1{});
+        const bool need = !(rs <= kSumBound);
+        mbar_wait(&misc->pv_lo[t], j & 1);
+        tc_fence_after();
+        const float alpha = need ? exp2f(-xmax) : 1.f;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float part[32];
-            tmem_ld_32x32b_x32(o_addr + c * 32, part);
-            uint32_t w[32];
+        for (int c = 0; c < 4; ++c) {
+          float part[32];
+          tmem_ld_32x32b_x32(o_addr + c * 32, part);
+          uint32_t w[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(part[i] * alpha);
-            tmem_st_32x32b_x32(o_addr + c * 32, w);
-          }
-          if (need) {
-            l_run *= alpha;
-            m_ref += xmax;
-          }
-          nm2 = make_float2(-m_ref, -m_ref);
-          take_rs();
-          store_half(H1{}, std::false_type{});
+          for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(part[i] * alpha);
+          tmem_st_32x32b_x32(o_addr + c * 32, w);
         }
-      } else {
-        store_half(H1{}, std::false_type{});
+        if (need) {
+          l_run *= alpha;
+          m_ref += xmax;
+        }
+        nm2 = make_float2(-m_ref, -m_ref);
+        store_half(H1{});
+        rs = take_rs();
       }
-      l_run += take_rs();
+      l_run += rs;
 #ifdef KB_PF_TIMING
       t_c += clock64();
 #endif

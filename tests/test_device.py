@@ -272,6 +272,41 @@ def test_swap_pages_round_trip_bit_exact(rt):
     pool.close()
 
 
+@pytest.mark.parametrize("kv_splits", [1, 2])
+def test_paged_prefill_rescale_paths(rt, kv_splits):
+    """Keys whose scores jump far above the running row max, in the first
+    and in the second 64-key half of later tiles: the prefill takes its
+    rare rescale paths (O, l rescaled; P recomputed; for the second half
+    after the first half's P.V has landed) and still matches the oracle."""
+    from paper_2412_18169_b200 import runtime
+    shape = ATTN_SHAPES[0]
+    model = shape.spec()
+    pool = rt.create_pool(0, model, model.param_bytes + 64 * MIB, shape)
+    gen = torch.Generator().manual_seed(31)
+    hkv, hq, B = shape.n_kv_heads, shape.n_q_heads, shape.block_tokens
+    pre, c = 640, 256
+    n = pre + c
+    assert pool.grow([(0, 0, 1, (n + B - 1) // B)])
+    q = rand_bf16((c, hq, 128), gen)
+    k = rand_bf16((n, hkv, 128), gen)
+    v = rand_bf16((n, hkv, 128), gen)
+    qdir = q.float().mean(dim=(0, 1))
+    qdir = qdir / qdir.norm()
+    for pos, gain in ((150, 40.0), (300, 80.0), (420, 120.0), (700, 160.0)):
+        # 300 and 700 sit in the second half of their 128-key tiles
+        k[pos, :, :] = (qdir * gain).to(torch.bfloat16)
+    append(pool, 0, k, v, 0, 0)
+    out = torch.zeros((c, hq, 128), dtype=torch.bfloat16, device="cuda")
+    dev = lambda xs: torch.tensor(xs, dtype=torch.int32, device="cuda")  # noqa: E731
+    runtime.paged_prefill(pool, 0, q.cuda(), dev([0]), dev([0]), dev([c]), dev([pre]), c, out,
+                          128 ** -0.5, kv_splits=kv_splits)
+    torch.cuda.synchronize()
+    want = prefill_ref(q.float().numpy(), k.float().numpy(), v.float().numpy(), pre, 128 ** -0.5)
+    ma, mr = check_close(out.float().cpu().numpy(), bf16_to_f32(f32_to_bf16(want)))
+    assert ma <= 2e-2 and mr <= 1e-3, (kv_splits, ma, mr)
+    pool.close()
+
+
 def test_baseline_moves_through_the_transfer_engine(rt):
     """The baselines' whole-request KV moves as the engine issues them
     (engine.py:906-1047): swap out to HOST, swap back in on other pages,
