@@ -14,8 +14,12 @@
 namespace kb {
 
 constexpr int kPlanThreads = 1024;
+constexpr int kMaxLayers = 256;  // per-layer work-item counters in the workspace
 constexpr int kLenBuckets = 1024;
-constexpr int kItemsPerCta = 4;  // target work items per persistent CTA
+#ifndef KB_DEC_ITEMS_PER_CTA
+#define KB_DEC_ITEMS_PER_CTA 2  // swept 1-8 on B200 with dynamic fetching: 1-2 best
+#endif
+constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per persistent CTA
 
 // Split-KV combine: one CTA per (sequence, q head), thread = head_dim lane.
 __global__ void decode_combine_kernel(const float* __restrict__ part_o,
@@ -47,13 +51,14 @@ __global__ void __launch_bounds__(kPlanThreads)
 decode_plan_kernel(const int32_t* __restrict__ ctx, int nseq, int Hkv, int Hq, int max_splits,
                    int grid_ctas, int min_tiles, int32_t* __restrict__ nsplit_of,
                    DecodeItem* __restrict__ items, int32_t* __restrict__ n_items,
-                   float* __restrict__ part_ml) {
+                   float* __restrict__ part_ml, int32_t* __restrict__ item_counter) {
   __shared__ int hist[kLenBuckets];
   __shared__ int cursor[kLenBuckets];
   __shared__ unsigned long long total_tiles;
   __shared__ int T;
   const int tid = threadIdx.x;
   if (tid == 0) total_tiles = 0;
+  for (int i = tid; i < kMaxLayers; i += blockDim.x) item_counter[i] = 0;
   for (int b = tid; b < kLenBuckets; b += blockDim.x) hist[b] = 0;
   __syncthreads();
   unsigned long long local = 0;
@@ -119,7 +124,7 @@ extern "C" int64_t kb_decode_workspace_bytes(int32_t nseq, int32_t n_q_heads, in
   const int64_t sh = (int64_t)nseq * n_q_heads * max_splits;
   // items: at most nseq * n_kv_heads * max_splits <= sh
   return ws_part_o(sh) + ws_part_ml(sh) + round_up((int64_t)nseq * 4, 256) +
-         round_up(sh * (int64_t)sizeof(DecodeItem), 256) + 256;
+         round_up(sh * (int64_t)sizeof(DecodeItem), 256) + 256 + kMaxLayers * 4;
 }
 
 extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uint64_t q,
@@ -132,7 +137,7 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   if (p->m.head_dim != 128) return fail(KB_EINVAL, "head_dim must be 128");
   if (n_q_heads % Hkv || n_q_heads / Hkv > 8) return fail(KB_EINVAL, "GQA group must be <= 8");
   if (B != 64 && B != 128) return fail(KB_EINVAL, "block_tokens must be 64 or 128");
-  if (layer < 0 || layer >= p->m.num_layers) return fail(KB_EINVAL, "bad layer");
+  if (layer < 0 || layer >= p->m.num_layers || layer >= kMaxLayers) return fail(KB_EINVAL, "bad layer");
   if (max_splits < 1 || max_splits > 64) return fail(KB_EINVAL, "max_splits out of range");
   if (nseq <= 0) return KB_OK;
   (void)max_ctx;
@@ -147,6 +152,7 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
                                                      round_up((int64_t)nseq * 4, 256));
   int32_t* n_items = reinterpret_cast<int32_t*>(
       reinterpret_cast<char*>(items) + round_up(sh * (int64_t)sizeof(DecodeItem), 256));
+  int32_t* item_counter = n_items + 64;  // kMaxLayers ints after the 256-byte n_items slot
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device);
   const int grid = dev_sms;  // persistent: one CTA per SM (the kernel needs ~210 KB smem)
@@ -155,11 +161,12 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   if (!(flags & KB_DECODE_REUSE_PLAN)) {
     decode_plan_kernel<<<1, kPlanThreads, 0, st>>>(reinterpret_cast<const int32_t*>(ctx_lens),
                                                    nseq, Hkv, n_q_heads, max_splits, grid, 2,
-                                                   nsplit, items, n_items, part_ml);
+                                                   nsplit, items, n_items, part_ml,
+                                                   item_counter);
     KB_LAUNCH_CHECK();
   }
   rc = launch_decode_tc(p, layer, n_q_heads, q, slots, ctx_lens, grid, scale, part_o, part_ml,
-                            items, n_items, nsplit, out, max_splits, st);
+                            items, n_items, item_counter, nsplit, out, max_splits, st);
   if (rc) return rc;
   decode_combine_kernel<<<nseq * n_q_heads, 128, 0, st>>>(part_o, part_ml, nsplit,
                                                           reinterpret_cast<__nv_bfloat16*>(out),

@@ -39,6 +39,7 @@ constexpr int kQBytes = 4096;            // 16 rows x 128 d bf16, SW128 K-major
 constexpr int kPBytes = 4096;            // 16 rows x 128 tok bf16, SW128 K-major
 constexpr int kDecSmem = kDecStages * kStageBytes + 2 * kQBytes + 2 * kPBytes + 1024 + 1024;
 constexpr uint32_t kDecTmemCols = 64;    // S0 S1 O0 O1, 16 columns each
+constexpr int kRing = 16;                // dynamically fetched work items in flight per CTA
 
 struct DecodeItem {
   int32_t seq, h, split, t_beg, nt, _pad[3];
@@ -51,6 +52,9 @@ struct DecodeMisc {
   uint64_t o_full[2];
   uint64_t p_full[2];
   uint64_t q_full[2];
+  uint64_t ring_full[kRing];   // item index published by the producer
+  uint64_t ring_empty[kRing];  // MMA warp + softmax done with the item
+  int32_t ring_item[kRing];    // index into the sorted item list, -1 = no more work
   uint32_t tmem_base;
   uint32_t _pad;
   float red[2][4][8];
@@ -62,25 +66,19 @@ __global__ void __launch_bounds__(kDecThreads, 1)
 decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* __restrict__ q,
                  const int32_t* __restrict__ bt, const int32_t* __restrict__ slots,
                  const int32_t* __restrict__ ctx_lens, const DecodeItem* __restrict__ items,
-                 const int32_t* __restrict__ n_items_ptr, const int32_t* __restrict__ nsplit_of,
+                 const int32_t* __restrict__ n_items_ptr, int32_t* __restrict__ item_counter,
+                 const int32_t* __restrict__ nsplit_of,
                  __nv_bfloat16* __restrict__ out, float* __restrict__ part_o,
                  float* __restrict__ part_ml, int Hkv, int G, int Hq, int L, int maxp, int layer,
                  int max_splits, float scale_log2) {
   using namespace sm100;
   constexpr int kPPT = kTileTok / kB;  // pages per tile
-  // Items are sorted longest first; CTA c takes one item per round in
-  // boustrophedon order (round r: c, or NG-1-c when r is odd), so a CTA
-  // that drew a long item in one round draws a short one in the next
-  // (ncu r1d: SMs were idle 13% of the kernel with plain striding).
+  // Work items are sorted longest first and handed out dynamically: the
+  // producer warp of each persistent CTA takes the next index from a
+  // per-layer global counter (a greedy longest-processing-time schedule, so
+  // the CTAs finish within one short item of each other) and publishes it
+  // to the MMA and softmax warps through a small shared-memory ring.
   const int n_items = *n_items_ptr;
-  const int NG = (int)gridDim.x, c = (int)blockIdx.x;
-  const int full_rounds = n_items / NG, rem = n_items % NG;
-  const bool in_last = (full_rounds & 1) ? (NG - 1 - c < rem) : (c < rem);
-  const int n_mine = full_rounds + (in_last ? 1 : 0);
-  if (n_mine == 0) return;
-  auto item_of = [&](int r) {
-    return items[(int64_t)r * NG + ((r & 1) ? NG - 1 - c : c)];
-  };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   extern __shared__ uint8_t smem_raw[];
@@ -102,6 +100,10 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         mbar_init(&misc->q_full[b], 128);
         mbar_init(&misc->p_full[b], 128);
       }
+      for (int r = 0; r < kRing; ++r) {
+        mbar_init(&misc->ring_full[r], 1);
+        mbar_init(&misc->ring_empty[r], 2);
+      }
       fence_barrier_init();
     }
     __syncwarp();
@@ -112,13 +114,44 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = misc->tmem_base;
+  // item r of this CTA (every role reads the ring in the same order)
+  auto get_item = [&](int r, DecodeItem& it) -> bool {
+    const int slot = r % kRing;
+    mbar_wait(&misc->ring_full[slot], (r / kRing) & 1);
+    const int idx = *reinterpret_cast<volatile int32_t*>(&misc->ring_item[slot]);
+    if (idx < 0) return false;
+    it = items[idx];
+    return true;
+  };
 
   if (warp == 4) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
+      int published = 0;
+      bool exhausted = false;
+      // fetch the next item index and publish it; two items ahead of the
+      // loads, so the softmax can stage the next item's Q early
+      auto publish = [&]() {
+        if (exhausted) return;
+        const int r = published++;
+        const int slot = r % kRing;
+        if (r >= kRing) mbar_wait(&misc->ring_empty[slot], ((r / kRing) - 1) & 1);
+        int idx = atomicAdd(item_counter + layer, 1);
+        if (idx >= n_items) {
+          // the last CTA to run dry re-arms the counter (a reused plan)
+          if (idx == n_items + (int)gridDim.x - 1) item_counter[layer] = 0;
+          idx = -1;
+          exhausted = true;
+        }
+        misc->ring_item[slot] = idx;
+        mbar_arrive(&misc->ring_full[slot]);
+      };
+      publish();
+      publish();
       int j = 0;  // global tile counter of this CTA
-      for (int r = 0; r < n_mine; ++r) {
-        const DecodeItem it = item_of(r);
+      for (int r = 0;; ++r) {
+        DecodeItem it;
+        if (!get_item(r, it)) break;
         const int ctx = ctx_lens[it.seq];
         const int32_t* bt_row = bt + ((int64_t)slots[it.seq] * L + layer) * maxp;
         for (int t = 0; t < it.nt; ++t, ++j) {
@@ -148,6 +181,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
             tma_load_2d(sV + kHalfBytes + off, &tmap, 64, rv, &misc->full[stage]);
           }
         }
+        publish();
       }
     }
   } else if (warp == 5) {
@@ -158,14 +192,15 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     const uint32_t p_base = smem_u32(sP);
     // QK cursor runs one tile ahead of the PV cursor, across item borders
     int qr = 0, qt = 0, qj = 0;
-    DecodeItem qit = item_of(0);
+    DecodeItem qit;
+    bool qvalid = get_item(0, qit);
     auto issue_next_qk = [&]() -> bool {
-      while (qr < n_mine && qt >= qit.nt) {
+      while (qvalid && qt >= qit.nt) {
         ++qr;
         qt = 0;
-        if (qr < n_mine) qit = item_of(qr);
+        qvalid = get_item(qr, qit);
       }
-      if (qr >= n_mine) return false;
+      if (!qvalid) return false;
       if (qt == 0) mbar_wait(&misc->q_full[qr & 1], (qr >> 1) & 1);
       const int stage = qj % kDecStages;
       mbar_wait(&misc->full[stage], (qj / kDecStages) & 1);
@@ -184,8 +219,10 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     };
     issue_next_qk();
     int j = 0;
-    for (int r = 0; r < n_mine; ++r) {
-      const int nt = item_of(r).nt;
+    for (int r = 0;; ++r) {
+      DecodeItem cur;
+      if (!get_item(r, cur)) break;
+      const int nt = cur.nt;
       for (int t = 0; t < nt; ++t, ++j) {
         issue_next_qk();
         mbar_wait(&misc->p_full[j & 1], (j >> 1) & 1);
@@ -202,11 +239,12 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         }
         __syncwarp();
       }
+      if (lane == 0) mbar_arrive(&misc->ring_empty[r % kRing]);  // done with item r
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------ softmax / epilogue (tid < 128)
-    auto write_q = [&](int r) {
-      const DecodeItem it = item_of(r);
+    auto write_q = [&](int r, const DecodeItem& it) {
       uint8_t* dst = sQ + (r & 1) * kQBytes;
       for (int c = tid; c < 16 * 16; c += 128) {
         const int g = c >> 4, chunk = c & 15;  // 16-byte chunk of 8 d values
@@ -222,14 +260,15 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     // both P buffers start zero: rows >= 8 (GQA padding) are never written
     for (int c = tid; c < 2 * kPBytes / 16; c += 128)
       reinterpret_cast<int4*>(sP)[c] = make_int4(0, 0, 0, 0);
-    write_q(0);
-    if (n_mine > 1) write_q(1);
+    DecodeItem it, nxt;
+    bool have = get_item(0, it);
+    if (have) write_q(0, it);
+    if (have && get_item(1, nxt)) write_q(1, nxt);
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     int j = 0;
-    for (int r = 0; r < n_mine; ++r) {
+    for (int r = 0; have; ++r) {
       // Q of item r+1 goes into the buffer item r-1 used (its QKs are done)
-      if (r >= 1 && r + 1 < n_mine) write_q(r + 1);
-      const DecodeItem it = item_of(r);
+      if (r >= 1 && get_item(r + 1, nxt)) write_q(r + 1, nxt);
       const int ctx = ctx_lens[it.seq];
       float m_run[8], l_part[8], o_acc[8], alpha_hist[2][8];
 #pragma unroll
@@ -345,6 +384,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         }
       }
       named_bar_sync(1, 128);  // lred is reused by the next item
+      if (tid == 0) mbar_arrive(&misc->ring_empty[r % kRing]);  // done with item r
+      have = get_item(r + 1, it);
     }
   }
   tc_fence_before();
@@ -358,7 +399,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
 inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t slots,
                             uint64_t ctx_lens, int grid, float scale, float* part_o,
                             float* part_ml, const DecodeItem* items, const int32_t* n_items,
-                            const int32_t* nsplit, uint64_t out, int max_splits, cudaStream_t st) {
+                            int32_t* item_counter, const int32_t* nsplit, uint64_t out,
+                            int max_splits, cudaStream_t st) {
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
   const float scale_log2 = scale * 1.4426950408889634f;
   if (B == 64) {
@@ -371,7 +413,8 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
     decode_tc_kernel<64><<<grid, kDecThreads, kDecSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
-        items, n_items, nsplit, reinterpret_cast<__nv_bfloat16*>(out), part_o, part_ml, Hkv,
+        items, n_items, item_counter, nsplit, reinterpret_cast<__nv_bfloat16*>(out), part_o,
+        part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2);
   } else {
     static bool attr = false;
@@ -383,7 +426,8 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
     decode_tc_kernel<128><<<grid, kDecThreads, kDecSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
-        items, n_items, nsplit, reinterpret_cast<__nv_bfloat16*>(out), part_o, part_ml, Hkv,
+        items, n_items, item_counter, nsplit, reinterpret_cast<__nv_bfloat16*>(out), part_o,
+        part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2);
   }
   KB_LAUNCH_CHECK();
