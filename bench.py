@@ -516,9 +516,11 @@ def main():
 
     # configs[2] across GPUs: replica r on GPU r, PP-2 groups spanning GPU
     # pairs, every exchange / restore / consolidation byte pulled over NVLink
-    nvl = nvl4 = None
+    nvl = nvl4 = sweep_n = None
     if ws > 1:
         nvl = nvlink_measure(rt, shape, args)
+        from paper_2412_18169_b200.dist import nvlink_sweep  # config 5 across GPUs
+        sweep_n = nvlink_sweep(rt)
     if ws >= 4 and ws % 4 == 0:  # configs[3]: Qwen2.5-14B replicas into PP-4 groups
         nvl4 = nvlink_measure(rt, SHAPES["qwen25_14b"], args, pp=4)
 
@@ -571,6 +573,7 @@ def main():
             "p99_ttft": ttft,
             "nvlink_cycle": nvl,
             "nvlink_cycle_pp4": nvl4,
+            "nvlink_sweep": sweep_n,
             "parity": parity,
             "e2e": {"value": round(e_moved / e2e_s / 1e9, 1), "unit": "GB/s",
                     "h2d_bytes_per_step": tok.numel() * 4, "d2h_bytes_per_step": res.numel() * 4,

@@ -304,3 +304,52 @@ class ActChannel:
             self.shm.unlink()
         else:
             dist.barrier()
+
+
+def nvlink_sweep(rt, max_bytes: int = 2 << 30, iters: int = 5) -> dict:
+    """Config 5 across GPUs: every rank pulls contiguous byte ranges (64 KiB
+    to `max_bytes`, x4 steps) from its partner's (rank ^ 1) device buffer
+    through a CUDA-IPC mapping with the repo's copy kernel -- the transfer a
+    layer restore makes -- both directions at once.  Returns
+    [[bytes, GB/s per direction], ...] with the time max-reduced over ranks."""
+    import torch
+    import torch.distributed as dist
+    from .runtime import IpcBuffer, copy_bytes
+    rank, world = dist.get_rank(), dist.get_world_size()
+    peer = rank ^ 1
+    mine = IpcBuffer.allocate(rt.device, max_bytes)
+    mine.tensor().fill_(rank & 0xFF)
+    objs = [None] * world
+    dist.all_gather_object(objs, mine.export())
+    theirs = IpcBuffer.open(rt.device, objs[peer], max_bytes) if peer < world else None
+    dst = torch.empty(max_bytes, dtype=torch.uint8, device=f"cuda:{rt.device}")
+    st = torch.cuda.current_stream()
+    dev = f"cuda:{rt.device}" if dist.get_backend() == "nccl" else None
+    out = []
+    size = 64 << 10
+    while size <= max_bytes:
+        torch.cuda.synchronize(rt.device)
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if theirs is not None:
+            copy_bytes(dst.data_ptr(), theirs.ptr, size, stream=st)  # warm-up
+            a.record(st)
+            for _ in range(iters):
+                copy_bytes(dst.data_ptr(), theirs.ptr, size, stream=st)
+            b.record(st)
+            b.synchronize()
+            ms = a.elapsed_time(b) / iters
+        else:
+            ms = 0.0
+        ms = max_over_ranks(ms, device=dev)
+        out.append([size, round(size / (ms / 1e3) / 1e9, 1) if ms > 0 else None])
+        size *= 4
+    torch.cuda.synchronize(rt.device)
+    ok = bool((dst[:64] == (peer & 0xFF)).all().item()) if theirs is not None else True
+    dist.barrier()
+    if theirs is not None:
+        theirs.close()
+    dist.barrier()
+    mine.close()
+    return {"sizes_gbs": out, "bytes_checked": ok,
+            "unit": "GB/s per direction (each rank pulls from rank ^ 1 concurrently)"}
