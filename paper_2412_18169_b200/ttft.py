@@ -25,9 +25,14 @@ def burst_trace(duration_s: float = 20.0, base_rps: float = 1.0, burst_factor: f
                        duration_s * 3 / 4, input_mean, output_mean, "lognormal", 0.6, seed)
 
 
-def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None) -> dict:
+def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None, cost=None) -> dict:
+    """cost: CostCoefficients for the scheduler's planning (lookahead
+    microbatch formulation, exchange chunk sizing); stage times themselves
+    are always measured."""
     cfg = device_config(shape, instances=2, kv_bytes=kv_bytes)
     cfg.policy.kind = policy
+    if cost is not None:
+        cfg.cost = cost
     cfg.report.drain_s = 60.0
     t0 = time.perf_counter()
     eng = DeviceEngine(cfg, trace, runtimes=runtimes)
@@ -85,11 +90,18 @@ def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b",
     # warm-up: load every kernel / cuBLAS heuristic and walk one drop cycle
     # so the measured runs see steady-state stage times
     warm = burst_trace(duration_s=4.0, base_rps=4.0, input_mean=1660, output_mean=8, seed=11)
-    run_policy("kunserve", warm, shape, int(0.25 * (1 << 30)))
+    w, _ = run_policy("kunserve", warm, shape, int(0.25 * (1 << 30)))
+    # the scheduler plans with the cost model refit on the warm-up's measured
+    # B200 stage times (engine.py:389-397, 729-734)
+    fit = w.get("cost_fit")
+    cost = None
+    if fit:
+        from .costmodel import CostCoefficients
+        cost = CostCoefficients(alpha=fit["alpha"], beta=fit["beta"], gamma=fit["gamma"])
     res = {}
     samples_all = []
     for pol in policies:
-        r, samples = run_policy(pol, trace, shape, int(kv_gib * (1 << 30)))
+        r, samples = run_policy(pol, trace, shape, int(kv_gib * (1 << 30)), cost=cost)
         res[pol] = r
         samples_all += samples
     k, r = res["kunserve"], res["recompute"]
@@ -114,6 +126,9 @@ def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b",
                             if tpot_ratio else None,
                             "bounds": "ttft ratio >= 5, tpot ratio <= 1.35 "
                                       "(reference desk config; this is a different model/trace)"},
+            "planning_cost": None if cost is None else
+            {"alpha": cost.alpha, "beta": cost.beta, "gamma": cost.gamma,
+             "source": "refit on the warm-up run's measured stage times"},
             **{p: res[p] for p in policies},
             "trace": {"requests": len(trace), "input_mean": trace_kw.get("input_mean", 1660),
                       "output_mean": trace_kw.get("output_mean", 64), "burst": "4x",
