@@ -467,6 +467,11 @@ def main():
     pk_ms = sum(r.param_kernel_ms for r in reps)
     pbytes = sum(r.bytes_param for r in reps)
     achieved = 2 * pbytes / (pk_ms / 1e3) / 1e9 if pk_ms else 0.0
+    # the other big mover: KV page copies (exchange + consolidation bursts,
+    # their block-table grows included), also read + write HBM
+    kv_ms = sum(r.kv_kernel_ms for r in reps)
+    kv_bytes = sum(r.bytes_kv_exchange + r.bytes_kv_consolidate for r in reps)
+    kv_achieved = 2 * kv_bytes / (kv_ms / 1e3) / 1e9 if kv_ms else 0.0
 
     # paged decode in the merged state
     cyc.pause_merged = True
@@ -567,6 +572,11 @@ def main():
                          "traffic_algorithmic": 2 * pbytes // max(1, sum(r.param_launches for r in reps)),
                          "kernel": "copy_flat_kernel (peer slab pull; same-GPU replicas: "
                                    "read+write HBM)", "peak_source": peak_src},
+            "roofline_kv_pages": {"bound": "hbm", "achieved": round(kv_achieved, 1),
+                                  "peak": hbm_peak, "unit": "GB/s",
+                                  "frac": round(kv_achieved / hbm_peak, 4),
+                                  "kernel": "copy_pages_kernel bursts (grows included), "
+                                            "read+write HBM"},
             "paged_decode": dec,
             "paged_prefill": prefill,
             "copy_sweep": sweep,
