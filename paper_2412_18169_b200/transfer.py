@@ -111,6 +111,10 @@ class TransferEngine:
         lo, hi = torch.cuda.Stream.priority_range()
         self.bulk = torch.cuda.Stream(priority=lo)   # KV chunks + param shards, FIFO
         self.urgent = torch.cuda.Stream(priority=hi)  # activations
+        # block-table growth for the next burst runs here while the previous
+        # burst's copies stream on `bulk`; the pool's device ordering makes
+        # the copies into the new pages wait for it (kb::pool_enter)
+        self.meta = torch.cuda.Stream(priority=lo)
         self.flows: dict[tuple[int, int, int], KVFlow] = {}
         self.chunk_of: dict[int, tuple[tuple[int, int, int], int]] = {}
         self.param_off: dict[int, int] = {}
@@ -264,7 +268,7 @@ class TransferEngine:
                              fl.npages))
                     fl.grown = True
         for dst, reqs in grows.items():
-            if not self.pools[dst].grow(reqs, stream=stream):
+            if not self.pools[dst].grow(reqs, stream=self.meta):
                 raise runtime.DeviceError(f"instance {dst} out of KV pages for an exchange")
         pairs: dict[tuple[int, int], list] = {}
         runs: list = []
