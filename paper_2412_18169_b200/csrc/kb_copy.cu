@@ -286,7 +286,9 @@ extern "C" int kb_copy_pages_host(kb_pool* p, const kb_move* mv, void* host, int
   PoolView pv{p->d_bt, reinterpret_cast<uint8_t*>(p->kva), L, p->maxp};
   int rc = pool_enter(p, st);
   if (rc) return rc;
-  copy_pages_host_kernel<<<grid_for(total * pieces, 1, 148 * 4), kThreads, 0, st>>>(
+  // PCIe-bound: 16 CTAs keep ~0.5 MB in flight -- enough for the host link --
+  // and leave the other SMs to the compute the swap overlaps with
+  copy_pages_host_kernel<<<grid_for(total * pieces, 1, 16), kThreads, 0, st>>>(
       pv, static_cast<uint8_t*>(dhost), *mv, total, p->m.page_bytes, pieces, to_host);
   KB_LAUNCH_CHECK();
   return pool_leave(p, st);
