@@ -472,6 +472,80 @@ def test_paged_prefill_matches_oracle(rt, shape, kv_splits):
     pool.close()
 
 
+def test_attention_at_full_context_sampled_rows():
+    """BASELINE config 4's sizes: the last 2,048-token chunk of a 32k Qwen
+    prompt (prefix 30,720) and decodes at 32k context, with the split counts
+    the runtime picks and explicit ones.  The oracle is exact per row, so
+    sampled rows (tile borders, split borders, the causal diagonal's end)
+    are checked against it; every head of each sampled row."""
+    from paper_2412_18169_b200 import runtime
+    rt32 = runtime.Runtime(0, max_slots=4, max_pages_per_seq=520, slack_pages=64)
+    shape = ATTN_SHAPES[1]  # Qwen2.5-14B heads: 40 q / 8 kv
+    model = shape.spec()
+    pool = rt32.create_pool(0, model, model.param_bytes + 400 * MIB, shape)
+    gen = torch.Generator().manual_seed(32)
+    hkv, hq, B = shape.n_kv_heads, shape.n_q_heads, shape.block_tokens
+    n, c = 32768, 2048
+    pre = n - c
+    assert pool.grow([(0, 0, 1, n // B), (1, 0, 1, (n - 1 + B - 1) // B)])
+    k = rand_bf16((n, hkv, 128), gen)
+    v = rand_bf16((n, hkv, 128), gen)
+    append(pool, 0, k, v, 0, 0)
+    append(pool, 0, k[:n - 1], v[:n - 1], 1, 0)
+    kf, vf = k.float().numpy(), v.float().numpy()
+    scale = 128 ** -0.5
+    dev = lambda xs: torch.tensor(xs, dtype=torch.int32, device="cuda")  # noqa: E731
+    q = rand_bf16((c, hq, 128), gen)
+    rows = [0, 1, 63, 64, 127, 128, 129, 1000, 1023, 1024, 1535, 2046, 2047]
+    for kv_splits in (None, 1, 8):
+        out = torch.zeros((c, hq, 128), dtype=torch.bfloat16, device="cuda")
+        kw = {"max_kv_len": n} if kv_splits is None else {"kv_splits": kv_splits}
+        runtime.paged_prefill(pool, 0, q.cuda(), dev([0]), dev([0]), dev([c]), dev([pre]), c, out,
+                              scale, **kw)
+        torch.cuda.synchronize()
+        got = out.float().cpu().numpy()
+        for r in rows:
+            want = prefill_ref(q[r:r + 1].float().numpy(), kf[:pre + r + 1], vf[:pre + r + 1],
+                               pre + r, scale)
+            ma, mr = check_close(got[r:r + 1], bf16_to_f32(f32_to_bf16(want)))
+            assert ma <= 2e-2 and mr <= 1e-3, (kv_splits, r, ma, mr)
+    # decode: context 32,768 and 32,767 (a ragged last page)
+    qd = rand_bf16((2, hq, 128), gen)
+    lens = [n, n - 1]
+    for max_splits in (1, 16):
+        ws = torch.empty(runtime.decode_workspace_bytes(2, hq, max_splits), dtype=torch.uint8,
+                         device="cuda")
+        out = torch.empty((2, hq, 128), dtype=torch.bfloat16, device="cuda")
+        runtime.paged_decode(pool, 0, qd.cuda(), dev([0, 1]), dev(lens), n, out, ws, scale,
+                             max_splits=max_splits)
+        torch.cuda.synchronize()
+        got = out.float().cpu().numpy()
+        for i, ctx in enumerate(lens):
+            want = decode_ref(qd[i].float().numpy(), kf[:ctx], vf[:ctx], scale)
+            ma, mr = check_close(got[i], bf16_to_f32(f32_to_bf16(want)))
+            assert ma <= 2e-2 and mr <= 1e-3, (max_splits, ctx, ma, mr)
+    pool.close()
+
+
+def test_attention_empty_batches(rt):
+    """No prefill chunks / no decode sequences: the calls are no-ops that
+    leave the output untouched (the device engine issues them for
+    decode-only and prefill-only microbatches)."""
+    from paper_2412_18169_b200 import runtime
+    shape = ATTN_SHAPES[0]
+    model = shape.spec()
+    pool = rt.create_pool(0, model, model.param_bytes + 64 * MIB, shape)
+    e32 = torch.empty(0, dtype=torch.int32, device="cuda")
+    q = torch.empty((0, shape.n_q_heads, 128), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty_like(q)
+    ws = torch.empty(runtime.decode_workspace_bytes(1, shape.n_q_heads, 4), dtype=torch.uint8,
+                     device="cuda")
+    runtime.paged_decode(pool, 0, q, e32, e32, 0, out, ws, 1.0, max_splits=4)
+    runtime.paged_prefill(pool, 0, q, e32, e32, e32, e32, 0, out, 1.0)
+    torch.cuda.synchronize()
+    pool.close()
+
+
 def test_layer_elementwise_kernels_match_torch(rt):
     """kb_add_rmsnorm / kb_silu_mul (the device engine's stage execution)
     against a plain PyTorch fp32 reference of the same ops."""
