@@ -313,8 +313,9 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
     b.record(st)
     b.synchronize()
     ms = a.elapsed_time(b) / iters
-    # per member: one plan, then attention + combine per layer
-    launches = sum(1 + 2 * (hi - lo) for _, lo, hi, *_ in work)
+    # per member: one plan, then one attention launch per layer (the KV
+    # splits are merged inside it)
+    launches = sum(1 + (hi - lo) for _, lo, hi, *_ in work)
     gbs = algo_bytes / (ms / 1e3) / 1e9
     return {"value": round(nres / (ms / 1e3), 1), "unit": "tok/s",
             "tokens_per_step": nres, "ms_per_token_step": round(ms, 4),

@@ -6,8 +6,9 @@
 // (pkg/src/dropsim/costmodel.py:50-57).  Parity is against the fp32 CPU
 // restatement oracle/attention.py with max-abs <= 2e-2, mean-rel <= 1e-3.
 //
-// Three launches per layer: plan (work items), the persistent tcgen05
-// kernel (kb_decode_tc.cuh), and the split-KV combine.
+// One launch per layer: the persistent tcgen05 kernel (kb_decode_tc.cuh),
+// which also merges the KV splits; plus one plan launch (work items) per
+// decode step, reused by every layer.
 #include "kb_common.cuh"
 #include "kb_decode_tc.cuh"
 
@@ -21,28 +22,6 @@ constexpr int kLenBuckets = 1024;
 #endif
 constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per persistent CTA
 
-// Split-KV combine: one CTA per (sequence, q head), thread = head_dim lane.
-__global__ void decode_combine_kernel(const float* __restrict__ part_o,
-                                      const float* __restrict__ part_ml,
-                                      const int32_t* __restrict__ nsplit_of,
-                                      __nv_bfloat16* __restrict__ out, int Hq, int max_splits) {
-  const int sh = blockIdx.x;  // seq * Hq + head
-  const int seq = sh / Hq;
-  const int ns = nsplit_of[seq];
-  if (ns == 1) return;  // the attention kernel wrote this row directly
-  const float* ml = part_ml + (int64_t)sh * max_splits * 2;
-  float mstar = -INFINITY;
-  for (int s = 0; s < ns; ++s) mstar = fmaxf(mstar, ml[2 * s]);
-  float l = 0.f, o = 0.f;
-  for (int s = 0; s < ns; ++s) {
-    const float ms = ml[2 * s];
-    const float w = ms == -INFINITY ? 0.f : exp2f(ms - mstar);
-    l += w * ml[2 * s + 1];
-    o += w * part_o[((int64_t)sh * max_splits + s) * 128 + threadIdx.x];
-  }
-  out[(int64_t)sh * 128 + threadIdx.x] = __float2bfloat16(l > 0.f ? o / l : 0.f);
-}
-
 // Work items: sequence i is cut into s_i = clamp(ceil(tiles_i / T), 1,
 // max_splits) splits per kv head, T chosen so the items spread ~kItemsPerCta
 // per persistent CTA; items are bucket-sorted longest first.  Sequences with
@@ -51,7 +30,8 @@ __global__ void __launch_bounds__(kPlanThreads)
 decode_plan_kernel(const int32_t* __restrict__ ctx, int nseq, int Hkv, int Hq, int max_splits,
                    int grid_ctas, int min_tiles, int32_t* __restrict__ nsplit_of,
                    DecodeItem* __restrict__ items, int32_t* __restrict__ n_items,
-                   float* __restrict__ part_ml, int32_t* __restrict__ item_counter) {
+                   float* __restrict__ part_ml, int32_t* __restrict__ item_counter,
+                   int32_t* __restrict__ split_done) {
   __shared__ int hist[kLenBuckets];
   __shared__ int cursor[kLenBuckets];
   __shared__ unsigned long long total_tiles;
@@ -59,6 +39,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, int nseq, int Hkv, int Hq, i
   const int tid = threadIdx.x;
   if (tid == 0) total_tiles = 0;
   for (int i = tid; i < kMaxLayers; i += blockDim.x) item_counter[i] = 0;
+  for (int i = tid; i < nseq * Hkv; i += blockDim.x) split_done[i] = 0;
   for (int b = tid; b < kLenBuckets; b += blockDim.x) hist[b] = 0;
   __syncthreads();
   unsigned long long local = 0;
@@ -79,7 +60,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, int nseq, int Hkv, int Hq, i
   for (int i = tid; i < nseq; i += blockDim.x) {
     const int tiles = (ctx[i] + kTileTok - 1) / kTileTok;
     const int s = splits_of(tiles);
-    // no context: no item; the combine kernel writes a zero row (0 splits)
+    // no context: no item; the attention kernel writes a zero row (0 splits)
     nsplit_of[i] = tiles == 0 ? 0 : s;
     if (tiles == 0) continue;
     for (int k = 0; k < s; ++k) {
@@ -124,7 +105,8 @@ extern "C" int64_t kb_decode_workspace_bytes(int32_t nseq, int32_t n_q_heads, in
   const int64_t sh = (int64_t)nseq * n_q_heads * max_splits;
   // items: at most nseq * n_kv_heads * max_splits <= sh
   return ws_part_o(sh) + ws_part_ml(sh) + round_up((int64_t)nseq * 4, 256) +
-         round_up(sh * (int64_t)sizeof(DecodeItem), 256) + 256 + kMaxLayers * 4;
+         round_up(sh * (int64_t)sizeof(DecodeItem), 256) + 256 + kMaxLayers * 4 +
+         (int64_t)nseq * n_q_heads * 4;  // per-(sequence, kv head) split counters
 }
 
 extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uint64_t q,
@@ -153,6 +135,7 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   int32_t* n_items = reinterpret_cast<int32_t*>(
       reinterpret_cast<char*>(items) + round_up(sh * (int64_t)sizeof(DecodeItem), 256));
   int32_t* item_counter = n_items + 64;  // kMaxLayers ints after the 256-byte n_items slot
+  int32_t* split_done = item_counter + kMaxLayers;  // nseq * Hkv finished-split counters
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, p->device);
   const int grid = dev_sms;  // persistent: one CTA per SM (the kernel needs ~210 KB smem)
@@ -162,15 +145,12 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
     decode_plan_kernel<<<1, kPlanThreads, 0, st>>>(reinterpret_cast<const int32_t*>(ctx_lens),
                                                    nseq, Hkv, n_q_heads, max_splits, grid, 2,
                                                    nsplit, items, n_items, part_ml,
-                                                   item_counter);
+                                                   item_counter, split_done);
     KB_LAUNCH_CHECK();
   }
   rc = launch_decode_tc(p, layer, n_q_heads, q, slots, ctx_lens, grid, scale, part_o, part_ml,
-                            items, n_items, item_counter, nsplit, out, max_splits, st);
+                        items, n_items, item_counter, nsplit, split_done, nseq, out, max_splits,
+                        st);
   if (rc) return rc;
-  decode_combine_kernel<<<nseq * n_q_heads, 128, 0, st>>>(part_o, part_ml, nsplit,
-                                                          reinterpret_cast<__nv_bfloat16*>(out),
-                                                          n_q_heads, max_splits);
-  KB_LAUNCH_CHECK();
   return pool_leave(p, st);
 }

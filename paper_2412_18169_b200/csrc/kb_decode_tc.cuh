@@ -56,7 +56,7 @@ struct DecodeMisc {
   uint64_t ring_empty[kRing];  // MMA warp + softmax done with the item
   int32_t ring_item[kRing];    // index into the sorted item list, -1 = no more work
   uint32_t tmem_base;
-  uint32_t _pad;
+  int32_t last;  // this CTA finished the last split of its (sequence, kv head)
   float red[2][4][8];
   float lred[4][8];
 };
@@ -67,8 +67,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
                  const int32_t* __restrict__ bt, const int32_t* __restrict__ slots,
                  const int32_t* __restrict__ ctx_lens, const DecodeItem* __restrict__ items,
                  const int32_t* __restrict__ n_items_ptr, int32_t* __restrict__ item_counter,
-                 const int32_t* __restrict__ nsplit_of,
-                 __nv_bfloat16* __restrict__ out, float* __restrict__ part_o,
+                 const int32_t* __restrict__ nsplit_of, int32_t* __restrict__ split_done,
+                 int nseq, __nv_bfloat16* __restrict__ out, float* __restrict__ part_o,
                  float* __restrict__ part_ml, int Hkv, int G, int Hq, int L, int maxp, int layer,
                  int max_splits, float scale_log2) {
   using namespace sm100;
@@ -244,6 +244,10 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     }
   } else {
     // ------------------------------------------------ softmax / epilogue (tid < 128)
+    // sequences with no context have no item: their rows are zero
+    for (int sq = blockIdx.x; sq < nseq; sq += gridDim.x)
+      if (nsplit_of[sq] == 0)
+        for (int h = 0; h < Hq; ++h) out[((int64_t)sq * Hq + h) * 128 + tid] = __float2bfloat16(0.f);
     auto write_q = [&](int r, const DecodeItem& it) {
       uint8_t* dst = sQ + (r & 1) * kQBytes;
       for (int c = tid; c < 16 * 16; c += 128) {
@@ -368,11 +372,11 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         if (lane == 0) misc->lred[warp][g] = v;
       }
       named_bar_sync(1, 128);
-      const bool direct = nsplit_of[it.seq] == 1;  // no combine needed
+      const int ns = nsplit_of[it.seq];
       for (int g = 0; g < G; ++g) {
         const float l = misc->lred[0][g] + misc->lred[1][g] + misc->lred[2][g] + misc->lred[3][g];
         const int64_t hrow = (int64_t)it.seq * Hq + it.h * G + g;
-        if (direct) {
+        if (ns == 1) {  // no merge needed
           out[hrow * 128 + tid] = __float2bfloat16(l > 0.f ? o_acc[g] / l : 0.f);
         } else {
           const int64_t row = hrow * max_splits + it.split;
@@ -383,7 +387,35 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           }
         }
       }
-      named_bar_sync(1, 128);  // lred is reused by the next item
+      if (ns > 1) {
+        // Split-KV merge, fused: the CTA that finishes the last split of
+        // (sequence, kv head) merges all of them (threadfence-reduction
+        // pattern) -- no combine launch per layer.  It re-arms the counter
+        // for the next layer's launch.
+        __threadfence();
+        named_bar_sync(1, 128);
+        int32_t* done = split_done + it.seq * Hkv + it.h;
+        if (tid == 0) misc->last = atomicAdd(done, 1) == ns - 1;
+        named_bar_sync(1, 128);
+        if (misc->last) {
+          __threadfence();
+          for (int g = 0; g < G; ++g) {
+            const int64_t base = ((int64_t)it.seq * Hq + it.h * G + g) * max_splits;
+            float mstar = -INFINITY;
+            for (int s = 0; s < ns; ++s) mstar = fmaxf(mstar, __ldcg(part_ml + (base + s) * 2));
+            float l = 0.f, o = 0.f;
+            for (int s = 0; s < ns; ++s) {
+              const float ms = __ldcg(part_ml + (base + s) * 2);
+              const float w = ms == -INFINITY ? 0.f : exp2f(ms - mstar);
+              l += w * __ldcg(part_ml + (base + s) * 2 + 1);
+              o += w * __ldcg(part_o + (base + s) * 128 + tid);
+            }
+            out[(base / max_splits) * 128 + tid] = __float2bfloat16(l > 0.f ? o / l : 0.f);
+          }
+          if (tid == 0) *done = 0;
+        }
+      }
+      named_bar_sync(1, 128);  // lred / last are reused by the next item
       if (tid == 0) mbar_arrive(&misc->ring_empty[r % kRing]);  // done with item r
       have = get_item(r + 1, it);
     }
@@ -399,7 +431,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
 inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t slots,
                             uint64_t ctx_lens, int grid, float scale, float* part_o,
                             float* part_ml, const DecodeItem* items, const int32_t* n_items,
-                            int32_t* item_counter, const int32_t* nsplit, uint64_t out,
+                            int32_t* item_counter, const int32_t* nsplit, int32_t* split_done,
+                            int nseq, uint64_t out,
                             int max_splits, cudaStream_t st) {
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
   const float scale_log2 = scale * 1.4426950408889634f;
@@ -413,7 +446,8 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
     decode_tc_kernel<64><<<grid, kDecThreads, kDecSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
-        items, n_items, item_counter, nsplit, reinterpret_cast<__nv_bfloat16*>(out), part_o,
+        items, n_items, item_counter, nsplit, split_done, nseq,
+        reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2);
   } else {
@@ -426,7 +460,8 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
     decode_tc_kernel<128><<<grid, kDecThreads, kDecSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
-        items, n_items, item_counter, nsplit, reinterpret_cast<__nv_bfloat16*>(out), part_o,
+        items, n_items, item_counter, nsplit, split_done, nseq,
+        reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2);
   }

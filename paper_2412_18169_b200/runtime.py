@@ -536,7 +536,7 @@ def paged_decode(pool: DevicePool, layer: int, q, slots, ctx_lens, max_ctx: int,
     _check(_lib.kb_paged_decode(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
                                 ctx_lens.data_ptr(), q.shape[0], max_ctx, scale,
                                 out.data_ptr(), workspace.data_ptr(), max_splits, flags,
-                                _stream(stream)), launches=2 if reuse_plan else 3)
+                                _stream(stream)), launches=1 if reuse_plan else 2)
 
 
 def prefill_splits(nseq: int, n_q_heads: int, max_q_len: int, max_kv_len: int,
