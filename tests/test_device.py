@@ -431,6 +431,46 @@ def test_paged_decode_matches_oracle(rt, shape):
     pool.close()
 
 
+def test_paged_decode_plan_reuse_across_layers(rt):
+    """One plan, several layer launches (KB_DECODE_REUSE_PLAN), as a decode
+    step runs them: the in-kernel split merge's per-(sequence, kv head)
+    counters must re-arm after every launch, so each layer -- and a repeat
+    of the first -- still matches the oracle."""
+    from paper_2412_18169_b200 import runtime
+    shape = ATTN_SHAPES[0]
+    model = shape.spec()
+    pool = rt.create_pool(0, model, model.param_bytes + 96 * MIB, shape)
+    gen = torch.Generator().manual_seed(13)
+    ctxs = [2047, 1500, 700, 129, 64, 1]
+    hkv, hq, B = shape.n_kv_heads, shape.n_q_heads, shape.block_tokens
+    kv = {}
+    for i, c in enumerate(ctxs):
+        assert pool.grow([(i, 0, 2, (c + B - 1) // B)])
+        for l in (0, 1):
+            k = rand_bf16((c, hkv, 128), gen)
+            v = rand_bf16((c, hkv, 128), gen)
+            append(pool, l, k, v, i, 0)
+            kv[(i, l)] = (k.float().numpy(), v.float().numpy())
+    q = rand_bf16((len(ctxs), hq, 128), gen)
+    scale = 128 ** -0.5
+    slots = torch.arange(len(ctxs), dtype=torch.int32, device="cuda")
+    lens = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    ws = torch.empty(runtime.decode_workspace_bytes(len(ctxs), hq, 16), dtype=torch.uint8,
+                     device="cuda")
+    for n, l in enumerate((0, 1, 0, 1)):
+        out = torch.empty((len(ctxs), hq, 128), dtype=torch.bfloat16, device="cuda")
+        runtime.paged_decode(pool, l, q.cuda(), slots, lens, max(ctxs), out, ws, scale,
+                             max_splits=16, reuse_plan=n > 0)
+        torch.cuda.synchronize()
+        got = out.float().cpu().numpy()
+        for i in range(len(ctxs)):
+            k, v = kv[(i, l)]
+            want = bf16_to_f32(f32_to_bf16(decode_ref(q[i].float().numpy(), k, v, scale)))
+            ma, mr = check_close(got[i], want)
+            assert ma <= 2e-2 and mr <= 1e-3, (n, l, ctxs[i], ma, mr)
+    pool.close()
+
+
 @pytest.mark.parametrize("kv_splits", [1, 3, 8])
 @pytest.mark.parametrize("shape", ATTN_SHAPES[:2], ids=lambda s: s.name)
 def test_paged_prefill_matches_oracle(rt, shape, kv_splits):
