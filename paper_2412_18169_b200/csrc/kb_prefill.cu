@@ -643,22 +643,26 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 
 // Merge the KV splits of every (sequence, 256-row tile, q head) unit:
 // O = sum_i O_i 2^(m_i - M) / sum_i l_i 2^(m_i - M), M = max_i m_i.
+// One CTA per 64 rows of a unit (blockIdx.y = row quarter): 4x the CTAs of
+// one-per-unit, so the HBM-bound merge fills the 148 SMs.
+constexpr int kCombRows = 64;
 __global__ void __launch_bounds__(256)
 prefill_combine_kernel(const uint8_t* __restrict__ part, const int32_t* __restrict__ q_off,
                        const int32_t* __restrict__ q_len, int mtiles, int Hq, int splits,
                        __nv_bfloat16* __restrict__ out) {
   constexpr int kRows = 2 * kPfTile;
-  __shared__ float s_w[kRows][8];
+  __shared__ float s_w[kCombRows][8];
   const int unit = blockIdx.x;  // (seq * mtiles + mt) * Hq + hq
   const int hq = unit % Hq, cta = unit / Hq;
   const int seq = cta / mtiles, mt = cta % mtiles;
   const int qlen = q_len[seq], qo = q_off[seq];
-  const int row0 = mt * kRows;
+  const int rbase = blockIdx.y * kCombRows;  // first row of this CTA within the unit
+  const int row0 = mt * kRows + rbase;
   if (row0 >= qlen) return;
   const int64_t units = (int64_t)gridDim.x;
   const float* ml = reinterpret_cast<const float*>(part + units * splits * kRows * 256);
-  {
-    const int r = threadIdx.x;
+  if (threadIdx.x < kCombRows) {
+    const int r = rbase + threadIdx.x;
     float m = -INFINITY;
     for (int s = 0; s < splits; ++s)
       m = fmaxf(m, ml[(((int64_t)unit * splits + s) * kRows + r) * 2]);
@@ -666,14 +670,14 @@ prefill_combine_kernel(const uint8_t* __restrict__ part, const int32_t* __restri
     for (int s = 0; s < splits; ++s) {
       const float* e = ml + (((int64_t)unit * splits + s) * kRows + r) * 2;
       const float w = (m == -INFINITY || e[0] == -INFINITY) ? 0.f : e[1] * exp2f(e[0] - m);
-      s_w[r][s] = w;
+      s_w[threadIdx.x][s] = w;
       wsum += w;
     }
     const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-    for (int s = 0; s < splits; ++s) s_w[r][s] *= inv;
+    for (int s = 0; s < splits; ++s) s_w[threadIdx.x][s] *= inv;
   }
   __syncthreads();
-  const int rows = min(kRows, qlen - row0);
+  const int rows = min(kCombRows, qlen - row0);
   // 16 threads per row, 8 fp16 (16 B) each
   for (int i = threadIdx.x; i < rows * 16; i += blockDim.x) {
     const int r = i >> 4, c8 = i & 15;
@@ -682,7 +686,7 @@ prefill_combine_kernel(const uint8_t* __restrict__ part, const int32_t* __restri
       const float w = s_w[r][s];
       if (w == 0.f) continue;
       const int4 v = reinterpret_cast<const int4*>(
-          part + (((int64_t)unit * splits + s) * kRows + r) * 256)[c8];
+          part + (((int64_t)unit * splits + s) * kRows + rbase + r) * 256)[c8];
       const __half2* h = reinterpret_cast<const __half2*>(&v);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -753,7 +757,8 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
   rc = B == 64 ? launch(prefill_tc_kernel<64>) : launch(prefill_tc_kernel<128>);
   if (rc) return rc;
   if (splits > 1) {
-    prefill_combine_kernel<<<nseq * mtiles * n_q_heads, 256, 0, st>>>(
+    prefill_combine_kernel<<<dim3(nseq * mtiles * n_q_heads, 2 * kPfTile / kCombRows), 256, 0,
+                             st>>>(
         reinterpret_cast<const uint8_t*>(workspace), reinterpret_cast<const int32_t*>(q_off),
         reinterpret_cast<const int32_t*>(q_len), mtiles, n_q_heads, splits,
         reinterpret_cast<__nv_bfloat16*>(out));
