@@ -313,9 +313,10 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
     b.record(st)
     b.synchronize()
     ms = a.elapsed_time(b) / iters
-    # per member: one plan, then one attention launch per layer (the KV
-    # splits are merged inside it)
-    launches = sum(1 + (hi - lo) for _, lo, hi, *_ in work)
+    # per member: one plan, then per layer one attention launch (which
+    # merges the KV splits itself at this batch size) or attention + combine
+    launches = sum(1 + (hi - lo) * (1 if q.shape[0] * pool.shape.n_kv_heads >= 4 * 148 else 2)
+                   for pool, lo, hi, q, *_ in work)
     gbs = algo_bytes / (ms / 1e3) / 1e9
     return {"value": round(nres / (ms / 1e3), 1), "unit": "tok/s",
             "tokens_per_step": nres, "ms_per_token_step": round(ms, 4),

@@ -6,9 +6,9 @@
 // (pkg/src/dropsim/costmodel.py:50-57).  Parity is against the fp32 CPU
 // restatement oracle/attention.py with max-abs <= 2e-2, mean-rel <= 1e-3.
 //
-// One launch per layer: the persistent tcgen05 kernel (kb_decode_tc.cuh),
-// which also merges the KV splits; plus one plan launch (work items) per
-// decode step, reused by every layer.
+// Per layer: the persistent tcgen05 kernel (kb_decode_tc.cuh), which for
+// large batches also merges the KV splits, else a split-KV combine launch;
+// plus one plan launch (work items) per decode step, reused by every layer.
 #include "kb_common.cuh"
 #include "kb_decode_tc.cuh"
 
@@ -21,6 +21,30 @@ constexpr int kLenBuckets = 1024;
 #define KB_DEC_ITEMS_PER_CTA 2  // swept 1-8 on B200 with dynamic fetching: 1-2 best
 #endif
 constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per persistent CTA
+
+// Split-KV combine for small batches: one CTA per (sequence, q head),
+// thread = head_dim lane.  Sequences with 0 splits (no context) get a zero
+// row, with 1 split the attention kernel wrote the row itself.
+__global__ void decode_combine_kernel(const float* __restrict__ part_o,
+                                      const float* __restrict__ part_ml,
+                                      const int32_t* __restrict__ nsplit_of,
+                                      __nv_bfloat16* __restrict__ out, int Hq, int max_splits) {
+  const int sh = blockIdx.x;  // seq * Hq + head
+  const int seq = sh / Hq;
+  const int ns = nsplit_of[seq];
+  if (ns <= 1) return;
+  const float* ml = part_ml + (int64_t)sh * max_splits * 2;
+  float mstar = -INFINITY;
+  for (int s = 0; s < ns; ++s) mstar = fmaxf(mstar, ml[2 * s]);
+  float l = 0.f, o = 0.f;
+  for (int s = 0; s < ns; ++s) {
+    const float ms = ml[2 * s];
+    const float w = ms == -INFINITY ? 0.f : exp2f(ms - mstar);
+    l += w * ml[2 * s + 1];
+    o += w * part_o[((int64_t)sh * max_splits + s) * 128 + threadIdx.x];
+  }
+  out[(int64_t)sh * 128 + threadIdx.x] = __float2bfloat16(l > 0.f ? o / l : 0.f);
+}
 
 // Work items: sequence i is cut into s_i = clamp(ceil(tiles_i / T), 1,
 // max_splits) splits per kv head, T chosen so the items spread ~kItemsPerCta
@@ -69,14 +93,35 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, int nseq, int Hkv, int Hq, i
     }
   }
   __syncthreads();
-  // exclusive scan of the (descending-length) histogram
-  if (tid == 0) {
-    int run = 0;
-    for (int b = 0; b < kLenBuckets; ++b) {
-      cursor[b] = run;
-      run += hist[b];
+  // exclusive scan of the (descending-length) histogram, one bucket per
+  // thread: warp shuffles, then the 32 warp totals (a serial scan by one
+  // thread cost ~30 us per decode step)
+  static_assert(kLenBuckets == kPlanThreads && kPlanThreads == 1024, "one bucket per thread");
+  __shared__ int warp_sum[32];
+  {
+    const int lane = tid & 31, w = tid >> 5;
+    const int v = hist[tid];
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    *n_items = run;
+    if (lane == 31) warp_sum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int t = warp_sum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_sum[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const int before = (w ? warp_sum[w - 1] : 0) + x - v;
+    cursor[tid] = before;
+    if (tid == kLenBuckets - 1) *n_items = before + v;
   }
   __syncthreads();
   for (int i = tid; i < nseq; i += blockDim.x) {
@@ -148,9 +193,18 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
                                                    item_counter, split_done);
     KB_LAUNCH_CHECK();
   }
+  // merge inside the attention kernel when the batch is large (>= 4
+  // (sequence, kv head) pairs per CTA; B200 A/B: 191 vs 200 us per Llama
+  // layer at 147 sequences, equal at 64, slower below: 26 vs 21 us at 4)
+  const int fuse = (int64_t)nseq * Hkv >= 4LL * grid;
   rc = launch_decode_tc(p, layer, n_q_heads, q, slots, ctx_lens, grid, scale, part_o, part_ml,
-                        items, n_items, item_counter, nsplit, split_done, nseq, out, max_splits,
-                        st);
+                        items, n_items, item_counter, nsplit, split_done, nseq, fuse, out,
+                        max_splits, st);
   if (rc) return rc;
+  if (!fuse) {
+    decode_combine_kernel<<<nseq * n_q_heads, 128, 0, st>>>(
+        part_o, part_ml, nsplit, reinterpret_cast<__nv_bfloat16*>(out), n_q_heads, max_splits);
+    KB_LAUNCH_CHECK();
+  }
   return pool_leave(p, st);
 }

@@ -68,7 +68,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
                  const int32_t* __restrict__ ctx_lens, const DecodeItem* __restrict__ items,
                  const int32_t* __restrict__ n_items_ptr, int32_t* __restrict__ item_counter,
                  const int32_t* __restrict__ nsplit_of, int32_t* __restrict__ split_done,
-                 int nseq, __nv_bfloat16* __restrict__ out, float* __restrict__ part_o,
+                 int nseq, int fuse_merge, __nv_bfloat16* __restrict__ out,
+                 float* __restrict__ part_o,
                  float* __restrict__ part_ml, int Hkv, int G, int Hq, int L, int maxp, int layer,
                  int max_splits, float scale_log2) {
   using namespace sm100;
@@ -387,11 +388,13 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           }
         }
       }
-      if (ns > 1) {
+      if (ns > 1 && fuse_merge) {
         // Split-KV merge, fused: the CTA that finishes the last split of
         // (sequence, kv head) merges all of them (threadfence-reduction
         // pattern) -- no combine launch per layer.  It re-arms the counter
-        // for the next layer's launch.
+        // for the next layer's launch.  (Chosen for large batches only: the
+        // fence + counter per split item costs more than a combine launch
+        // when the items are short.)
         __threadfence();
         named_bar_sync(1, 128);
         int32_t* done = split_done + it.seq * Hkv + it.h;
@@ -432,7 +435,7 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
                             uint64_t ctx_lens, int grid, float scale, float* part_o,
                             float* part_ml, const DecodeItem* items, const int32_t* n_items,
                             int32_t* item_counter, const int32_t* nsplit, int32_t* split_done,
-                            int nseq, uint64_t out,
+                            int nseq, int fuse_merge, uint64_t out,
                             int max_splits, cudaStream_t st) {
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
   const float scale_log2 = scale * 1.4426950408889634f;
@@ -446,7 +449,7 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
     decode_tc_kernel<64><<<grid, kDecThreads, kDecSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
-        items, n_items, item_counter, nsplit, split_done, nseq,
+        items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
         reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2);
@@ -460,7 +463,7 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
     decode_tc_kernel<128><<<grid, kDecThreads, kDecSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
-        items, n_items, item_counter, nsplit, split_done, nseq,
+        items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
         reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2);

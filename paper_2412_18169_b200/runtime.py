@@ -533,10 +533,14 @@ def paged_decode(pool: DevicePool, layer: int, q, slots, ctx_lens, max_ctx: int,
     reuse_plan: the workspace already holds the plan for these ctx_lens (a
     previous layer of the same decode step)."""
     flags = DECODE_REUSE_PLAN if reuse_plan else 0
+    # the split merge runs inside the attention kernel for large batches,
+    # else in a combine launch (kb_decode.cu)
+    fused = q.shape[0] * pool.shape.n_kv_heads >= 4 * _sm_count(pool.rt.device)
     _check(_lib.kb_paged_decode(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
                                 ctx_lens.data_ptr(), q.shape[0], max_ctx, scale,
                                 out.data_ptr(), workspace.data_ptr(), max_splits, flags,
-                                _stream(stream)), launches=1 if reuse_plan else 2)
+                                _stream(stream)),
+           launches=(1 if reuse_plan else 2) + (0 if fused else 1))
 
 
 def prefill_splits(nseq: int, n_q_heads: int, max_q_len: int, max_kv_len: int,

@@ -431,17 +431,26 @@ def test_paged_decode_matches_oracle(rt, shape):
     pool.close()
 
 
-def test_paged_decode_plan_reuse_across_layers(rt):
+@pytest.mark.parametrize("batch", ["small", "large"])
+def test_paged_decode_plan_reuse_across_layers(rt, batch):
     """One plan, several layer launches (KB_DECODE_REUSE_PLAN), as a decode
-    step runs them: the in-kernel split merge's per-(sequence, kv head)
-    counters must re-arm after every launch, so each layer -- and a repeat
-    of the first -- still matches the oracle."""
+    step runs them.  Small batch: the combine launch merges the KV splits.
+    Large batch (>= 4 (sequence, kv head) pairs per SM): the attention
+    kernel merges them itself, and its per-(sequence, kv head) counters must
+    re-arm after every launch, so each layer -- and a repeat of the first --
+    still matches the oracle."""
     from paper_2412_18169_b200 import runtime
-    shape = ATTN_SHAPES[0]
+    # large: Llama-3-8B heads (8 kv heads), so 80 sequences give 640 pairs
+    shape = ATTN_SHAPES[0] if batch == "small" else next(x for x in ATTN_SHAPES if x.name == "g4")
     model = shape.spec()
-    pool = rt.create_pool(0, model, model.param_bytes + 96 * MIB, shape)
+    r = rt if batch == "small" else runtime.Runtime(0, max_slots=96, max_pages_per_seq=256,
+                                                    slack_pages=128)
+    pool = r.create_pool(0, model, model.param_bytes + 256 * MIB, shape)
     gen = torch.Generator().manual_seed(13)
     ctxs = [2047, 1500, 700, 129, 64, 1]
+    if batch == "large":  # two long sequences (split 16 ways) among many short ones
+        ctxs = [4000, 3000] + [1 + (37 * i) % 200 for i in range(78)]
+        assert len(ctxs) * shape.n_kv_heads >= 4 * 148
     hkv, hq, B = shape.n_kv_heads, shape.n_q_heads, shape.block_tokens
     kv = {}
     for i, c in enumerate(ctxs):

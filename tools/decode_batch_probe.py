@@ -1,0 +1,50 @@
+"""Paged decode latency per layer at serving batch sizes (Llama-3-8B heads,
+ShareGPT-like contexts): the small batches a pipeline stage decodes, where
+the split merge sits on the kernel's critical path.  A/B builds through
+KB_LIB_PATH."""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, '.')
+from paper_2412_18169_b200 import build  # noqa: E402
+build.build()
+from paper_2412_18169_b200 import runtime  # noqa: E402
+from paper_2412_18169_b200.core import ModelShape  # noqa: E402
+
+shape = ModelShape("g4", num_layers=2, hidden=4096, n_q_heads=32, n_kv_heads=8, head_dim=128,
+                   ffn=1024, vocab=1024, block_tokens=64)
+rt = runtime.Runtime(0, max_slots=256, max_pages_per_seq=128, slack_pages=256)
+model = shape.spec()
+pool = rt.create_pool(0, model, model.param_bytes + (12 << 30), shape)
+rng = np.random.default_rng(5)
+out = {}
+for nseq in (4, 16, 32, 64, 147):
+    ctx = np.clip(rng.lognormal(np.log(1500), 0.6, nseq), 16, 8000).astype(int)
+    slots = list(range(nseq))
+    for s, c in zip(slots, ctx):
+        pool.release([s], 0, 2)
+        assert pool.grow([(s, 0, 2, (int(c) + 63) // 64)])
+    q = torch.randn((nseq, 32, 128), device="cuda").to(torch.bfloat16)
+    o = torch.empty_like(q)
+    sl = torch.tensor(slots, dtype=torch.int32, device="cuda")
+    cl = torch.tensor(ctx, dtype=torch.int32, device="cuda")
+    ws = torch.empty(runtime.decode_workspace_bytes(nseq, 32, 16), dtype=torch.uint8, device="cuda")
+
+    def step():
+        for i in range(16):
+            runtime.paged_decode(pool, i % 2, q, sl, cl, int(ctx.max()), o, ws, 128 ** -0.5,
+                                 max_splits=16, reuse_plan=i > 0)
+    for _ in range(5):
+        step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(20):
+        step()
+    b.record()
+    b.synchronize()
+    out[nseq] = round(a.elapsed_time(b) / 20 / 16 * 1000, 2)  # us per layer
+print(json.dumps({"us_per_layer": out}))
