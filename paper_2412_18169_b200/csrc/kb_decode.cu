@@ -21,6 +21,10 @@ constexpr int kLenBuckets = 1024;
 #define KB_DEC_ITEMS_PER_CTA 2  // swept 1-8 on B200 with dynamic fetching: 1-2 best
 #endif
 constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per persistent CTA
+#ifndef KB_DEC_MIN_TILES
+#define KB_DEC_MIN_TILES 2
+#endif
+constexpr int kMinTiles = KB_DEC_MIN_TILES;  // shortest split (128-token tiles)
 
 // Split-KV combine for small batches: one CTA per (sequence, q head),
 // thread = head_dim lane.  Sequences with 0 splits (no context) get a zero
@@ -188,7 +192,7 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   if (rc) return rc;
   if (!(flags & KB_DECODE_REUSE_PLAN)) {
     decode_plan_kernel<<<1, kPlanThreads, 0, st>>>(reinterpret_cast<const int32_t*>(ctx_lens),
-                                                   nseq, Hkv, n_q_heads, max_splits, grid, 2,
+                                                   nseq, Hkv, n_q_heads, max_splits, grid, kMinTiles,
                                                    nsplit, items, n_items, part_ml,
                                                    item_counter, split_done);
     KB_LAUNCH_CHECK();
