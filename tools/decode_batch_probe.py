@@ -1,5 +1,5 @@
-"""Paged decode latency per layer at serving batch sizes (Llama-3-8B heads,
-ShareGPT-like contexts): the small batches a pipeline stage decodes, where
+"""Paged decode device time per layer (CUDA-graph replay, 16 layers per
+plan) at serving batch sizes (Llama-3-8B heads, ShareGPT-like contexts): the small batches a pipeline stage decodes, where
 the split merge sits on the kernel's critical path.  A/B builds through
 KB_LIB_PATH."""
 import json
@@ -40,10 +40,17 @@ for nseq in (4, 16, 32, 64, 147):
     for _ in range(5):
         step()
     torch.cuda.synchronize()
+    # captured in a CUDA graph, as the device engine replays decode-only
+    # stages: device time, not the host's per-call launch cost
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    g.replay()
+    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(20):
-        step()
+        g.replay()
     b.record()
     b.synchronize()
     out[nseq] = round(a.elapsed_time(b) / 20 / 16 * 1000, 2)  # us per layer
