@@ -3,6 +3,7 @@ plan) at serving batch sizes (Llama-3-8B heads, ShareGPT-like contexts): the sma
 the split merge sits on the kernel's critical path.  A/B builds through
 KB_LIB_PATH."""
 import json
+import os
 import sys
 
 import numpy as np
@@ -20,6 +21,7 @@ rt = runtime.Runtime(0, max_slots=256, max_pages_per_seq=128, slack_pages=256)
 model = shape.spec()
 pool = rt.create_pool(0, model, model.param_bytes + (12 << 30), shape)
 rng = np.random.default_rng(5)
+MS = int(os.environ.get("KB_PROBE_MAX_SPLITS", "16"))
 out = {}
 for nseq in (4, 16, 32, 64, 147):
     ctx = np.clip(rng.lognormal(np.log(1500), 0.6, nseq), 16, 8000).astype(int)
@@ -36,7 +38,7 @@ for nseq in (4, 16, 32, 64, 147):
     def step():
         for i in range(16):
             runtime.paged_decode(pool, i % 2, q, sl, cl, int(ctx.max()), o, ws, 128 ** -0.5,
-                                 max_splits=16, reuse_plan=i > 0)
+                                 max_splits=MS, reuse_plan=i > 0)
     for _ in range(5):
         step()
     torch.cuda.synchronize()
