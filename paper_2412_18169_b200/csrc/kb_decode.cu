@@ -33,6 +33,8 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml,
                                       const int32_t* __restrict__ nsplit_of,
                                       __nv_bfloat16* __restrict__ out, int Hq, int max_splits) {
+  sm100::pdl_wait();  // the attention kernel's partials
+  sm100::pdl_launch_dependents();
   const int sh = blockIdx.x;  // seq * Hq + head
   const int seq = sh / Hq;
   const int ns = nsplit_of[seq];
@@ -206,8 +208,20 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
                         max_splits, st);
   if (rc) return rc;
   if (!fuse) {
-    decode_combine_kernel<<<nseq * n_q_heads, 128, 0, st>>>(
-        part_o, part_ml, nsplit, reinterpret_cast<__nv_bfloat16*>(out), n_q_heads, max_splits);
+    // programmatic dependent launch: the combine CTAs start while the
+    // attention kernel drains and wait for its memory (griddepcontrol.wait)
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nseq * n_q_heads);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    KB_RT(cudaLaunchKernelEx(&cfg, decode_combine_kernel, (const float*)part_o,
+                             (const float*)part_ml, (const int32_t*)nsplit,
+                             reinterpret_cast<__nv_bfloat16*>(out), (int)n_q_heads, (int)max_splits));
     KB_LAUNCH_CHECK();
   }
   return pool_leave(p, st);

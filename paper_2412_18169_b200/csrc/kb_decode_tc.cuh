@@ -79,7 +79,6 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
   // per-layer global counter (a greedy longest-processing-time schedule, so
   // the CTAs finish within one short item of each other) and publishes it
   // to the MMA and softmax warps through a small shared-memory ring.
-  const int n_items = *n_items_ptr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   extern __shared__ uint8_t smem_raw[];
@@ -115,6 +114,12 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = misc->tmem_base;
+  // launched with programmatic stream serialization: the prologue above
+  // overlapped the previous kernel's tail; everything below may read what
+  // it wrote (plan, q, appended K/V, the previous layer's workspace use)
+  pdl_wait();
+  pdl_launch_dependents();
+  const int n_items = *n_items_ptr;
   // item r of this CTA (every role reads the ring in the same order)
   auto get_item = [&](int r, DecodeItem& it) -> bool {
     const int slot = r % kRing;
@@ -439,6 +444,16 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
                             int max_splits, cudaStream_t st) {
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
   const float scale_log2 = scale * 1.4426950408889634f;
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kDecThreads);
+  cfg.dynamicSmemBytes = kDecSmem;
+  cfg.stream = st;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
   if (B == 64) {
     static bool attr = false;
     if (!attr) {
@@ -446,13 +461,13 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
                                  kDecSmem));
       attr = true;
     }
-    decode_tc_kernel<64><<<grid, kDecThreads, kDecSmem, st>>>(
+    KB_RT(cudaLaunchKernelEx(&cfg, decode_tc_kernel<64>,
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
         items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
         reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
-        Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2);
+        Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2));
   } else {
     static bool attr = false;
     if (!attr) {
@@ -460,13 +475,13 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem));
       attr = true;
     }
-    decode_tc_kernel<128><<<grid, kDecThreads, kDecSmem, st>>>(
+    KB_RT(cudaLaunchKernelEx(&cfg, decode_tc_kernel<128>,
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
         items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
         reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
-        Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2);
+        Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2));
   }
   KB_LAUNCH_CHECK();
   return KB_OK;
