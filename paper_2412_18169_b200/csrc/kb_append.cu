@@ -34,6 +34,9 @@ __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __rest
                                  const int32_t* __restrict__ slots, const int32_t* __restrict__ pos,
                                  int ntok, int Hkv, int B, int L, int maxp, int layer,
                                  int64_t page_bytes, int64_t row_vec) {
+  // the attention launch that follows (programmatic dependent launch) may
+  // run its prologue now; it waits for this grid's writes before reading
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= ntok * Hkv) return;

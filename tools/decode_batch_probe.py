@@ -22,6 +22,7 @@ model = shape.spec()
 pool = rt.create_pool(0, model, model.param_bytes + (12 << 30), shape)
 rng = np.random.default_rng(5)
 MS = int(os.environ.get("KB_PROBE_MAX_SPLITS", "16"))
+APPEND = os.environ.get("KB_PROBE_APPEND", "0") == "1"
 out = {}
 for nseq in (4, 16, 32, 64, 147):
     ctx = np.clip(rng.lognormal(np.log(1500), 0.6, nseq), 16, 8000).astype(int)
@@ -35,8 +36,13 @@ for nseq in (4, 16, 32, 64, 147):
     cl = torch.tensor(ctx, dtype=torch.int32, device="cuda")
     ws = torch.empty(runtime.decode_workspace_bytes(nseq, 32, 16), dtype=torch.uint8, device="cuda")
 
+    kn = torch.randn((nseq, 8, 128), device="cuda").to(torch.bfloat16)
+    pos = torch.tensor(ctx - 1, dtype=torch.int32, device="cuda")
+
     def step():
         for i in range(16):
+            if APPEND:  # the new token's K/V first, as a decode stage does
+                runtime.kv_append(pool, i % 2, kn, kn, sl, pos)
             runtime.paged_decode(pool, i % 2, q, sl, cl, int(ctx.max()), o, ws, 128 ** -0.5,
                                  max_splits=MS, reuse_plan=i > 0)
     for _ in range(5):
