@@ -267,7 +267,8 @@ def prefill_measure(rt, tensor_peak: float, ctx: int = 32768, chunk: int = 2048,
             "ms_per_layer": round(ms, 3), "chunks": len(calls),
             "roofline": {"bound": "tensor", "achieved": round(tf, 1), "peak": tensor_peak,
                          "unit": "TFLOP/s", "frac": round(tf / tensor_peak, 4),
-                         "traffic": _traffic("prefill_tc_kernel"),
+                         "traffic": (_traffic("prefill_tc_kernel") or {}).get(
+                             "dram_bytes_per_launch"),
                          "flops_per_layer": flops}}
 
 
@@ -323,7 +324,8 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
             "note": "attention only, one token per resident through 32 layers",
             "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
-                         "traffic": _traffic("decode_tc_kernel")},
+                         "traffic": (_traffic("decode_tc_kernel") or {}).get(
+                             "dram_bytes_per_launch")},
             "launches_per_step": launches}
 
 
@@ -367,14 +369,37 @@ def nvlink_measure(rt, shape, args, pp: int = 2) -> dict:
 
 
 def _traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/ncu_traffic.json), or None."""
+    """{dram_bytes_per_launch, source} of `kernel` from the committed ncu
+    capture (profiles/ncu_traffic.json: which capture, when), or None.  ncu
+    cannot run inside the timed bench, so this is the last capture's number,
+    labelled with its date."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f)[kernel]["dram_bytes_per_launch"]
+            d = json.load(f)[kernel]
+        return {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"),
+                "source": d.get("source", "profiles/ncu_traffic.json")}
     except (OSError, KeyError, ValueError):
         return None
+
+
+def _summary(line: dict) -> dict:
+    """The numbers a reader needs, last in the line (the driver keeps its tail)."""
+    t = line.get("p99_ttft") or {}
+    dec = (line.get("paged_decode") or {}).get("roofline", {})
+    pre = (line.get("paged_prefill") or {}).get("roofline", {})
+    pol = {p: {"p99_ttft_s": (t.get(p) or {}).get("p99_ttft_s"),
+               "p50_tpot_s": (t.get(p) or {}).get("p50_tpot_s"),
+               "served": (t.get(p) or {}).get("served")}
+           for p in ("kunserve", "recompute", "swap", "migrate") if t.get(p)}
+    return {"payload_gbs_same_gpu_proxy": line["value"], "e2e_gbs": line["e2e"]["value"],
+            "copy_pages_frac": line["roofline"]["frac"],
+            "param_pull_frac": line["roofline_param_pull"]["frac"],
+            "decode_frac": dec.get("frac"), "prefill_frac": pre.get("frac"),
+            "parity": line["parity"]["weights_bit_exact"] and line["parity"]["kv_bit_exact"],
+            "ttft_clock": t.get("clock"), "ttft": pol,
+            "criterion_4": t.get("criterion_4"),
+            "nvlink_frac": (line.get("roofline_nvlink") or {}).get("frac")}
 
 
 def main():
@@ -451,29 +476,38 @@ def main():
     clk = clocks.stop()
 
     dev_ms = sum(r.ms["total"] for r in reps)
-    moved = sum(r.bytes_moved for r in reps)
+    payload = sum(r.payload_bytes for r in reps)
     if ws > 1:
-        t = torch.tensor([dev_ms, float(moved)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dev_ms, float(payload)], dtype=torch.float64, device="cuda")
         mx = t.clone()
         torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
         sm = t.clone()
         torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        dev_ms, moved = float(mx[0]), int(sm[1])
-    value = moved / (dev_ms / 1e3) / 1e9
-    # parity at full size: boot layout, weights and every KV page round-trip
+        dev_ms, payload = float(mx[0]), int(sm[1])
+    # headline: the reference's payload (sum of TransferTask.size_bytes of the
+    # exchange, restore and consolidation tasks) per device-timed step
+    value = payload / (dev_ms / 1e3) / 1e9
+    # parity at full size, position-sensitive: every slab's 64-bit content
+    # hash equals its boot value AND the other replica's (identical weights);
+    # every long-lived resident's per-page hashes, in block-table order, equal
+    # their boot values
     w1 = cyc.weight_checksums()
     k1 = cyc.kv_checksums()
-    parity = {"weights_bit_exact": w0 == w1,
-              "kv_bit_exact": all(torch.equal(k0[r], k1[r]) for r in k0)}
-    # dominant kernel: the peer slab pull (copy_flat_kernel), HBM read+write
-    pk_ms = sum(r.param_kernel_ms for r in reps)
-    pbytes = sum(r.bytes_param for r in reps)
-    achieved = 2 * pbytes / (pk_ms / 1e3) / 1e9 if pk_ms else 0.0
-    # the other big mover: KV page copies (exchange + consolidation bursts,
-    # their block-table grows included), also read + write HBM
-    kv_ms = sum(r.kv_kernel_ms for r in reps)
-    kv_bytes = sum(r.bytes_kv_exchange + r.bytes_kv_consolidate for r in reps)
-    kv_achieved = 2 * kv_bytes / (kv_ms / 1e3) / 1e9 if kv_ms else 0.0
+    L = shape.num_layers
+    parity = {"weights_bit_exact": w0 == w1 and all(w1[(0, l)] == w1[(1, l)] for l in range(L)),
+              "kv_bit_exact": set(k0) == set(k1) and all(torch.equal(k0[r], k1[r]) for r in k0),
+              "check": "kb_hash_segments (position-sensitive 64-bit hash) of all "
+                       f"{2 * L} slabs and {sum(v.numel() for v in k1.values())} resident KV pages"}
+    # the copy launches alone (events around them, no grows or queueing):
+    # KV page copies (copy_pages_kernel, the time-dominant kernel) and slab
+    # pulls (copy_flat_kernel); same-GPU copies read + write HBM
+    kv_ms = sum(r.kv_copy_ms for r in reps)
+    kv_b = sum(r.kv_copy_bytes for r in reps)
+    kv_achieved = 2 * kv_b / (kv_ms / 1e3) / 1e9 if kv_ms else 0.0
+    pk_ms = sum(r.param_copy_ms for r in reps)
+    pk_b = sum(r.param_copy_bytes for r in reps)
+    pk_achieved = 2 * pk_b / (pk_ms / 1e3) / 1e9 if pk_ms else 0.0
+    kv_launches = sum(r.kv_copy_launches for r in reps)
 
     # paged decode in the merged state
     cyc.pause_merged = True
@@ -481,30 +515,35 @@ def main():
     dec = decode_measure(cyc, args.decode_iters, hbm_peak)
     cyc.resume()
 
-    # e2e: host wall clock of the public-API step incl. planning, plus the
-    # step's inputs (request token table) H2D from pinned memory and its
-    # result (per-request KV checksum of the first layer page) D2H
-    tok = torch.tensor(list(cyc.tokens.values()), dtype=torch.int32).pin_memory()
+    # e2e through the public API: each step's input is a queued burst (the
+    # request table per replica, host data: traceio.synth_burst lengths) from
+    # which plan_drop sizes the merge; the plan reaches the device as
+    # descriptors through the C-ABI (block-table grows, page moves, release
+    # lists, slab ranges: h2d_bytes_per_step, counted by the runtime); the
+    # step's result -- every long-lived resident's first page on its home
+    # pool, plus the compactions' moved-page counts -- is read back D2H
     res = torch.empty(len(cyc.tokens), dtype=torch.int32).pin_memory()
     cyc.auto_refill = False
     e2e_s = 0.0
     e2e_steps = []
     gc.collect()
     gc.disable()
-    e_moved = 0
+    e_payload = 0
+    h2d = []
     for i in range(args.warmup + args.steps):  # the first W steps are warm-up
+        burst = cyc.burst_for(seed=100 + i)
         torch.cuda.synchronize()
+        h0 = runtime.H2D_BYTES[0]
         t0 = time.perf_counter()
-        tok_d = tok.to("cuda", non_blocking=True)
-        r = cyc.step()
+        r = cyc.step(burst=burst)
         res.copy_(cyc.home_first_pages(), non_blocking=True)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             e2e_steps.append(round(dt * 1e3, 2))
             e2e_s += dt
-            e_moved += r.bytes_moved
-        del tok_d
+            e_payload += r.payload_bytes
+            h2d.append(runtime.H2D_BYTES[0] - h0)
         cyc.refill()  # the next burst's arrivals: not part of the cycle
     gc.enable()
     cyc.auto_refill = True
@@ -513,9 +552,9 @@ def main():
     _, tensor_peak, _ = load_peaks()
     prefill = prefill_measure(rt, tensor_peak or 1590.0)
 
-    # P99 TTFT: the reference's scheduler on real pools with measured stage
-    # times, KunServe vs the recompute baseline on one 4x burst
     sweep = copy_sweep(rt) if ws == 1 else None
+    # P99 TTFT: the reference's scheduler on real pools, KunServe vs the
+    # reference's three baselines on one 4x burst
     ttft = None
     if not args.no_ttft and ws == 1:  # a single-GPU measurement (two replicas per GPU)
         from paper_2412_18169_b200.ttft import measure
@@ -551,11 +590,16 @@ def main():
                    "sample": f"3 CPU cycles of 2 of 32 layer slabs + {len(res_toks)} residents' "
                              f"pages, numpy copies on {cc.threads} threads"}
         r0 = r_last
+        trf = _traffic("copy_pages_kernel")
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dev_ms / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "value_label": ("drop/restore payload GB/s (sum of TransferTask.size_bytes per "
+                            "device-timed step); at N=1 a SAME-GPU HBM PROXY -- both replicas "
+                            "share one B200, so no byte crosses NVLink; cross-GPU numbers are "
+                            "nvlink_* (N>1)"),
             "config": {"workload": "llama3_8b bf16, 2 replicas per GPU -> 1 PP-2 group; "
                                    "ShareGPT-shaped residents at 90% KV; drop+exchange+"
                                    "restore+consolidate per step",
@@ -563,22 +607,33 @@ def main():
                        "kv_budget_gib_per_replica": args.kv_gib,
                        "residents": len(cyc.tokens), "parallelism": f"pp2 x{ws} (replica pairs)",
                        "l2": "inputs larger than L2 (GB-scale moves per step)"},
-            "breakdown": {"bytes_per_step": r0.bytes_moved, "kv_exchange": r0.bytes_kv_exchange,
-                          "param_restore": r0.bytes_param, "kv_consolidate": r0.bytes_kv_consolidate,
-                          "compaction_rw": r0.bytes_compaction, "ms": r0.ms,
+            "breakdown": {"payload_bytes_per_step": r0.payload_bytes,
+                          "payload": {"kv_exchange": r0.payload_kv_exchange,
+                                      "param_restore": r0.payload_param,
+                                      "kv_consolidate": r0.payload_kv_consolidate},
+                          "device_bytes": {"kv_exchange_pages": r0.bytes_kv_exchange,
+                                           "param_restore": r0.bytes_param,
+                                           "kv_consolidate_pages": r0.bytes_kv_consolidate},
+                          "compaction_bytes_not_in_value": r0.bytes_compaction,
+                          "ms": {k: round(v, 3) for k, v in r0.ms.items()},
                           "remap_ms": round(r0.remap_ns / 1e6, 3), "tasks": r0.n_tasks,
                           "host_enqueue_ms": {k: round(v, 3) for k, v in r0.host_ms.items()}},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
-                         "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                         "traffic": _traffic("copy_flat_kernel"),
-                         "traffic_algorithmic": 2 * pbytes // max(1, sum(r.param_launches for r in reps)),
-                         "kernel": "copy_flat_kernel (peer slab pull; same-GPU replicas: "
-                                   "read+write HBM)", "peak_source": peak_src},
-            "roofline_kv_pages": {"bound": "hbm", "achieved": round(kv_achieved, 1),
-                                  "peak": hbm_peak, "unit": "GB/s",
-                                  "frac": round(kv_achieved / hbm_peak, 4),
-                                  "kernel": "copy_pages_kernel bursts (grows included), "
-                                            "read+write HBM"},
+            "roofline": {"bound": "hbm", "achieved": round(kv_achieved, 1), "peak": hbm_peak,
+                         "unit": "GB/s", "frac": round(kv_achieved / hbm_peak, 4),
+                         "traffic": trf.get("dram_bytes_per_launch") if trf else None,
+                         "traffic_source": trf.get("source") if trf else None,
+                         "kernel": "copy_pages_kernel (KV exchange + consolidation page copies; "
+                                   "the step's time-dominant kernel); achieved = 2 x page bytes "
+                                   "(read + write HBM) / copy-launch time, events around the "
+                                   "launches alone",
+                         "algorithmic_bytes_per_launch": round(2 * kv_b / max(1, kv_launches)),
+                         "kernel_ms_per_step": round(kv_ms / args.steps, 3),
+                         "peak_source": peak_src},
+            "roofline_param_pull": {"bound": "hbm", "achieved": round(pk_achieved, 1),
+                                    "peak": hbm_peak, "unit": "GB/s",
+                                    "frac": round(pk_achieved / hbm_peak, 4),
+                                    "kernel": "copy_flat_kernel (slab pulls)",
+                                    "kernel_ms_per_step": round(pk_ms / args.steps, 3)},
             "paged_decode": dec,
             "paged_prefill": prefill,
             "copy_sweep": sweep,
@@ -586,15 +641,20 @@ def main():
             "nvlink_cycle": nvl,
             "nvlink_cycle_pp4": nvl4,
             "nvlink_sweep": sweep_n,
+            "roofline_nvlink": (nvl or {}).get("roofline"),
             "parity": parity,
-            "e2e": {"value": round(e_moved / e2e_s / 1e9, 1), "unit": "GB/s",
-                    "h2d_bytes_per_step": tok.numel() * 4, "d2h_bytes_per_step": res.numel() * 4,
-                    "ms_per_step": e2e_steps},
+            "e2e": {"value": round(e_payload / e2e_s / 1e9, 1), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(sum(h2d) / max(1, len(h2d))),
+                    "d2h_bytes_per_step": res.numel() * 4 + 16 * 2,
+                    "ms_per_step": e2e_steps,
+                    "input": "queued burst per replica -> plan_drop -> C-ABI descriptors "
+                             "(grows, page moves, releases, slab ranges)"},
             "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,
             "host_s_timed": round(host_s, 3),
         }
+        line["summary"] = _summary(line)
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()

@@ -24,7 +24,8 @@
  *   KV VA     : [slack pages | residual | dropped slab 0 | dropped slab 1 ...]
  *               page p at kv_base + p*page_bytes; a page holds one layer of
  *               `block_tokens` tokens of one request:
- *               [K|V][n_kv_heads][block_tokens][head_dim] bf16.
+ *               [K|V][n_kv_heads][block_tokens][head_dim], K bf16, V fp16
+ *               (V converted on append; range-guarded, see kb_pool_kv_status).
  *   metadata  : page bitmap (1 = live), owner[page] (reverse map),
  *               block_table[slot][layer][max_pages_per_seq] (int32, -1 empty),
  *               npages[slot][layer].
@@ -147,7 +148,12 @@ uint64_t kb_weight_ptr(kb_pool* pool, int32_t layer);
  * every stream that touched the pool (no page is freed or moved under a
  * reader); copies, appends and attention after the last grow / release /
  * drop / compaction.  Inside a CUDA graph capture the graph's own edges are
- * the ordering.  */
+ * the ordering; a REPLAY of such a graph is invisible to the pool, so the
+ * caller brackets it with kb_pool_stream_begin / kb_pool_stream_end on the
+ * replay stream (wait for the last bitmap op; later releases and
+ * compactions wait for the replay). */
+int kb_pool_stream_begin(kb_pool* pool, uintptr_t stream);
+int kb_pool_stream_end(kb_pool* pool, uintptr_t stream);
 
 /* ---- N2: paged KV block tables (KVAllocator, memory.py:70-129) ---------- */
 /* Grow block tables on device: the kernel takes the K lowest free page ids
@@ -244,10 +250,24 @@ int kb_ipc_mem_close(uint64_t ptr);
 int kb_kv_append(kb_pool* pool, int32_t layer, uint64_t k, uint64_t v,
                  uint64_t slots, uint64_t pos, int32_t ntok, int64_t row_stride,
                  uintptr_t stream);
+/* The V cache is fp16: exact for bf16 V values of magnitude in [2^-14,
+ * 65504] (or 0).  Appends flag, in the pool's sticky status word,
+ * KB_KV_V_OVERFLOW for any |v| >= 2^16 (inf, NaN included) and
+ * KB_KV_V_UNDERFLOW for a V row (one token, one kv head) whose largest |v|
+ * is nonzero and below 2^-14 (the whole row would be fp16-subnormal; small
+ * entries beside a normal row maximum keep the normal range's 2^-11 error
+ * bound relative to it), and still store the fp16 rounding.
+ * kb_pool_kv_status returns the flags of every append that has completed
+ * (synchronize the appending stream first for an exact answer) and clears
+ * them when `clear` != 0; the host shims raise ValueError on any flag. */
+#define KB_KV_V_OVERFLOW 1u
+#define KB_KV_V_UNDERFLOW 2u
+int kb_pool_kv_status(kb_pool* pool, uint32_t* flags, int32_t clear);
 /* Decode: q [nseq][n_q_heads][head_dim] bf16, one query token per sequence
  * attending to ctx_lens[i] cached tokens of slot slots[i] (including its
  * own, already appended).  out [nseq][n_q_heads][head_dim] bf16.
- * workspace: kb_decode_workspace_bytes() bytes of device scratch.  The work
+ * workspace: workspace_bytes >= kb_decode_workspace_bytes(nseq, ...) bytes of
+ * device scratch (KB_EINVAL otherwise: its layout grows with nseq).  The work
  * plan (KV splits, item order) depends only on ctx_lens: with
  * flags & KB_DECODE_REUSE_PLAN the plan already in `workspace` (from an
  * earlier call with the same ctx_lens, e.g. the previous layer of the same
@@ -256,8 +276,8 @@ int kb_kv_append(kb_pool* pool, int32_t layer, uint64_t k, uint64_t v,
 int64_t kb_decode_workspace_bytes(int32_t nseq, int32_t n_q_heads, int32_t max_splits);
 int kb_paged_decode(kb_pool* pool, int32_t layer, int32_t n_q_heads, uint64_t q,
                     uint64_t slots, uint64_t ctx_lens, int32_t nseq, int32_t max_ctx,
-                    float scale, uint64_t out, uint64_t workspace, int32_t max_splits,
-                    int32_t flags, uintptr_t stream);
+                    float scale, uint64_t out, uint64_t workspace, int64_t workspace_bytes,
+                    int32_t max_splits, int32_t flags, uintptr_t stream);
 /* Chunked prefill: for sequence i, q rows [q_off[i], q_off[i]+q_len[i]) are
  * positions [prefix[i], prefix[i]+q_len[i]) of slot slots[i]; they attend
  * causally over pages [0, prefix[i]+q_len[i]) (the chunk's K/V must be
@@ -271,6 +291,18 @@ int kb_paged_prefill(kb_pool* pool, int32_t layer, int32_t n_q_heads, uint64_t q
                      uint64_t slots, uint64_t q_off, uint64_t q_len, uint64_t prefix,
                      int32_t nseq, int32_t max_q_len, float scale, uint64_t out,
                      uint64_t workspace, int32_t kv_splits, uintptr_t stream);
+
+/* ---- parity at production sizes -------------------------------------- */
+/* Position-sensitive content hash of nseg device segments of seg_bytes
+ * bytes (16-byte aligned, multiple of 16): segment i starts at
+ * base + seg_index[i] * seg_bytes (seg_index: device int64 array, or 0 for
+ * i itself).  out (device uint64[nseg]) receives
+ *   H = fmix(S ^ seg_bytes),  S = sum_j fmix(w_j ^ j * 0x9E3779B97F4A7C15)
+ * over the segment's little-endian uint64 words w_j (fmix = splitmix64's
+ * finalizer).  Used to compare whole slabs and every KV page against their
+ * expected contents without host copies; oracle/kvpool.py restates it. */
+int kb_hash_segments(uint64_t base, int64_t seg_bytes, uint64_t seg_index, int32_t nseg,
+                     uint64_t out, uintptr_t stream);
 
 /* ---- decoder-layer elementwise ops for the device-backed engine --------- */
 /* Stage execution of a pipeline member (engine.py:389-397 charges its time):

@@ -172,9 +172,51 @@ def copy_pages(dst: OraclePool, src: OraclePool, moves) -> int:
 
 def bf16_bits_to_f16_bits(x: np.ndarray) -> np.ndarray:
     """bf16 bit patterns -> fp16 bit patterns, round-to-nearest-even (what
-    __floats2half2_rn does in csrc/kb_append.cu)."""
+    __floats2half2_rn does in csrc/kb_append.cu); out-of-range values
+    saturate to inf / flush like the device (which also flags them)."""
     f = (np.asarray(x, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
-    return f.astype(np.float16).view(np.uint16)
+    with np.errstate(over="ignore", under="ignore"):
+        return f.astype(np.float16).view(np.uint16)
+
+
+def v_range_flags(v_bits: np.ndarray) -> int:
+    """KB_KV_V_OVERFLOW (1) / KB_KV_V_UNDERFLOW (2) for bf16 V bit patterns
+    [..., head_dim] (csrc/kb_append.cu): any |v| >= 2^16 (inf / NaN
+    included), or a row (one token, one kv head) whose largest magnitude is
+    nonzero and below 2^-14."""
+    m = np.asarray(v_bits, dtype=np.uint16).astype(np.uint32) & 0x7FFF
+    flags = 0
+    if (m >= 0x4780).any():
+        flags |= 1
+    rmax = m.max(axis=-1)
+    if ((rmax > 0) & (rmax < 0x3880)).any():
+        flags |= 2
+    return flags
+
+
+_PHI = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def _fmix64(z: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * _M1
+        z = (z ^ (z >> np.uint64(27))) * _M2
+    return z ^ (z >> np.uint64(31))
+
+
+def hash_bytes(buf) -> int:
+    """Position-sensitive 64-bit content hash of one segment
+    (csrc/kb_hash.cu kb_hash_segments): fmix(S ^ nbytes) with
+    S = sum_j fmix(w_j ^ j * phi) mod 2^64 over little-endian uint64 words."""
+    a = np.frombuffer(bytes(buf) if not isinstance(buf, np.ndarray) else buf.tobytes(),
+                      dtype="<u8")
+    with np.errstate(over="ignore"):
+        idx = np.arange(a.size, dtype=np.uint64) * _PHI
+        s = np.sum(_fmix64(a ^ idx), dtype=np.uint64)
+    h = _fmix64(np.array([s ^ np.uint64(a.size * 8)], dtype=np.uint64))[0]
+    return int(h.astype(np.int64))  # as the device's int64 view
 
 
 def kv_append(pool: OraclePool, layer: int, k: np.ndarray, v: np.ndarray, slots, pos,

@@ -12,10 +12,23 @@
 
 namespace kb {
 
-// bf16 -> fp16 for 8 packed values (exact for |x| in fp16's normal range;
-// V activations live far inside it).  Storing V as fp16 lets the attention
-// kernels feed P as fp16 (11-bit mantissa) into the P.V tcgen05 MMA, which
-// needs both operands in the same format.
+// bf16 -> fp16 for 8 packed values (exact for |x| in fp16's normal range
+// [2^-14, 65504]; V activations live far inside it).  Storing V as fp16 lets
+// the attention kernels feed P as fp16 (11-bit mantissa) into the P.V
+// tcgen05 MMA, which needs both operands in the same format.
+//
+// The range is GUARDED, not assumed.  A bf16 value's magnitude bits
+// (b & 0x7FFF) order like its magnitude, so with M = the largest magnitude
+// of one token's V row (128 values of one kv head):
+//   KB_KV_V_OVERFLOW   any |v| >= 2^16 (M >= 0x4780; inf / NaN included):
+//                      fp16 would hold inf;
+//   KB_KV_V_UNDERFLOW  0 < M < 2^-14 (0x3880): the whole row sits in fp16's
+//                      subnormal range, where its relative precision is lost.
+// A row whose max is a normal fp16 keeps every element within 2^-11 of M
+// (subnormal elements err by <= 2^-25 <= 2^-11 M), the same bound the normal
+// range gives -- so small entries next to normal ones are fine.  The append
+// kernel ORs the flags into the pool's sticky status word (pinned host
+// memory), which kb_pool_kv_status reports and the host raises on.
 __device__ __forceinline__ int4 bf16x8_to_f16x8(int4 v) {
   uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
 #pragma unroll
@@ -27,13 +40,23 @@ __device__ __forceinline__ int4 bf16x8_to_f16x8(int4 v) {
   return make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
 }
 
+// largest bf16 magnitude field of 8 packed values
+__device__ __forceinline__ uint32_t max_mag8(int4 v) {
+  const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) m = max(m, max(w[i] & 0x7FFFu, (w[i] >> 16) & 0x7FFFu));
+  return m;
+}
+
 // one warp per (token, kv head): lanes 0-15 move K (bf16), lanes 16-31 move
 // V (bf16 in, fp16 stored), 16 bytes each (head_dim 128 = 256 B per row).
 __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __restrict__ bt,
                                  const int4* __restrict__ k, const int4* __restrict__ v,
                                  const int32_t* __restrict__ slots, const int32_t* __restrict__ pos,
                                  int ntok, int Hkv, int B, int L, int maxp, int layer,
-                                 int64_t page_bytes, int64_t row_vec) {
+                                 int64_t page_bytes, int64_t row_vec,
+                                 uint32_t* __restrict__ status) {
   // the attention launch that follows (programmatic dependent launch) may
   // run its prologue now; it waits for this grid's writes before reading
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -51,6 +74,15 @@ __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __rest
                                       ((int64_t)h * B + row) * 256) + (lane & 15);
   const int4 val = *src;
   *dst = which ? bf16x8_to_f16x8(val) : val;
+  // V-row range guard: max magnitude over lanes 16-31 (xor shuffles stay
+  // inside each 16-lane half)
+  uint32_t m = max_mag8(val);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const uint32_t bad = !which ? 0u
+                       : (m >= 0x4780u ? KB_KV_V_OVERFLOW : 0u) |
+                             (m > 0u && m < 0x3880u ? KB_KV_V_UNDERFLOW : 0u);
+  if (lane == 16 && bad) atomicOr_system(status, bad);  // rare: one write per offending row
 }
 
 }  // namespace kb
@@ -74,7 +106,16 @@ extern "C" int kb_kv_append(kb_pool* p, int32_t layer, uint64_t k, uint64_t v, u
       reinterpret_cast<uint8_t*>(p->kva), p->d_bt, reinterpret_cast<const int4*>(k),
       reinterpret_cast<const int4*>(v), reinterpret_cast<const int32_t*>(slots),
       reinterpret_cast<const int32_t*>(pos), ntok, p->m.n_kv_heads, p->m.block_tokens,
-      p->m.num_layers, p->maxp, layer, p->m.page_bytes, stride / 8);
+      p->m.num_layers, p->maxp, layer, p->m.page_bytes, stride / 8, p->d_status);
   KB_LAUNCH_CHECK();
   return pool_leave(p, (cudaStream_t)stream);
+}
+
+extern "C" int kb_pool_kv_status(kb_pool* p, uint32_t* flags, int32_t clear) {
+  if (!p || !flags) return fail(KB_EINVAL, "null argument");
+  if (p->view) return refuse_view();
+  volatile uint32_t* h = p->h_status;
+  *flags = *h;
+  if (clear) *h = 0;
+  return KB_OK;
 }

@@ -121,6 +121,10 @@ struct kb_pool {
   void* d_scratch = nullptr;
   int64_t scratch_bytes = 0;
   int32_t* h_pinned = nullptr;  // small pinned readback buffer
+  // sticky KV status (KB_KV_V_* bits), pinned + mapped: appends OR into it
+  // from the device, the host reads it without a copy (kb_pool_kv_status)
+  uint32_t* h_status = nullptr;
+  uint32_t* d_status = nullptr;
   cudaStream_t own_stream = nullptr;
   // Cross-stream ordering without host synchronization (kb::pool_enter /
   // pool_leave / pool_meta_begin / pool_meta_end): the last pool operation
@@ -142,6 +146,10 @@ struct kb_pool {
 };
 
 namespace kb {
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a property of (kernel,
+// device): opt `fn` in on `device` once (thread-safe; every template
+// instantiation is its own kernel pointer).
+int ensure_smem_attr(const void* fn, int bytes, int device);
 int ensure_scratch(kb_pool* p, int64_t bytes);
 int refuse_view();
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

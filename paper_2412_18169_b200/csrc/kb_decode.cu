@@ -162,8 +162,9 @@ extern "C" int64_t kb_decode_workspace_bytes(int32_t nseq, int32_t n_q_heads, in
 
 extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uint64_t q,
                                uint64_t slots, uint64_t ctx_lens, int32_t nseq, int32_t max_ctx,
-                               float scale, uint64_t out, uint64_t workspace, int32_t max_splits,
-                               int32_t flags, uintptr_t stream) {
+                               float scale, uint64_t out, uint64_t workspace,
+                               int64_t workspace_bytes, int32_t max_splits, int32_t flags,
+                               uintptr_t stream) {
   if (!p) return fail(KB_EINVAL, "null pool");
   if (p->view) return refuse_view();
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
@@ -174,6 +175,13 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   if (max_splits < 1 || max_splits > 64) return fail(KB_EINVAL, "max_splits out of range");
   if (nseq <= 0) return KB_OK;
   (void)max_ctx;
+  // the plan, the split partials and the counters all grow with nseq: a
+  // workspace sized for fewer sequences would be overrun silently
+  const int64_t need = kb_decode_workspace_bytes(nseq, n_q_heads, max_splits);
+  if (!workspace || workspace_bytes < need)
+    return fail(KB_EINVAL, "decode workspace holds " + std::to_string(workspace_bytes) + " < " +
+                               std::to_string(need) + " bytes for " + std::to_string(nseq) +
+                               " sequences");
   KB_RT(cudaSetDevice(p->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t sh = (int64_t)nseq * n_q_heads * max_splits;

@@ -455,12 +455,9 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
   if (B == 64) {
-    static bool attr = false;
-    if (!attr) {
-      KB_RT(cudaFuncSetAttribute(decode_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kDecSmem));
-      attr = true;
-    }
+    int rc = ensure_smem_attr(reinterpret_cast<const void*>(decode_tc_kernel<64>), kDecSmem,
+                              p->device);
+    if (rc) return rc;
     KB_RT(cudaLaunchKernelEx(&cfg, decode_tc_kernel<64>,
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
@@ -469,12 +466,9 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
         part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2));
   } else {
-    static bool attr = false;
-    if (!attr) {
-      KB_RT(cudaFuncSetAttribute(decode_tc_kernel<128>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem));
-      attr = true;
-    }
+    int rc = ensure_smem_attr(reinterpret_cast<const void*>(decode_tc_kernel<128>), kDecSmem,
+                              p->device);
+    if (rc) return rc;
     KB_RT(cudaLaunchKernelEx(&cfg, decode_tc_kernel<128>,
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),

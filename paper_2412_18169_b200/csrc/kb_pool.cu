@@ -27,6 +27,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "kb_common.cuh"
 
@@ -72,6 +75,17 @@ int refuse_view() {
   return fail(KB_EINVAL, "pool is a read-only peer view: its owner process performs this operation");
 }
 
+int ensure_smem_attr(const void* fn, int bytes, int device) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(fn, device, bytes);
+  if (done.count(key)) return KB_OK;
+  KB_RT(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert(key);
+  return KB_OK;
+}
+
 int ensure_scratch(kb_pool* p, int64_t bytes) {
   if (p->scratch_bytes >= bytes) return KB_OK;
   if (p->d_scratch) cudaFree(p->d_scratch);
@@ -102,9 +116,14 @@ int pool_leave(kb_pool* p, cudaStream_t st) {
       KB_RT(cudaEventRecord(se.second, st));
       return KB_OK;
     }
-  if (p->op_ev.size() >= 32) {  // many short-lived streams: fold them
-    KB_RT(cudaDeviceSynchronize());
-    for (auto& se : p->op_ev) cudaEventDestroy(se.second);
+  if (p->op_ev.size() >= 32) {
+    // many short-lived streams: fold them into this one ON THE DEVICE -- st
+    // waits for every other stream's last pool op, so the event recorded
+    // below stands for all of them (no host synchronization)
+    for (auto& se : p->op_ev) {
+      KB_RT(cudaStreamWaitEvent(st, se.second, 0));
+      cudaEventDestroy(se.second);  // released once the wait has resolved
+    }
     p->op_ev.clear();
   }
   cudaEvent_t ev;
@@ -595,6 +614,10 @@ extern "C" int kb_pool_create(int32_t device, const kb_model_desc* model, int64_
   p->h_np.assign(cells, 0);
   if (cudaMallocHost(&p->h_pinned, 64) != cudaSuccess)
     return bail(fail(KB_ECUDA, "cudaMallocHost failed"));
+  if (cudaHostAlloc(&p->h_status, 64, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->d_status), p->h_status, 0) != cudaSuccess)
+    return bail(fail(KB_ECUDA, "cudaHostAlloc(status) failed"));
+  *p->h_status = 0;
   if (cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(KB_ECUDA, "cudaStreamCreate failed"));
   if (cudaEventCreateWithFlags(&p->counts_ev, cudaEventDisableTiming) != cudaSuccess ||
@@ -641,6 +664,7 @@ extern "C" int kb_pool_destroy(kb_pool* p) {
   }
   if (p->d_scratch) cudaFree(p->d_scratch);
   if (p->h_pinned) cudaFreeHost(p->h_pinned);
+  if (p->h_status) cudaFreeHost(p->h_status);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
   for (auto& se : p->op_ev) cudaEventDestroy(se.second);
   if (p->counts_ev) cudaEventDestroy(p->counts_ev);
@@ -1056,3 +1080,18 @@ extern "C" int kb_pool_view_refresh(kb_pool* p, const uint8_t* layer_held, int32
 }
 
 extern "C" int kb_pool_is_view(kb_pool* p) { return p && p->view ? 1 : 0; }
+
+// Work the pool cannot see (a CUDA graph replay: captures record no pool
+// events) brackets itself with these, so the replay waits for the last
+// bitmap op and later releases / compactions wait for the replay.
+extern "C" int kb_pool_stream_begin(kb_pool* p, uintptr_t stream) {
+  if (!p) return fail(KB_EINVAL, "null pool");
+  KB_RT(cudaSetDevice(p->device));
+  return pool_enter(p, (cudaStream_t)stream);
+}
+
+extern "C" int kb_pool_stream_end(kb_pool* p, uintptr_t stream) {
+  if (!p) return fail(KB_EINVAL, "null pool");
+  KB_RT(cudaSetDevice(p->device));
+  return pool_leave(p, (cudaStream_t)stream);
+}

@@ -738,11 +738,9 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
   if (splits > 1 && !workspace) return fail(KB_EINVAL, "kv_splits > 1 needs a workspace");
   dim3 grid((unsigned)(nseq * mtiles), n_q_heads, splits);
   auto launch = [&](auto kernel) -> int {
-    static bool attr = false;
-    if (!attr) {
-      KB_RT(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPfSmem));
-      attr = true;
-    }
+    // per (instantiation, device): <64> and <128> share this lambda's type
+    int arc = ensure_smem_attr(reinterpret_cast<const void*>(kernel), kPfSmem, p->device);
+    if (arc) return arc;
     kernel<<<grid, kPfThreads, kPfSmem, st>>>(
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
         reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(q_off),

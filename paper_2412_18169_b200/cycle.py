@@ -45,10 +45,23 @@ def _span_ms(done) -> float:
 
 @dataclass
 class CycleReport:
+    # device bytes copied (whole pages for KV; slab bytes for parameters)
     bytes_kv_exchange: int = 0
     bytes_param: int = 0
     bytes_kv_consolidate: int = 0
+    # restore-time page compaction inside one pool (not a TransferTask)
     bytes_compaction: int = 0
+    # the reference's payload: sum of TransferTask.size_bytes (exchange.py
+    # share_bytes per flow, plan_restore_transfers shards, consolidation)
+    payload_kv_exchange: int = 0
+    payload_param: int = 0
+    payload_kv_consolidate: int = 0
+    # copy launches alone (events around them, transfer.kernel_spans)
+    kv_copy_ms: float = 0.0
+    kv_copy_bytes: int = 0
+    kv_copy_launches: int = 0
+    param_copy_ms: float = 0.0
+    param_copy_bytes: int = 0
     pages_compacted: int = 0
     remap_ns: int = 0
     n_tasks: int = 0
@@ -60,9 +73,15 @@ class CycleReport:
     param_launches: int = 0        # parameter-pull launches (coalesced runs)
 
     @property
+    def payload_bytes(self) -> int:
+        """Sum of the step's TransferTask.size_bytes: the headline's bytes."""
+        return self.payload_kv_exchange + self.payload_param + self.payload_kv_consolidate
+
+    @property
     def bytes_moved(self) -> int:
-        return (self.bytes_kv_exchange + self.bytes_param + self.bytes_kv_consolidate
-                + self.bytes_compaction)
+        """Device bytes the transfer kernels copied (pages, slabs); the
+        compaction is reported separately (bytes_compaction)."""
+        return self.bytes_kv_exchange + self.bytes_param + self.bytes_kv_consolidate
 
 
 class OverloadCycle:
@@ -146,6 +165,22 @@ class OverloadCycle:
                 w.copy_((torch.randn(n, device=w.device, generator=g) * 0.02).to(torch.bfloat16))
         torch.cuda.synchronize()
 
+    def burst_for(self, seed: int) -> dict:
+        """A queued ShareGPT-shaped burst per replica (traceio.synth_burst
+        lengths) whose KV outgrows the replica's free pool by at least a
+        quarter of one parameter copy: instance -> prompt lengths."""
+        kvbpt = self.model.kv_bytes_per_token
+        trace = synth_burst(10_000.0, 8.0, 32.0, 0.0, 10_000.0, 1660, 373, seed=seed)
+        out, k = {}, 0
+        for iid, inst in sorted(self.instances.items()):
+            need = inst.kv.free_tokens + self.model.param_bytes // 4 // kvbpt
+            lens = []
+            while sum(lens) < need:
+                lens.append(trace[k % len(trace)].input_len)
+                k += 1
+            out[iid] = lens
+        return out
+
     def home_first_pages(self):
         """Device int32 [residents]: each long-lived resident's first layer-0
         page on its home pool after the cycle (the step's result, read back
@@ -177,28 +212,50 @@ class OverloadCycle:
         return bt.view(torch.int32).view(inf.max_slots, self.L, inf.max_pages_per_seq)
 
     def weight_checksums(self) -> dict:
-        torch = self.torch
-        return {(iid, l): int(pool.weight_bytes(l).view(torch.int32).to(torch.int64).sum().item())
-                for iid, pool in self.pools.items() for l in range(self.L)}
+        """(iid, layer) -> position-sensitive 64-bit hash of the layer's whole
+        slab (runtime.hash_segments: every word's position enters the hash,
+        so a permuted or misplaced 16-byte vector changes it)."""
+        out = {}
+        for iid, pool in self.pools.items():
+            with self.torch.cuda.device(pool.rt.device):
+                h = runtime.hash_segments(pool.weight_ptr(0), self.model.bytes_per_layer,
+                                          self.L).cpu().tolist()
+            out.update({(iid, l): h[l] for l in range(self.L)})
+        return out
 
     def kv_checksums(self) -> dict:
-        """Long-lived residents: per (layer, page) int32 sums of the pages on
-        their home instance, in block-table order."""
+        """Long-lived residents: position-sensitive 64-bit hash of every
+        (layer, page) of their KV on their home instance, in block-table
+        order (a page moved to the wrong slot, or bytes moved inside a page,
+        change the vector)."""
         torch = self.torch
         out = {}
         for iid, pool in self.pools.items():
             bt = self._bt_view(iid)
-            kv = pool.kv_bytes().view(torch.int32).view(-1, pool.page_bytes // 4)
-            for rid, home in self.home.items():
+            rids, idx = [], []
+            for rid, home in sorted(self.home.items()):
                 if home != iid or rid in self.transient:
                     continue
                 npg = -(-self.tokens[rid] // self.shape.block_tokens)
-                pages = bt[self.slots[iid].of[rid], :, :npg].reshape(-1).long()
-                out[rid] = kv.index_select(0, pages).to(torch.int64).sum(dim=1).cpu()
+                rids.append((rid, npg * self.L))
+                idx.append(bt[self.slots[iid].of[rid], :, :npg].reshape(-1))
+            if not idx:
+                continue
+            pages = torch.cat(idx).to(torch.int64)
+            h = runtime.hash_segments(pool.info().kv_base, pool.page_bytes, pages.numel(),
+                                      index=pages).cpu()
+            o = 0
+            for rid, n in rids:
+                out[rid] = h[o:o + n]
+                o += n
         return out
 
     # ------------------------------------------------------------------ cycle
-    def step(self) -> CycleReport:
+    def step(self, burst: dict | None = None) -> CycleReport:
+        """One overload cycle.  burst: instance -> prompt lengths of the
+        requests queued on it (the step's input; plan_drop sizes the merge
+        from their KV demand).  Default: a queue that outgrows every
+        replica's free KV by a quarter of one parameter copy."""
         torch = self.torch
         rep = CycleReport()
         st = self.te.bulk
@@ -215,7 +272,8 @@ class OverloadCycle:
         demand = 0
         for i, inst in sorted(self.instances.items()):
             free = inst.kv.free_tokens * kvbpt
-            pending = (free + self.model.param_bytes // 4) // kvbpt
+            pending = (sum(burst[i]) if burst is not None
+                       else (free + self.model.param_bytes // 4) // kvbpt)
             demand += compute_demand(pending, free, kvbpt)
         plan = plan_drop(groups, demand, self.model)
         assert plan.merges and not plan.fallback, plan.to_text()
@@ -400,10 +458,22 @@ class OverloadCycle:
             k = p.task.tid
             if k < x_end:
                 rep.bytes_kv_exchange += p.bytes_moved
+                rep.payload_kv_exchange += p.task.size_bytes
             elif k < r_end:
                 rep.bytes_param += p.bytes_moved
+                rep.payload_param += p.task.size_bytes
             else:
                 rep.bytes_kv_consolidate += p.bytes_moved
+                rep.payload_kv_consolidate += p.task.size_bytes
+        for kind, a, b, nbytes in self.te.kernel_spans:
+            if kind == "kv":
+                rep.kv_copy_ms += a.elapsed_time(b)
+                rep.kv_copy_bytes += nbytes
+                rep.kv_copy_launches += 1
+            else:
+                rep.param_copy_ms += a.elapsed_time(b)
+                rep.param_copy_bytes += nbytes
+        self.te.kernel_spans.clear()
         rep.kv_kernel_ms += _span_ms([p for p in done if p.task.kind is TaskKind.KVCACHE_CHUNK])
         rep.param_kernel_ms += _span_ms([p for p in done if p.task.kind is TaskKind.PARAM_SHARD])
         rep.pages_compacted = sum(self.pools[iid].last_moved_pages for iid in restored)

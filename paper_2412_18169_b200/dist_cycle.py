@@ -47,6 +47,9 @@ class DistReport:
     bytes_compaction: int = 0
     kv_kernel_ms: float = 0.0
     param_kernel_ms: float = 0.0
+    payload_bytes: int = 0         # sum of this rank's TransferTask.size_bytes
+    copy_kernel_ms: float = 0.0    # the copy launches alone (kernel_spans)
+    copy_kernel_bytes: int = 0
     ms: dict = field(default_factory=dict)
 
 
@@ -190,25 +193,35 @@ class DistCycle:
 
     # ------------------------------------------------------------------ checks
     def weight_checksums(self) -> list[int]:
-        torch = self.torch
-        return [int(self.pool.weight_bytes(l).view(torch.int32).to(torch.int64).sum().item())
-                for l in range(self.L)]
+        """Position-sensitive 64-bit hash of every layer slab (kb_hash_segments)."""
+        from .runtime import hash_segments
+        with self.torch.cuda.device(self.device):
+            return hash_segments(self.pool.weight_ptr(0), self.model.bytes_per_layer,
+                                 self.L).cpu().tolist()
 
     def kv_checksums(self) -> dict:
-        """This rank's long-lived home residents: per-page int32 sums."""
+        """This rank's long-lived home residents: position-sensitive hash of
+        every (layer, page), in block-table order."""
         torch = self.torch
         inf = self.pool.info()
-        from .runtime import device_bytes
+        from .runtime import device_bytes, hash_segments
         bt = device_bytes(inf.block_table, inf.max_slots * self.L * inf.max_pages_per_seq * 4)
         bt = bt.view(torch.int32).view(inf.max_slots, self.L, inf.max_pages_per_seq)
-        kv = self.pool.kv_bytes().view(torch.int32).view(-1, self.pool.page_bytes // 4)
-        out = {}
-        for rid, home in self.home.items():
+        rids, idx = [], []
+        for rid, home in sorted(self.home.items()):
             if home != self.me or rid in self.transient:
                 continue
             npg = -(-self.tokens[rid] // self.shape.block_tokens)
-            pages = bt[self.slots[self.me].of[rid], :, :npg].reshape(-1).long()
-            out[rid] = kv.index_select(0, pages).to(torch.int64).sum(dim=1).cpu()
+            rids.append((rid, npg * self.L))
+            idx.append(bt[self.slots[self.me].of[rid], :, :npg].reshape(-1))
+        out = {}
+        if idx:
+            pages = torch.cat(idx).to(torch.int64)
+            h = hash_segments(inf.kv_base, self.pool.page_bytes, pages.numel(), index=pages).cpu()
+            o = 0
+            for rid, n in rids:
+                out[rid] = h[o:o + n]
+                o += n
         return out
 
     # ------------------------------------------------------------------- cycle
@@ -374,8 +387,13 @@ class DistCycle:
             else:
                 rep.bytes_kv_consolidate += p.bytes_moved
             rep.bytes_pulled += p.bytes_moved
+            rep.payload_bytes += p.task.size_bytes
             if p.task.src != self.me:
                 rep.bytes_pulled_peer += p.bytes_moved
+        for _, a, b, nbytes in self.te.kernel_spans:
+            rep.copy_kernel_ms += a.elapsed_time(b)
+            rep.copy_kernel_bytes += nbytes
+        self.te.kernel_spans.clear()
         rep.kv_kernel_ms = _span_ms([p for p in done if p.task.kind is TaskKind.KVCACHE_CHUNK])
         rep.param_kernel_ms = _span_ms([p for p in done if p.task.kind is TaskKind.PARAM_SHARD])
         ev["cons"].synchronize()
@@ -400,6 +418,7 @@ class DistCycle:
         and the transport checksums."""
         import torch
         from .dist import ActChannel
+        from .runtime import hash_tensor
         from .serving import StageRunner
         g = final[self.me]
         members = list(g.member_instances)
@@ -436,13 +455,13 @@ class DistCycle:
                     x = runner.run(lo, hi, inputs[k], b)
                     chan.send(x.contiguous())
                     if record:
-                        sums.append(x.view(torch.int16).to(torch.int64).sum())
+                        sums.append(hash_tensor(x.contiguous())[0])
                 else:
                     raw = chan.recv(b["n"] * H * 2)
                     x = raw.view(torch.bfloat16).view(b["n"], H).clone()
                     chan.done()
                     if record:
-                        sums.append(x.view(torch.int16).to(torch.int64).sum())
+                        sums.append(hash_tensor(x)[0])
                     runner.run(lo, hi, x, b)
         one_pass(True)  # warm-up (cuBLAS handles, lazy attributes) + checksums
         torch.cuda.synchronize(self.device)
@@ -529,12 +548,19 @@ def run(rt, shape, kv_budget_bytes: int, steps: int, warmup: int, pipeline: bool
                 "groups": len(by_group), "handoff_bit_exact": ok}
     out = {
         "ms_total_max": max_over_ranks(ms, device=dev),
-        "bytes_total": sum_over_ranks(sum(r.bytes_pulled + r.bytes_compaction for r in reps),
-                                      device=dev),
+        # headline bytes: the reference's payload (TransferTask.size_bytes);
+        # page-granular device bytes and the compaction separately
+        "bytes_total": sum_over_ranks(sum(r.payload_bytes for r in reps), device=dev),
+        "bytes_device": sum_over_ranks(sum(r.bytes_pulled for r in reps), device=dev),
+        "bytes_compaction": sum_over_ranks(sum(r.bytes_compaction for r in reps), device=dev),
         "bytes_peer": sum_over_ranks(sum(r.bytes_pulled_peer for r in reps),
                                      device=dev),
         "peer_kernel_ms_max": max_over_ranks(sum(r.kv_kernel_ms + r.param_kernel_ms for r in reps),
                                              device=dev),
+        # the copy launches alone, max over ranks, and the bytes they moved
+        # (all ranks): the NVLink roofline's kernel time
+        "copy_kernel_ms_max": max_over_ranks(sum(r.copy_kernel_ms for r in reps), device=dev),
+        "copy_kernel_bytes": sum_over_ranks(sum(r.copy_kernel_bytes for r in reps), device=dev),
         "parity_fail": sum_over_ranks(0.0 if (w_ok and kv_ok) else 1.0,
                                       device=dev),
         "residents_local": len(k0),

@@ -31,6 +31,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 KB_OK, KB_REFUSED = 0, 1
+KB_KV_V_OVERFLOW, KB_KV_V_UNDERFLOW = 1, 2
 
 
 class ModelDesc(C.Structure):
@@ -86,6 +87,9 @@ _sigs = {
                                  C.POINTER(_P)]),
     "kb_pool_view_refresh": (C.c_int, [_P, C.POINTER(C.c_uint8), C.c_int32]),
     "kb_pool_is_view": (C.c_int, [_P]),
+    "kb_pool_stream_begin": (C.c_int, [_P, _S]),
+    "kb_pool_stream_end": (C.c_int, [_P, _S]),
+    "kb_pool_kv_status": (C.c_int, [_P, C.POINTER(C.c_uint32), C.c_int32]),
     "kb_drop_layers": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P]),
     "kb_restore_begin": (C.c_int, [_P, C.c_int32, C.c_int32, _S, _I64P, _I64P]),
     "kb_restore_complete": (C.c_int, [_P, C.c_int32, C.c_int32]),
@@ -103,6 +107,7 @@ _sigs = {
                                           C.c_int64, _S]),
     "kb_copy_bytes": (C.c_int, [_U, _U, C.c_int64, _S]),
     "kb_copy_pages_host": (C.c_int, [_P, C.POINTER(Move), _P, C.c_int32, _S]),
+    "kb_hash_segments": (C.c_int, [_U, C.c_int64, _U, C.c_int32, _U, _S]),
     "kb_add_rmsnorm": (C.c_int, [_U, _U, _U, _U, C.c_int32, C.c_int32, C.c_float, _S]),
     "kb_silu_mul": (C.c_int, [_U, _U, C.c_int32, C.c_int32, _S]),
     "kb_device_alloc": (C.c_int, [C.c_int32, C.c_int64, C.POINTER(C.c_uint64)]),
@@ -113,7 +118,7 @@ _sigs = {
     "kb_kv_append": (C.c_int, [_P, C.c_int32, _U, _U, _U, _U, C.c_int32, C.c_int64, _S]),
     "kb_decode_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
     "kb_paged_decode": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, C.c_int32, C.c_int32,
-                                  C.c_float, _U, _U, C.c_int32, C.c_int32, _S]),
+                                  C.c_float, _U, _U, C.c_int64, C.c_int32, C.c_int32, _S]),
     "kb_prefill_workspace_bytes": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "kb_paged_prefill": (C.c_int, [_P, C.c_int32, C.c_int32, _U, _U, _U, _U, _U, C.c_int32,
                                    C.c_int32, C.c_float, _U, _U, C.c_int32, _S]),
@@ -138,6 +143,12 @@ class Refused(ValueError):
 # Kernel launches issued by this process through the library (the bench's
 # `gpu_launches` claim): incremented by the wrappers that launch.
 LAUNCHES = [0]
+# Host -> device descriptor bytes this process passed through the C-ABI for
+# device work (block-table grow requests, release slot lists, page-move
+# lists): the per-step host input of the drop / exchange / restore path,
+# which the library ships in kernel parameter space.  bench.py's e2e leg
+# reports it per step.
+H2D_BYTES = [0]
 
 
 def _check(rc: int, launches: int = 0) -> None:
@@ -285,6 +296,37 @@ class DevicePool:
     def restore_complete(self, lo: int, hi: int) -> None:
         _check(_lib.kb_restore_complete(self.h, lo, hi))
 
+    # -- work the pool cannot see (CUDA graph replays)
+    def stream_begin(self, stream=None) -> None:
+        _check(_lib.kb_pool_stream_begin(self.h, _stream(stream)))
+
+    def stream_end(self, stream=None) -> None:
+        _check(_lib.kb_pool_stream_end(self.h, _stream(stream)))
+
+    # -- fp16 V-cache range guard (kb_pool_kv_status)
+    def kv_status(self, clear: bool = False) -> int:
+        """KB_KV_V_* flags of every append that has completed (synchronize
+        the appending stream first for an exact answer)."""
+        f = C.c_uint32()
+        _check(_lib.kb_pool_kv_status(self.h, C.byref(f), 1 if clear else 0))
+        return f.value
+
+    def check_kv_range(self, synchronize: bool = True) -> None:
+        """Raise ValueError if any appended V value fell outside the fp16
+        cache's exact range (|v| in [2^-14, 65504] or 0); clears the flags."""
+        if synchronize:
+            import torch
+            torch.cuda.synchronize(self.rt.device)
+        f = self.kv_status(clear=True)
+        if f:
+            what = []
+            if f & KB_KV_V_OVERFLOW:
+                what.append("|v| >= 65536 (inf in fp16)")
+            if f & KB_KV_V_UNDERFLOW:
+                what.append("0 < |v| < 2^-14 (fp16 subnormal)")
+            raise ValueError(f"pool {self.iid}: V value out of the fp16 KV-cache range: "
+                             + ", ".join(what))
+
     def weight_ptr(self, layer: int) -> int:
         return int(_lib.kb_weight_ptr(self.h, layer))
 
@@ -306,6 +348,7 @@ class DevicePool:
         if not reqs:
             return True
         arr = (Grow * len(reqs))(*[Grow(*r) for r in reqs])
+        H2D_BYTES[0] += C.sizeof(arr)
         try:
             _check(_lib.kb_pages_grow(self.h, arr, len(reqs), _stream(stream)),
                    launches=-(-len(reqs) // 256))
@@ -316,6 +359,7 @@ class DevicePool:
     def release(self, slots: Sequence[int], lo: int, hi: int, stream=None) -> None:
         if not slots:
             return
+        H2D_BYTES[0] += 4 * len(slots)
         _check(_lib.kb_pages_release(self.h, _i32arr(slots), len(slots), lo, hi,
                                      _stream(stream)), launches=-(-len(slots) // 1024))
 
@@ -425,12 +469,14 @@ def copy_pages(dst: DevicePool, src: DevicePool,
     if not moves:
         return
     arr = (Move * len(moves))(*[Move(*m, 0) for m in moves])
+    H2D_BYTES[0] += C.sizeof(arr)
     _check(_lib.kb_copy_pages(dst.h, src.h, arr, len(moves), _stream(stream)),
            launches=-(-len(moves) // 256))
 
 
 def copy_slabs(dst: DevicePool, src: DevicePool, lo: int, hi: int, byte_lo: int,
                byte_hi: int, stream=None) -> None:
+    H2D_BYTES[0] += 24  # (lo, hi, byte_lo, byte_hi)
     _check(_lib.kb_copy_slabs(dst.h, src.h, lo, hi, byte_lo, byte_hi, _stream(stream)),
            launches=1)
 
@@ -489,6 +535,35 @@ class IpcBuffer:
             self.ptr = 0
 
 
+def hash_segments(base_ptr: int, seg_bytes: int, nseg: int, index=None, stream=None):
+    """Position-sensitive 64-bit hash of nseg device segments (int64 torch
+    tensor on the segments' device; see kb_hash_segments).  `index`: device
+    int64 tensor of segment numbers (segment i at base + index[i] * seg_bytes),
+    or None for 0..nseg-1."""
+    import torch
+    dev = index.device if index is not None else torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty(max(nseg, 0), dtype=torch.int64, device=dev)
+    if nseg <= 0:
+        return out
+    if index is not None and (index.dtype != torch.int64 or not index.is_contiguous()):
+        index = index.to(torch.int64).contiguous()
+    _check(_lib.kb_hash_segments(base_ptr, seg_bytes, 0 if index is None else index.data_ptr(), nseg,
+                                 out.data_ptr(), _stream(stream)), launches=2)
+    return out
+
+
+def hash_tensor(t, seg_bytes: Optional[int] = None, stream=None):
+    """hash_segments over a contiguous device tensor cut into seg_bytes
+    segments (default: one segment)."""
+    nbytes = t.numel() * t.element_size()
+    seg = seg_bytes or nbytes
+    if nbytes % seg:
+        raise ValueError("tensor size is not a multiple of the segment size")
+    import torch
+    with torch.cuda.device(t.device):
+        return hash_segments(t.data_ptr(), seg, nbytes // seg, stream=stream)
+
+
 def add_rmsnorm(x, res, w, out, eps: float = 1e-5, stream=None) -> None:
     """x (+)= res in place (res None: no add); out = rmsnorm(x) * w (bf16 rows)."""
     _check(_lib.kb_add_rmsnorm(x.data_ptr(), 0 if res is None else res.data_ptr(), w.data_ptr(),
@@ -538,7 +613,8 @@ def paged_decode(pool: DevicePool, layer: int, q, slots, ctx_lens, max_ctx: int,
     fused = q.shape[0] * pool.shape.n_kv_heads >= 4 * _sm_count(pool.rt.device)
     _check(_lib.kb_paged_decode(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
                                 ctx_lens.data_ptr(), q.shape[0], max_ctx, scale,
-                                out.data_ptr(), workspace.data_ptr(), max_splits, flags,
+                                out.data_ptr(), workspace.data_ptr(),
+                                workspace.numel() * workspace.element_size(), max_splits, flags,
                                 _stream(stream)),
            launches=(1 if reuse_plan else 2) + (0 if fused else 1))
 

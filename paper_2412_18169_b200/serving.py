@@ -147,7 +147,12 @@ class StageRunner:
         st["x"].copy_(x)
         for k in ("slots", "pos", "d_slots", "d_ctx"):
             st[k].copy_(batch[k])
+        # a replay is invisible to the pool's stream ordering (captures record
+        # no pool events): wait for its last bitmap op, and let later releases
+        # / compactions wait for the replay
+        self.pool.stream_begin()
         g.replay()
+        self.pool.stream_end()
         return st["out"]
 
     def run(self, lo: int, hi: int, x, batch: dict):
@@ -193,7 +198,7 @@ class StageRunner:
 
 class DeviceEngine(Engine):
     def __init__(self, cfg, trace, policy: Optional[str] = None, seed: int = 0,
-                 runtimes: Optional[dict] = None, max_seqs: int = 512):
+                 runtimes: Optional[dict] = None, max_seqs: Optional[int] = None):
         import torch
         self.torch = torch
         pol = policy or cfg.policy.kind
@@ -213,7 +218,9 @@ class DeviceEngine(Engine):
         self.transfer_hook = self._run_task
         for iid, inst in self.instances.items():
             init_weights(inst.pool, self.shape, inst.table.layers_held())
-        self.runners = {iid: StageRunner(p, self.shape, max_seqs=max_seqs)
+        # a decode microbatch can hold every slot of a pool: size the
+        # attention workspace for that (paged_decode refuses a smaller one)
+        self.runners = {iid: StageRunner(p, self.shape, max_seqs=max_seqs or cfg.device.max_slots)
                         for iid, p in self.pools.items()}
         self.emb = {}
         for d in set(cfg.device.devices):
@@ -448,6 +455,8 @@ class DeviceEngine(Engine):
                 e.record(st)
                 events.append((s, k, a, e, b["n"], b["units"], b["nd"], hi - lo))
         e.synchronize()
+        for iid in members:  # the fp16 V cache's range guard (kb_pool_kv_status)
+            self.pools[iid].check_kv_range(synchronize=False)
         times = [[1] * len(mbs) for _ in members]
         for s, k, a, e, n, units, nd, layers in events:
             us = max(1, int(round(a.elapsed_time(e) * 1000)))

@@ -121,6 +121,10 @@ class TransferEngine:
         self.pending: deque[Pending] = deque()
         self.stats = TransferStats()
         self.timing = timing
+        # timing=True: (kind, start, end, bytes) events around the copy
+        # launches alone of every burst (the roofline's kernel time: no grow
+        # or queueing inside), kind "kv" (copy_pages) or "param" (slab pulls)
+        self.kernel_spans: list = []
         # swapped-out KV (HOST endpoint): rid -> (pinned tensor, layers, npages)
         self.host_kv: dict[int, tuple] = {}
 
@@ -298,10 +302,29 @@ class TransferEngine:
                 self.stats.param_bytes += t.size_bytes
             else:
                 raise ValueError("activation tasks go through submit_activation")
-        for (s, d), moves in pairs.items():
-            runtime.copy_pages(self.pools[d], self.pools[s], moves, stream=stream)
-        for (src, dst, layers), a, b in runs:
-            self._copy_param(src, dst, layers, a, b, stream)
+        def span(kind, nbytes, launch):
+            if not self.timing:
+                launch()
+                return
+            a_ev = torch.cuda.Event(enable_timing=True)
+            b_ev = torch.cuda.Event(enable_timing=True)
+            a_ev.record(stream)
+            launch()
+            b_ev.record(stream)
+            self.kernel_spans.append((kind, a_ev, b_ev, nbytes))
+        if self.timing and grows:
+            stream.wait_stream(self.meta)  # the grows land before the span starts
+        if pairs:
+            def kv_launch():
+                for (s, d), moves in pairs.items():
+                    runtime.copy_pages(self.pools[d], self.pools[s], moves, stream=stream)
+            span("kv", sum((m[6] - m[5]) * self.pools[s].page_bytes
+                           for (s, _), ms in pairs.items() for m in ms), kv_launch)
+        if runs:
+            def param_launch():
+                for (src, dst, layers), a, b in runs:
+                    self._copy_param(src, dst, layers, a, b, stream)
+            span("param", sum(b - a for _, a, b in runs), param_launch)
         self.stats.param_launches += len(runs)
         ev = torch.cuda.Event(enable_timing=self.timing)
         ev.record(stream)

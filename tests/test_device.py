@@ -481,7 +481,7 @@ def test_paged_decode_plan_reuse_across_layers(rt, batch):
 
 
 @pytest.mark.parametrize("kv_splits", [1, 3, 8])
-@pytest.mark.parametrize("shape", ATTN_SHAPES[:2], ids=lambda s: s.name)
+@pytest.mark.parametrize("shape", ATTN_SHAPES, ids=lambda s: s.name)
 def test_paged_prefill_matches_oracle(rt, shape, kv_splits):
     from paper_2412_18169_b200 import runtime
     model = shape.spec()
@@ -529,7 +529,8 @@ def test_attention_at_full_context_sampled_rows():
     are checked against it; every head of each sampled row."""
     from paper_2412_18169_b200 import runtime
     rt32 = runtime.Runtime(0, max_slots=4, max_pages_per_seq=520, slack_pages=64)
-    shape = ATTN_SHAPES[1]  # Qwen2.5-14B heads: 40 q / 8 kv
+    shape = ATTN_SHAPES[2]  # Qwen2.5-14B heads: 40 q / 8 kv (GQA group 5)
+    assert (shape.n_q_heads, shape.n_kv_heads) == (40, 8)
     model = shape.spec()
     pool = rt32.create_pool(0, model, model.param_bytes + 400 * MIB, shape)
     gen = torch.Generator().manual_seed(32)
@@ -546,7 +547,9 @@ def test_attention_at_full_context_sampled_rows():
     dev = lambda xs: torch.tensor(xs, dtype=torch.int32, device="cuda")  # noqa: E731
     q = rand_bf16((c, hq, 128), gen)
     rows = [0, 1, 63, 64, 127, 128, 129, 1000, 1023, 1024, 1535, 2046, 2047]
-    for kv_splits in (None, 1, 8):
+    # None: the split count the runtime picks for this geometry (the bench's)
+    assert runtime.prefill_splits(1, hq, c, n) == 4
+    for kv_splits in (None, 1, 4, 8):
         out = torch.zeros((c, hq, 128), dtype=torch.bfloat16, device="cuda")
         kw = {"max_kv_len": n} if kv_splits is None else {"kv_splits": kv_splits}
         runtime.paged_prefill(pool, 0, q.cuda(), dev([0]), dev([0]), dev([c]), dev([pre]), c, out,
