@@ -6,6 +6,7 @@ engine runs are comparable; B200 additions live in `DeviceConfig`.
 
 from __future__ import annotations
 
+import configparser
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -15,6 +16,7 @@ from .traceio import TRACE_PRESETS  # noqa: F401  (re-export, ref config.py:20-2
 
 POLICIES = ("kunserve", "recompute", "swap", "migrate")
 FORMULATIONS = ("auto", "lookahead", "token_count")
+LENGTH_DISTS = ("fixed", "uniform", "lognormal")
 
 
 class ConfigError(ValueError):
@@ -103,6 +105,15 @@ def validate(cfg: SimConfig) -> None:
     if cfg.policy.formulation not in FORMULATIONS:
         raise ConfigError("policy.formulation",
                           f"unknown formulation {cfg.policy.formulation!r}")
+    if cfg.trace.source not in ("synth", "file"):
+        raise ConfigError("trace.source", f"unknown source {cfg.trace.source!r}")
+    if cfg.trace.source == "file" and not cfg.trace.path:
+        raise ConfigError("trace.path", "required when trace.source = file")
+    if cfg.trace.length_dist not in LENGTH_DISTS:
+        raise ConfigError("trace.length_dist", f"unknown distribution {cfg.trace.length_dist!r}")
+    if cfg.trace.preset and cfg.trace.preset not in TRACE_PRESETS:
+        raise ConfigError("trace.preset", f"unknown preset {cfg.trace.preset!r}, "
+                                          f"expected one of {', '.join(sorted(TRACE_PRESETS))}")
     if not 0.0 < cfg.policy.restore_threshold <= 1.0:
         raise ConfigError("policy.restore_threshold", "must be in (0, 1]")
     if cfg.cluster.instances < 1:
@@ -111,3 +122,92 @@ def validate(cfg: SimConfig) -> None:
         raise ConfigError("cluster.initial_group_size", "must divide cluster.instances")
     if cfg.model.param_bytes >= cfg.cluster.hbm_bytes:
         raise ConfigError("cluster.hbm_bytes", "must exceed one parameter copy")
+
+
+# ---------------------------------------------------------------- INI loader
+def _num(conv):
+    def parse(raw: str, name: str):
+        try:
+            return conv(float(raw)) if conv is int else conv(raw)
+        except ValueError as exc:
+            raise ConfigError(name, f"not a number: {raw!r}") from exc
+    return parse
+
+
+def _flag(raw: str, name: str) -> bool:
+    v = raw.strip().lower()
+    if v in ("1", "true", "yes", "on"):
+        return True
+    if v in ("0", "false", "no", "off"):
+        return False
+    raise ConfigError(name, f"not a boolean: {raw!r}")
+
+
+def _text(raw: str, name: str) -> str:
+    return raw.strip()
+
+
+# (section, key) -> (dataclass path, converter); ints accept scientific
+# notation (hbm_bytes = 24e9), like the reference (config.py:95-99)
+_FIELDS = {
+    "cluster": {k: _num(int) for k in ("instances", "hbm_bytes", "nic_bandwidth", "host_bandwidth",
+                                       "link_base_latency_us", "map_latency_us",
+                                       "initial_group_size")},
+    "policy": {"kind": _text, "formulation": _text, "token_budget": _num(int),
+               "min_batch_tokens": _num(int), "restore_threshold": _num(float),
+               "monitor_tick_us": _num(int), "autoscale_occupancy": _num(float),
+               "autoscale_window_s": _num(float)},
+    "trace": {"source": _text, "path": _text, "seed": _num(int), "duration_s": _num(float),
+              "base_rps": _num(float), "burst_rps": _num(float), "burst_start_s": _num(float),
+              "burst_end_s": _num(float), "length_dist": _text, "input_mean": _num(int),
+              "output_mean": _num(int), "sigma": _num(float), "preset": _text,
+              "rescale_factor": _num(float)},
+    "report": {"window_s": _num(float), "figures": _flag, "drain_s": _num(float)},
+}
+
+
+def load_config(path: str) -> SimConfig:
+    """INI file -> SimConfig (ref config.py:150-240): sections [model]
+    [cluster] [policy] [trace] [report], every key optional over the
+    desk-scale defaults; [model] also carries the cost coefficients (alpha,
+    beta, gamma, batch_discount); policy.slo_scales is a comma list; a trace
+    preset overrides the length means.  Bad values raise ConfigError naming
+    the field; the result is validated."""
+    ini = configparser.ConfigParser(inline_comment_prefixes=("#", ";"))
+    if not ini.read(path):
+        raise ConfigError("config", f"cannot read {path}")
+    cfg = SimConfig()
+
+    def get(section, key, conv, default):
+        if not ini.has_option(section, key):
+            return default
+        return conv(ini.get(section, key), f"{section}.{key}")
+
+    m, c = cfg.model, cfg.cost
+    cfg.model = ModelSpec(num_layers=get("model", "num_layers", _num(int), m.num_layers),
+                          bytes_per_layer=get("model", "bytes_per_layer", _num(int),
+                                              m.bytes_per_layer),
+                          kv_bytes_per_token=get("model", "kv_bytes_per_token", _num(int),
+                                                 m.kv_bytes_per_token),
+                          hidden_bytes_per_token=get("model", "hidden_bytes_per_token",
+                                                     _num(int), m.hidden_bytes_per_token))
+    cfg.cost = CostCoefficients(alpha=get("model", "alpha", _num(float), c.alpha),
+                                beta=get("model", "beta", _num(float), c.beta),
+                                gamma=get("model", "gamma", _num(float), c.gamma),
+                                batch_discount=get("model", "batch_discount", _num(float),
+                                                   c.batch_discount))
+    for section, keys in _FIELDS.items():
+        obj = getattr(cfg, section)
+        for key, conv in keys.items():
+            setattr(obj, key, get(section, key, conv, getattr(obj, key)))
+    if ini.has_option("policy", "slo_scales"):
+        raw = ini.get("policy", "slo_scales")
+        cfg.policy.slo_scales = tuple(_num(float)(x.strip(), "policy.slo_scales")
+                                      for x in raw.split(",") if x.strip())
+    t = cfg.trace
+    if t.preset:
+        if t.preset not in TRACE_PRESETS:
+            raise ConfigError("trace.preset", f"unknown preset {t.preset!r}")
+        t.input_mean, t.output_mean = TRACE_PRESETS[t.preset]
+    validate(cfg)
+    return cfg

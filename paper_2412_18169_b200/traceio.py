@@ -93,3 +93,37 @@ def save_trace(path: str, records: list[TraceRecord]) -> None:
         w.writerow(HEADER)
         for r in records:
             w.writerow([f"{r.arrival_us / 1_000_000:.6f}", r.input_len, r.output_len])
+
+
+def rescale(records: list[TraceRecord], factor: float, seed: int = 0) -> list[TraceRecord]:
+    """Scale a trace's arrival rate, keeping its temporal shape (ref
+    traceio.py:71-117).  factor < 1 keeps original i iff floor((i+1)f) >
+    floor(i f); factor > 1 adds ceil(f)-1 jittered replicas per arrival
+    (jitter drawn in [0, gap//2] from seed, gap = the local inter-arrival
+    gap, at least 2 us) and keeps round(n f) - n of them, evenly spaced over
+    the replica list; the result is sorted by (arrival, input, output)."""
+    if factor <= 0:
+        raise ValueError("rescale factor must be > 0")
+    n = len(records)
+    if n == 0 or factor == 1.0:
+        return list(records)
+    if factor < 1.0:
+        return [r for i, r in enumerate(records)
+                if math.floor((i + 1) * factor) > math.floor(i * factor)]
+    rng = random.Random(seed)
+    copies = math.ceil(factor) - 1
+    extra: list[TraceRecord] = []
+    for i, r in enumerate(records):
+        if i + 1 < n:
+            gap = records[i + 1].arrival_us - r.arrival_us
+        else:
+            gap = r.arrival_us - records[i - 1].arrival_us if i > 0 else 2
+        gap = max(gap, 2)
+        extra += [TraceRecord(r.arrival_us + rng.randrange(0, gap // 2 + 1), r.input_len,
+                              r.output_len) for _ in range(copies)]
+    want = int(round(n * factor)) - n
+    if want < 0:
+        raise ValueError("factor > 1 cannot shrink a trace")
+    want = min(want, len(extra))
+    picked = [extra[(j * len(extra)) // want] for j in range(want)]
+    return sorted(list(records) + picked, key=lambda r: (r.arrival_us, r.input_len, r.output_len))
