@@ -155,6 +155,53 @@ class StageRunner:
         self.pool.stream_end()
         return st["out"]
 
+    # -- padded decode graphs (wall-clock serving) ------------------------
+    # A decode-only microbatch of n rows replays the graph of the smallest
+    # bucket >= n; the extra rows decode a reserved dummy slot (one page per
+    # layer, context 1) from zero activations, so their K/V land in the dummy
+    # page and their outputs are dropped.  Graphs are captured ahead of time
+    # (capture_padded), so serving never captures.
+    def padded_batch(self, batch: dict, n_pad: int, dummy_slot: int) -> dict:
+        torch = self.torch
+        n = batch["n"]
+        extra = n_pad - n
+        dev = batch["slots"].device
+
+        def pad(t, val):
+            return torch.cat([t, torch.full((extra,), val, dtype=t.dtype, device=dev)]) \
+                if extra else t
+        return dict(batch, n=n_pad, nd=n_pad, slots=pad(batch["slots"], dummy_slot),
+                    pos=pad(batch["pos"], 0), d_slots=pad(batch["d_slots"], dummy_slot),
+                    d_ctx=pad(batch["d_ctx"], 1),
+                    d_rows=torch.arange(n_pad, dtype=torch.int64, device=dev),
+                    last=torch.arange(n_pad, dtype=torch.int64, device=dev),
+                    d_max=max(batch["d_max"], 1))
+
+    def capture_padded(self, lo: int, hi: int, n_pad: int, dummy_slot: int) -> None:
+        torch = self.torch
+        dev = self.pool.rt.device
+        i32 = lambda v: torch.full((n_pad,), v, dtype=torch.int32, device=f"cuda:{dev}")  # noqa: E731
+        b = {"n": n_pad, "np": 0, "nd": n_pad, "n_prefill_rows": 0, "slots": i32(dummy_slot),
+             "pos": i32(0), "d_slots": i32(dummy_slot), "d_ctx": i32(1), "d_max": 1,
+             "d_rows": torch.arange(n_pad, dtype=torch.int64, device=f"cuda:{dev}")}
+        x = torch.zeros((n_pad, self.shape.hidden), dtype=torch.bfloat16, device=f"cuda:{dev}")
+        self.prepare_decode_graph(lo, hi, x, b)
+
+    def run_padded_decode(self, lo: int, hi: int, x, batch: dict, n_pad: int):
+        """Replay the (lo, hi, n_pad) graph for the first batch["n"] rows of
+        `batch` (already padded with padded_batch); returns a fresh [n, hidden]
+        tensor (the graph's static output is overwritten by the next replay)."""
+        g, st = self._graphs[(lo, hi, n_pad)]
+        n = x.shape[0]
+        st["x"][:n].copy_(x)
+        st["x"][n:].zero_()
+        for k in ("slots", "pos", "d_slots", "d_ctx"):
+            st[k].copy_(batch[k])
+        self.pool.stream_begin()
+        g.replay()
+        self.pool.stream_end()
+        return st["out"][:n].clone()
+
     def run(self, lo: int, hi: int, x, batch: dict):
         """Layers [lo, hi) over the microbatch rows x (bf16 [n, hidden],
         updated in place as the residual stream)."""
@@ -216,6 +263,11 @@ class DeviceEngine(Engine):
         self.slots = {i: SlotTable(cfg.device.max_slots) for i in self.instances}
         self.te = TransferEngine(self.pools, self.slots)
         self.transfer_hook = self._run_task
+        # stream of block-table grows / releases (the transfer stream: a grow
+        # always sees every earlier release; the wall-clock engine moves them
+        # to the transfer engine's meta stream so they do not queue behind
+        # KV bursts -- the pool orders bitmap ops on the device either way)
+        self.page_stream = self.te.bulk
         for iid, inst in self.instances.items():
             init_weights(inst.pool, self.shape, inst.table.layers_held())
         # a decode microbatch can hold every slot of a pool: size the
@@ -251,7 +303,7 @@ class DeviceEngine(Engine):
                     reqs.append((slot, l, l + 1, add))
         # page ops share one stream (the transfer stream) so a grow always
         # sees every earlier release; execution waits on that stream
-        if reqs and not pool.grow(reqs, stream=self.te.bulk):
+        if reqs and not pool.grow(reqs, stream=self.page_stream):
             raise runtime.DeviceError(f"instance {iid}: out of KV pages for request {rid} "
                                       "(page slack exhausted)")
 
@@ -269,7 +321,7 @@ class DeviceEngine(Engine):
         for iid, slots in self.slots.items():
             slot = slots.of.get(rid)
             if slot is not None:
-                self.pools[iid].release([slot], 0, L, stream=self.te.bulk)
+                self.pools[iid].release([slot], 0, L, stream=self.page_stream)
                 slots.drop(rid)
 
     def group_free(self, grun: GroupRun, rid: int) -> None:
@@ -287,8 +339,15 @@ class DeviceEngine(Engine):
                                           self.requests[task.rid].context_len)
         self.te.submit(task)
 
+    def _transfers_landed(self) -> None:
+        """Called when the engine's clock says a transfer finished: the
+        simulated clock runs ahead of the device, so wait for the copies
+        (the wall-clock engine only fires the callback once the task's own
+        event completed, so there it just collects finished tasks)."""
+        self.te.drain()
+
     def _swap_in_done(self, gid, task, when) -> None:
-        self.te.drain()             # the host copy has been read
+        self._transfers_landed()    # the host copy has been read
         self.te.release_host(task.rid)
         super()._swap_in_done(gid, task, when)
 
@@ -338,7 +397,7 @@ class DeviceEngine(Engine):
             self.te.submit_many(extra)
 
     def _fetch_done(self, gid, task, when) -> None:
-        self.te.drain()
+        self._transfers_landed()
         key = (task.dst, task.layers)
         if key in self.fetch_left:
             self.fetch_left[key] -= 1
@@ -348,28 +407,31 @@ class DeviceEngine(Engine):
         super()._fetch_done(gid, task, when)
 
     def _exchange_chunk_done(self, task, when) -> None:
-        self.te.drain()
+        self._transfers_landed()
         self.te.finish_flow_sources()
         super()._exchange_chunk_done(task, when)
 
     def _restore_chunk_done(self, gid, task, when) -> None:
-        self.te.drain()  # the slab bytes land before complete_restore flips ownership
+        self._transfers_landed()  # the slab bytes land before complete_restore flips ownership
         super()._restore_chunk_done(gid, task, when)
 
     def _on_consolidation_planned(self, rid, peer, home, layers, tasks) -> None:
         self.te.register_chunked_kv(tasks, layers, {rid: self.requests[rid].context_len})
 
     def _on_consolidated(self, rid, peers) -> None:
-        self.te.drain()
+        self._transfers_landed()
         self.te.finish_flow_sources()
         L = self.model.num_layers
         for iid in peers:
             slot = self.slots[iid].of.get(rid)
             if slot is not None:
-                self.pools[iid].release([slot], 0, L, stream=self.te.bulk)
+                self.pools[iid].release([slot], 0, L, stream=self.page_stream)
                 self.slots[iid].drop(rid)
 
     # ---------------------------------------------------------- execution
+    def _to_device(self, xs, dtype, dev):
+        return self.torch.tensor(xs, dtype=dtype, device=dev)
+
     def _batch(self, iid: int, mb) -> dict:
         torch = self.torch
         dev = f"cuda:{self._dev_of(iid)}"
@@ -405,8 +467,8 @@ class DeviceEngine(Engine):
                 p_prefix.append(p)
                 row += c
                 last_rows.append(row - 1)
-        i32 = lambda xs: torch.tensor(xs, dtype=torch.int32, device=dev)  # noqa: E731
-        i64 = lambda xs: torch.tensor(xs, dtype=torch.int64, device=dev)  # noqa: E731
+        i32 = lambda xs: self._to_device(xs, torch.int32, dev)  # noqa: E731
+        i64 = lambda xs: self._to_device(xs, torch.int64, dev)  # noqa: E731
         return {"n": row, "slots": i32(slots), "pos": i32(pos), "n_prefill_rows": n_prefill_rows,
                 "np": len(p_slots), "p_rows": i64(p_rows), "p_slots": i32(p_slots),
                 "p_off": i32(p_off), "p_len": i32(p_len), "p_prefix": i32(p_prefix),

@@ -1,11 +1,16 @@
 """P99 TTFT under an overload burst on the B200 (BASELINE metric 1).
 
-Runs serving.DeviceEngine -- the reference's scheduler with real pools,
-page tables, device transfers and MEASURED stage times -- on a synthetic
-4x ShareGPT-shaped burst (traceio.synth_burst, the reference's generator),
-once with KunServe's policy and once with the recompute baseline, and reports
-nearest-rank P99 TTFT from the event logs (metrics.collect, the reference's
-metric code path).
+Runs the reference's scheduler on real Llama-3-8B pools against a synthetic
+4x ShareGPT-shaped burst (traceio.synth_burst, the reference's generator)
+with KunServe's policy and the reference's three baselines, and reports
+nearest-rank P99 TTFT / P50 TPOT from the event logs (metrics.collect, the
+reference's metric code path).
+
+clock="wall" (default): realtime.WallClockEngine -- arrivals on the wall
+clock, stages and transfers executing concurrently on the GPU, every token
+time a CUDA-event timestamp.  clock="sim": serving.DeviceEngine -- the same
+device work executed stage by stage, its measured durations fed to the
+reference's discrete-event clock, links on the link model (r1's mode).
 """
 
 from __future__ import annotations
@@ -13,7 +18,7 @@ from __future__ import annotations
 import time
 
 from .core import SHAPES
-from .metrics import collect, percentile
+from .metrics import bubble_ratio, collect, percentile
 from .serving import DeviceEngine, device_config
 from .traceio import synth_burst
 
@@ -25,7 +30,8 @@ def burst_trace(duration_s: float = 20.0, base_rps: float = 1.0, burst_factor: f
                        duration_s * 3 / 4, input_mean, output_mean, "lognormal", 0.6, seed)
 
 
-def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None, cost=None) -> dict:
+def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None, cost=None,
+               clock: str = "wall") -> dict:
     """cost: CostCoefficients for the scheduler's planning (lookahead
     microbatch formulation, exchange chunk sizing); stage times themselves
     are always measured."""
@@ -35,7 +41,12 @@ def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None, cost=Non
         cfg.cost = cost
     cfg.report.drain_s = 60.0
     t0 = time.perf_counter()
-    eng = DeviceEngine(cfg, trace, runtimes=runtimes)
+    if clock == "wall":
+        from .realtime import WallClockEngine
+        eng = WallClockEngine(cfg, trace, runtimes=runtimes)
+    else:
+        eng = DeviceEngine(cfg, trace, runtimes=runtimes)
+    t1 = time.perf_counter()
     res = eng.run()
     wall = time.perf_counter() - t0
     st = collect(res.log_lines)
@@ -59,10 +70,14 @@ def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None, cost=Non
            "drops": res.drop_events, "evictions": res.evictions,
            "exchanges": kinds.get("EXCHANGE", 0), "restores": kinds.get("RESTORE_DONE", 0),
            "rounds": kinds.get("ROUND", 0), "stages_measured": len(eng.stage_samples),
-           "wall_s": round(wall, 1)}
-    out["cost_fit"] = fit_stage_samples(eng.stage_samples, shape.num_layers)
+           "bubble_ratio": round(bubble_ratio(res.log_lines), 4),
+           "clock": clock, "wall_s": round(wall, 1), "setup_s": round(t1 - t0, 1)}
+    fit = fit_stage_samples(eng.stage_samples, shape.num_layers)
+    if fit:
+        out["cost_fit"] = {k: fit[k] for k in ("alpha", "beta", "gamma")}
     for pool in eng.pools.values():
         pool.close()
+    out["_log"] = res.log_lines
     return out, eng.stage_samples
 
 
@@ -84,13 +99,14 @@ def fit_stage_samples(samples, num_layers: int) -> dict:
 
 
 def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b",
-            policies=("kunserve", "recompute", "swap", "migrate"), **trace_kw) -> dict:
+            policies=("kunserve", "recompute", "swap", "migrate"), clock: str = "wall",
+            keep_logs: bool = False, **trace_kw) -> dict:
     shape = SHAPES[shape_name]
     trace = burst_trace(**trace_kw)
     # warm-up: load every kernel / cuBLAS heuristic and walk one drop cycle
     # so the measured runs see steady-state stage times
     warm = burst_trace(duration_s=4.0, base_rps=4.0, input_mean=1660, output_mean=8, seed=11)
-    w, _ = run_policy("kunserve", warm, shape, int(0.25 * (1 << 30)))
+    w, _ = run_policy("kunserve", warm, shape, int(0.25 * (1 << 30)), clock=clock)
     # the scheduler plans with the cost model refit on the warm-up's measured
     # B200 stage times (engine.py:389-397, 729-734)
     fit = w.get("cost_fit")
@@ -101,7 +117,11 @@ def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b",
     res = {}
     samples_all = []
     for pol in policies:
-        r, samples = run_policy(pol, trace, shape, int(kv_gib * (1 << 30)), cost=cost)
+        r, samples = run_policy(pol, trace, shape, int(kv_gib * (1 << 30)), cost=cost,
+                                clock=clock)
+        log = r.pop("_log")
+        if keep_logs:
+            r["_log"] = log
         res[pol] = r
         samples_all += samples
     k, r = res["kunserve"], res["recompute"]
@@ -113,7 +133,7 @@ def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b",
         if k["p99_ttft_s"] else None
     tpot_ratio = k["p50_tpot_s"] / min(res[p]["p50_tpot_s"] for p in base) \
         if k["p50_tpot_s"] else None
-    return {"value": k["p99_ttft_all_s"], "unit": "s",
+    return {"value": k["p99_ttft_all_s"], "unit": "s", "clock": clock,
             "note": "p99_ttft_all_s counts a request that never got its first token inside "
                     "the run (trace + 60 s drain) as infinitely late (null when such requests "
                     "fall in the top 1%); p99_ttft_s is the reference's served-only view",
@@ -133,6 +153,10 @@ def measure(kv_gib: float = 1.0, shape_name: str = "llama3_8b",
             "trace": {"requests": len(trace), "input_mean": trace_kw.get("input_mean", 1660),
                       "output_mean": trace_kw.get("output_mean", 64), "burst": "4x",
                       "kv_budget_gib_per_replica": kv_gib},
-            "timing": "stage times measured on the B200 (CUDA events around each stage's "
-                      "Llama-3-8B layers: cuBLAS GEMMs + paged attention kernels); links "
-                      "modeled at NVLink-5 900 GB/s (replicas share one GPU)"}
+            "timing": ("wall clock: arrivals on the host clock, every stage and transfer "
+                       "executing concurrently on the B200 (two replicas = two streams on one "
+                       "GPU), FIRST_TOKEN / TOKEN / STAGE times from CUDA events"
+                       if clock == "wall" else
+                       "simulated clock: stage times measured on the B200 one at a time (CUDA "
+                       "events around each stage's Llama-3-8B layers) and fed to the "
+                       "reference's event clock; links modeled at NVLink-5 900 GB/s")}

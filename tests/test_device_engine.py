@@ -30,14 +30,25 @@ def built():
     build.build()
 
 
+@pytest.mark.parametrize("clock", ["sim", "wall"])
 @pytest.mark.parametrize("policy", ["kunserve", "recompute", "swap", "migrate"])
-def test_device_engine_overload_cycle(built, policy):
+def test_device_engine_overload_cycle(built, policy, clock):
+    """clock="sim": serving.DeviceEngine (measured stage times on the
+    reference's event clock); clock="wall": realtime.WallClockEngine (stages
+    and transfers concurrent on the GPU, wall / CUDA-event clock)."""
     from paper_2412_18169_b200.serving import DeviceEngine, device_config
     shape = SHAPES["tiny"]
     cfg = device_config(shape, instances=2, kv_bytes=1 << 20)
     cfg.policy.kind = policy
-    trace = [TraceRecord(1000 * i, 250, 20) for i in range(8)]
-    eng = DeviceEngine(cfg, trace)
+    if clock == "sim":
+        trace = [TraceRecord(1000 * i, 250, 20) for i in range(8)]
+        eng = DeviceEngine(cfg, trace)
+    else:
+        from paper_2412_18169_b200.realtime import WallClockEngine
+        # long outputs: the overload must outlast the monitor's two-tick
+        # debounce (200 ms of wall time)
+        trace = [TraceRecord(1000 * i, 250, 400) for i in range(8)]
+        eng = WallClockEngine(cfg, trace)
     res = eng.run()
     k = kinds(res.log_lines)
     assert k.get("FINISH", 0) == len(trace)
@@ -55,9 +66,20 @@ def test_device_engine_overload_cycle(built, policy):
         assert inst.table.layers_held() == list(range(shape.num_layers))
         assert inst.kv.allocated_tokens == {} and inst.kv.reserved_bytes == 0
         info = inst.pool.info()
-        assert info.live_pages == 0 and info.layers_mapped == shape.num_layers
+        # the wall-clock engine keeps one page per layer for its padded
+        # decode rows (WallClockEngine.dummy)
+        dummy = shape.num_layers if clock == "wall" else 0
+        assert info.live_pages == dummy and info.layers_mapped == shape.num_layers
     st = collect(res.log_lines)
     assert len(st.ttfts()) == len(trace)
+    if clock == "wall":
+        # every timestamp is on the run's clock: a request's first token
+        # follows its arrival, and STAGE spans are real device intervals
+        assert all(r.first_token_us >= r.arrival_us for r in st.requests.values())
+        for line in res.log_lines:
+            t, kind, f = parse_line(line)
+            if kind == "STAGE":
+                assert 0 <= int(f["start"]) < int(f["end"])
     assert eng.stage_samples and all(s[-1] >= 1 for s in eng.stage_samples)
     for pool in eng.pools.values():
         pool.close()
