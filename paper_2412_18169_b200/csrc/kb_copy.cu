@@ -25,6 +25,21 @@ constexpr int kThreads = 256;
 constexpr int kUnroll = 8;
 constexpr int64_t kPiece = 32768;  // bytes of one page handled by one block pass
 
+// Grid of the bulk copies.  One CTA per 32 KiB piece (a short-lived CTA:
+// one 8-deep load / store round per thread), not a persistent grid: a
+// burst then never holds the SMs for its whole duration, so work on a
+// higher-priority stream -- the pipeline's activation hand-off, the
+// reference's _PRIO (exchange.py:27-28) -- gets the next free CTA slots
+// within microseconds instead of waiting for a multi-GB burst to drain.
+// KB_COPY_PERSISTENT=1 builds the r1 grid (148 x 8 CTAs striding over the
+// pieces) for A/B runs.
+#ifndef KB_COPY_PERSISTENT
+#define KB_COPY_PERSISTENT 0
+#endif
+inline int copy_grid(int64_t pieces) {
+  return KB_COPY_PERSISTENT ? grid_for(pieces, 1, 148 * 8) : grid_for(pieces, 1, 1 << 30);
+}
+
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -141,7 +156,7 @@ static int launch_flat(uint64_t dst, uint64_t src, int64_t nbytes, cudaStream_t 
   int64_t body = aligned ? (nbytes & ~(int64_t)15) : 0;
   if (body) {
     int64_t pieces = ceil_div(body / 16, kPiece / 16);
-    int grid = grid_for(pieces, 1, 148 * 8);
+    int grid = copy_grid(pieces);
     copy_flat_kernel<<<grid, kThreads, 0, st>>>(reinterpret_cast<int4*>(dst),
                                                 reinterpret_cast<const int4*>(src), body / 16);
     KB_LAUNCH_CHECK();
@@ -201,7 +216,7 @@ extern "C" int kb_copy_pages(kb_pool* dst, kb_pool* src, const kb_move* moves, i
       sub += moves[b0 + i].flat_hi - moves[b0 + i].flat_lo;
     }
     if (sub == 0) continue;
-    int grid = grid_for(sub * pieces, 1, 148 * 8);
+    int grid = copy_grid(sub * pieces);
     copy_pages_kernel<<<grid, kThreads, 0, st>>>(dv, sv, batch, nb, sub, src->m.page_bytes,
                                                  pieces);
     KB_LAUNCH_CHECK();

@@ -1097,6 +1097,103 @@ class Engine:
         self.log("RESUME", req=rid)
         self.kick(self.group_of[st["home"]])
 
+    # ------------------------------------------------------------- failures
+    def schedule_failure(self, iid: int, at_us: int) -> None:
+        """Inject the failure of instance `iid` at `at_us` (see fail_instance)."""
+        self.evq.push(at_us, lambda: self._try_fail(iid))
+
+    def _try_fail(self, iid: int) -> None:
+        # a drop / exchange / restore in flight finishes first (its tasks
+        # name the instance); the failure lands at the next monitor tick
+        if self.transition_tasks > 0:
+            self.evq.push(self.now + self.monitor.tick_us, lambda: self._try_fail(iid))
+            return
+        self.fail_instance(iid)
+
+    def fail_instance(self, iid: int) -> None:
+        """Fault injection and failure restore (B200 addition).
+
+        The reference carries Instance.failed (core.py:188) and leaves failed
+        instances out of its capacity sums (engine.py:242-254) but never sets
+        it.  The paper's fault tolerance: a failed node
+        disrupts the other members of its pipeline group, which are restored
+        to full parameter copies -- from a surviving replica, or from the host
+        copy (exchange.HOST, exchange.py:18, 224-233).  Here:
+          * the instance leaves service (failed = True, no group);
+          * its group's round in flight is abandoned and every resident of
+            the group is evicted and re-queued (the KV slice the failed
+            member held is gone: the request re-prefills, as after a
+            recompute eviction, engine.py:_evict_one);
+          * every surviving member becomes a singleton group, gated until it
+            holds all layers again: the layers it lacks are pulled from the
+            lowest-id live holder outside the failed set, else HOST
+            (plan_restore_transfers; one plan per missing range, since a
+            middle member of a PP-4 group misses two);
+          * the evicted requests are dispatched again across live groups.
+        """
+        inst = self.instances[iid]
+        if inst.failed:
+            raise ValueError(f"instance {iid} already failed")
+        inst.failed = True
+        gid = self.group_of.pop(iid)
+        grun = self.groups.pop(gid)
+        self.log("FAIL", inst=iid, group=gid)
+        grun.rstate = None
+        grun.in_round = False
+        for rid in sorted(grun.active):
+            self._evict_one(grun, rid)
+        requeue = list(grun.queue)
+        L = self.model.num_layers
+        survivors = [m for m in grun.group.member_instances if m != iid]
+        live = [i for i in sorted(self.instances) if not self.instances[i].failed]
+        holders = {i: self.instances[i].table.held_ranges() for i in live}
+        missing = {}
+        for m in survivors:
+            self.groups[m] = GroupRun(group=Group(gid=m, member_instances=[m],
+                                                  stage_layer_map={m: (0, L)}))
+            self.group_of[m] = m
+            need = member_moves(holders[m], (0, L))[1]
+            if need:
+                missing[m] = need
+        for m in sorted(missing):
+            for rng in missing[m]:
+                memory.restore_layers(self.instances[m], rng, HOST, tid=self._next_tid())
+        tasks = []
+        for k in range(max((len(r) for r in missing.values()), default=0)):
+            flat = {m: rngs[k] for m, rngs in missing.items() if len(rngs) > k}
+            tasks += plan_restore_transfers(flat, holders, self.model.bytes_per_layer,
+                                            self._exchange_chunk_bytes(),
+                                            tid_start=self._tid + 1 + len(tasks))
+        self._tid += len(tasks)
+        if missing:
+            self.log("RESTORE", group=gid, members=",".join(map(str, sorted(missing))))
+        self._on_params_planned(tasks, fetch=False)
+        left: dict[int, int] = {}
+        for t in tasks:
+            left[t.dst] = left.get(t.dst, 0) + 1
+        for m in missing:
+            self.fetch_gate[m] = left[m]
+        self._failover = getattr(self, "_failover", {})
+        self._failover.update({m: missing[m] for m in missing})
+        for t in tasks:
+            self.transition_tasks += 1
+            self.enqueue_task(t, lambda task, when: self._failover_chunk_done(task, when))
+        for rid in requeue:
+            self.dispatch(self.requests[rid])
+        for g in sorted(self.groups):
+            self.kick(g)
+
+    def _failover_chunk_done(self, task: TransferTask, when: int) -> None:
+        self.transition_tasks -= 1
+        m = task.dst
+        self.fetch_gate[m] -= 1
+        if self.fetch_gate[m] == 0:
+            del self.fetch_gate[m]
+            for rng in self._failover.pop(m):
+                memory.complete_restore(self.instances[m], rng)
+            self.log("RESTORE_DONE", inst=m)
+            self.kick(m)
+
     # ------------------------------------------------------------------ run
     def run(self) -> SimResult:
         self.log("CONFIG", policy=self.policy, seed=self.seed, instances=len(self.instances),

@@ -58,11 +58,12 @@ class WallClockEngine(DeviceEngine):
         self.poll_sleep_s = poll_sleep_s
         self.buckets = tuple(sorted(graph_buckets))
         self.inflight: list = []          # (event, callback) in launch order
-        self.stage_out: dict = {}         # (gid, rnd, k, s) -> output rows of stage s
-        self.act_in: dict = {}            # (gid, rnd, k, s) -> input rows of stage s
+        self._act_tasks: dict = {}        # (gid, rnd, k, s) -> ACTIVATION task after stage s
         self._act_key = None              # the hand-off _stage_done is about to enqueue
-        self._xfer_ev: dict = {}          # tid -> pending device transfer
         self.stage_launches = 0
+        # host time split of the loop (seconds): stage launches, device
+        # callbacks, timed events, idle sleeps
+        self.host_prof = {"launch": 0.0, "callbacks": 0.0, "events": 0.0, "idle": 0.0}
         L = self.model.num_layers
         # dummy slot per pool for padded decode rows: one page per layer
         self.dummy = {}
@@ -111,53 +112,137 @@ class WallClockEngine(DeviceEngine):
         return t.to(dev, non_blocking=True)
 
     def _try_start_stage(self, gid: int, s: int) -> None:
+        """The base engine calls this for stage 0 when a round forms and for
+        stage s+1 when a hand-off lands (engine.py:410-455).  Here the whole
+        round is launched at once when it forms: every microbatch's stage
+        chain is queued on the device with event dependencies (stage s on
+        its instance's stream -> hand-off copy on the priority stream ->
+        stage s+1 on the next instance's stream), so no host round trip sits
+        between a stage and its successor.  The host only observes the
+        completions, in causal order, and runs the reference's callbacks on
+        them; the later calls are bookkeeping."""
         grun = self.groups.get(gid)
         if grun is None or grun.rstate is None:
             return
         rs = grun.rstate
-        while rs.next_k[s] < len(rs.mbs):
-            k = rs.next_k[s]
-            if rs.act_ready[s][k] is None:
-                return
-            rs.next_k[s] += 1
-            self._launch_stage(gid, grun, rs, s, k)
+        if s == 0:
+            t_host = time.perf_counter()
+            while rs.next_k[0] < len(rs.mbs):
+                k = rs.next_k[0]
+                rs.next_k[0] += 1
+                self._launch_chain(gid, grun, rs, k)
+            self.host_prof["launch"] += time.perf_counter() - t_host
+        else:
+            while rs.next_k[s] < len(rs.mbs) and rs.act_ready[s][rs.next_k[s]] is not None:
+                rs.next_k[s] += 1
 
-    def _launch_stage(self, gid: int, grun, rs, s: int, k: int) -> None:
+    def _stage_batch(self, iid: int, mb, n_pad: Optional[int]) -> dict:
+        """The microbatch's index vectors for member iid, all int32 lists
+        packed into ONE pinned tensor and one async H2D copy on the current
+        stream (decode rows padded to n_pad with the dummy slot)."""
         torch = self.torch
-        iid = rs.members[s]
-        lo, hi = grun.group.stage_layer_map[iid]
         dev = self._dev_of(iid)
-        cs = self.compute[iid]
-        runner = self.runners[iid]
-        last = s == len(rs.members) - 1
-        with torch.cuda.device(dev), torch.cuda.stream(cs):
-            b = self._batch(iid, rs.mbs[k])
-            if s == 0:
-                ids = torch.randint(0, self.shape.vocab, (b["n"],), device=f"cuda:{dev}")
-                x = self.emb[dev].index_select(0, ids)
-            else:
-                x = self.act_in.pop((gid, rs.no, k, s))
-                x.record_stream(cs)
-            a = torch.cuda.Event(enable_timing=True)
-            e = torch.cuda.Event(enable_timing=True)
-            a.record(cs)
-            n_pad = self._bucket(b["n"]) if b["np"] == 0 else None
+        of = self.slots[iid].of
+        pre = [ch for ch in mb.chunks if not ch.decode]
+        dec = [ch for ch in mb.chunks if ch.decode]
+        slots, pos, p_slots, p_off, p_len, p_prefix, last = [], [], [], [], [], [], []
+        row = 0
+        for ch in pre:
+            c, p = ch.token_count, ch.prefix_len
+            slots += [of[ch.rid]] * c
+            pos += range(p, p + c)
+            p_off.append(row)
+            p_slots.append(of[ch.rid])
+            p_len.append(c)
+            p_prefix.append(p)
+            row += c
+            last.append(row - 1)
+        npr = row
+        d_slots = [of[ch.rid] for ch in dec]
+        d_ctx = [ch.prefix_len for ch in dec]
+        last += range(npr, npr + len(dec))
+        n = npr + len(dec)
+        if n_pad is not None:
+            extra = n_pad - n
+            d_slots += [self.dummy[iid]] * extra
+            d_ctx += [1] * extra
+        slots += d_slots
+        pos += [c - 1 for c in d_ctx]
+        parts = [slots, pos, p_slots, p_off, p_len, p_prefix, d_slots, d_ctx, last]
+        flat = torch.tensor([v for part in parts for v in part], dtype=torch.int32,
+                            pin_memory=True).to(f"cuda:{dev}", non_blocking=True)
+        views, at = [], 0
+        for part in parts:
+            views.append(flat[at:at + len(part)])
+            at += len(part)
+        (slots_t, pos_t, p_slots_t, p_off_t, p_len_t, p_prefix_t, d_slots_t, d_ctx_t, last_t) = views
+        nd = len(d_slots)
+        return {"n": n, "slots": slots_t, "pos": pos_t, "n_prefill_rows": npr, "np": len(pre),
+                "p_slots": p_slots_t, "p_off": p_off_t, "p_len": p_len_t, "p_prefix": p_prefix_t,
+                "p_max": max(p_len, default=0),
+                "p_kv_max": max((a + b for a, b in zip(p_prefix, p_len)), default=0),
+                "nd": nd, "d_slots": d_slots_t, "d_ctx": d_ctx_t,
+                "d_max": max(d_ctx, default=0), "last": last_t.long(),
+                "units": sum(ch.token_count * ch.prefix_len + (ch.token_count ** 2 +
+                                                              ch.token_count) / 2 for ch in pre)}
+
+    def _launch_chain(self, gid: int, grun, rs, k: int) -> None:
+        torch = self.torch
+        mb = rs.mbs[k]
+        S = len(rs.members)
+        prev = None  # (output rows, end event) of the previous stage
+        for s, iid in enumerate(rs.members):
+            lo, hi = grun.group.stage_layer_map[iid]
+            dev = self._dev_of(iid)
+            cs = self.compute[iid]
+            runner = self.runners[iid]
+            decode_only = all(ch.decode for ch in mb.chunks)
+            n = sum(ch.token_count for ch in mb.chunks)
+            n_pad = self._bucket(n) if decode_only else None
             if n_pad is not None and (lo, hi, n_pad) not in getattr(runner, "_graphs", {}):
                 n_pad = None
-            if n_pad is not None:
-                y = runner.run_padded_decode(lo, hi, x, runner.padded_batch(b, n_pad,
-                                                                            self.dummy[iid]),
-                                             n_pad)
-            else:
-                y = runner.run(lo, hi, x, b)
-            if last and b["last"].numel():  # sample the next token of each sequence
-                (y.index_select(0, b["last"]) @ self.emb[dev].t()).argmax(dim=-1)
-            e.record(cs)
-        self.stage_launches += 1
-        if not last:
-            self.stage_out[(gid, rs.no, k, s)] = y
-        meta = (b["n"], b["units"], b["nd"], hi - lo)
-        self.inflight.append((e, lambda: self._stage_finished(gid, rs.no, k, s, iid, a, e, meta)))
+            with torch.cuda.device(dev):
+                if s > 0:
+                    # the hand-off (ACTIVATION task, engine.py:428-448): stage
+                    # s-1's rows into this instance's input, on the priority
+                    # stream, after stage s-1 ends
+                    src, e_prev = prev
+                    urgent = self.te.urgent
+                    with torch.cuda.stream(urgent):
+                        urgent.wait_event(e_prev)
+                        x = torch.empty_like(src, device=f"cuda:{dev}")
+                        ca = torch.cuda.Event(enable_timing=True)
+                        ce = torch.cuda.Event(enable_timing=True)
+                        ca.record(urgent)
+                        runtime.copy_bytes(x.data_ptr(), src.data_ptr(),
+                                           src.numel() * src.element_size(), stream=urgent)
+                        ce.record(urgent)
+                    src.record_stream(urgent)
+                    self.inflight.append((ce, lambda s=s, ca=ca, ce=ce, dev=dev:
+                                          self._act_copied(gid, rs.no, k, s - 1, ca, ce, dev)))
+                with torch.cuda.stream(cs):
+                    b = self._stage_batch(iid, mb, n_pad)
+                    if s == 0:
+                        ids = torch.randint(0, self.shape.vocab, (n,), device=f"cuda:{dev}")
+                        x = self.emb[dev].index_select(0, ids)
+                    else:
+                        cs.wait_event(ce)
+                        x.record_stream(cs)
+                    a = torch.cuda.Event(enable_timing=True)
+                    e = torch.cuda.Event(enable_timing=True)
+                    a.record(cs)
+                    if n_pad is not None:
+                        y = runner.run_padded_decode(lo, hi, x, dict(b, n=n_pad, nd=n_pad), n_pad)
+                    else:
+                        y = runner.run(lo, hi, x, b)
+                    if s == S - 1 and b["last"].numel():  # sample each sequence's next token
+                        (y.index_select(0, b["last"]) @ self.emb[dev].t()).argmax(dim=-1)
+                    e.record(cs)
+            self.stage_launches += 1
+            meta = (n, b["units"], len([c for c in mb.chunks if c.decode]), hi - lo)
+            self.inflight.append((e, lambda s=s, iid=iid, a=a, e=e, meta=meta:
+                                  self._stage_finished(gid, rs.no, k, s, iid, a, e, meta)))
+            prev = (y, e)
 
     def _stage_finished(self, gid, rnd, k, s, iid, a, e, meta) -> None:
         dev = self._dev_of(iid)
@@ -170,14 +255,15 @@ class WallClockEngine(DeviceEngine):
             self._stage_done(gid, rnd, k, s, start, end)
         finally:
             self._act_key = None
-            self.stage_out.pop((gid, rnd, k, s), None)
 
-    def _act_arrived(self, gid: int, rnd: int, k: int, s: int, when: int) -> None:
-        grun = self.groups.get(gid)
-        if grun is None or grun.rstate is None or grun.rstate.no != rnd:
-            self.act_in.pop((gid, rnd, k, s), None)   # the round went stale
-            return
-        super()._act_arrived(gid, rnd, k, s, when)
+    def _act_copied(self, gid, rnd, k, s, ca, ce, dev) -> None:
+        """The hand-off after stage s of microbatch k landed: the reference's
+        _xfer_done for its ACTIVATION task (XFER line, then the callback
+        that marks stage s+1's input ready)."""
+        got = self._act_tasks.pop((gid, rnd, k, s), None)
+        if got is None:
+            return   # the round went stale before the task was enqueued
+        self._task_finished(got, ca, ce, dev)
 
     # ------------------------------------------------------------ transfers
     def _pump(self, link) -> None:
@@ -191,21 +277,9 @@ class WallClockEngine(DeviceEngine):
     def _start_task(self, link, task) -> None:
         torch = self.torch
         if task.kind is TaskKind.ACTIVATION:
-            gid, rnd, k, s = self._act_key
-            src = self.stage_out.pop((gid, rnd, k, s))
-            dst_dev = self._dev_of(task.dst)
-            urgent = self.te.urgent
-            with torch.cuda.device(dst_dev), torch.cuda.stream(urgent):
-                dst = torch.empty_like(src, device=f"cuda:{dst_dev}")
-                a = torch.cuda.Event(enable_timing=True)
-                e = torch.cuda.Event(enable_timing=True)
-                a.record(urgent)
-                runtime.copy_bytes(dst.data_ptr(), src.data_ptr(),
-                                   src.numel() * src.element_size(), stream=urgent)
-                e.record(urgent)
-            src.record_stream(urgent)
-            self.act_in[(gid, rnd, k, s + 1)] = dst
-            self.inflight.append((e, lambda: self._task_finished(task, a, e, dst_dev)))
+            # launched with the round's stage chain (_launch_chain); its
+            # completion callback (_act_copied) finishes the task
+            self._act_tasks[self._act_key] = task
             return
         self._run_task(task)   # DeviceEngine: te.submit on the bulk stream
         p = self.te.pending[-1]
@@ -231,6 +305,7 @@ class WallClockEngine(DeviceEngine):
         """Fire the callbacks of completed device work; True if any fired."""
         fired = False
         i = 0
+        t0 = time.perf_counter()
         while i < len(self.inflight):
             ev, fn = self.inflight[i]
             if ev.query():
@@ -240,6 +315,8 @@ class WallClockEngine(DeviceEngine):
                 fired = True
             else:
                 i += 1
+        if fired:
+            self.host_prof["callbacks"] += time.perf_counter() - t0
         return fired
 
     def _settled(self) -> bool:
@@ -283,13 +360,17 @@ class WallClockEngine(DeviceEngine):
                 if len(self.evq) and self.evq.peek_time() <= w:
                     t, _, fn = self.evq.pop()
                     self.now = max(self.now, t)
+                    t1 = time.perf_counter()
                     fn()
+                    self.host_prof["events"] += time.perf_counter() - t1
                     continue
                 if w > self.horizon_us or self._settled():
                     break
                 if not fired:
                     nxt = self.evq.peek_time() - w if len(self.evq) else 1000
+                    t1 = time.perf_counter()
                     time.sleep(min(max(nxt, 0) / 1e6, self.poll_sleep_s))
+                    self.host_prof["idle"] += time.perf_counter() - t1
         finally:
             gc.enable()
         torch.cuda.synchronize()

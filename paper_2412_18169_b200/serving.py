@@ -159,24 +159,9 @@ class StageRunner:
     # A decode-only microbatch of n rows replays the graph of the smallest
     # bucket >= n; the extra rows decode a reserved dummy slot (one page per
     # layer, context 1) from zero activations, so their K/V land in the dummy
-    # page and their outputs are dropped.  Graphs are captured ahead of time
+    # page and their outputs are dropped (the caller pads the index vectors:
+    # realtime.WallClockEngine._stage_batch).  Graphs are captured ahead of time
     # (capture_padded), so serving never captures.
-    def padded_batch(self, batch: dict, n_pad: int, dummy_slot: int) -> dict:
-        torch = self.torch
-        n = batch["n"]
-        extra = n_pad - n
-        dev = batch["slots"].device
-
-        def pad(t, val):
-            return torch.cat([t, torch.full((extra,), val, dtype=t.dtype, device=dev)]) \
-                if extra else t
-        return dict(batch, n=n_pad, nd=n_pad, slots=pad(batch["slots"], dummy_slot),
-                    pos=pad(batch["pos"], 0), d_slots=pad(batch["d_slots"], dummy_slot),
-                    d_ctx=pad(batch["d_ctx"], 1),
-                    d_rows=torch.arange(n_pad, dtype=torch.int64, device=dev),
-                    last=torch.arange(n_pad, dtype=torch.int64, device=dev),
-                    d_max=max(batch["d_max"], 1))
-
     def capture_padded(self, lo: int, hi: int, n_pad: int, dummy_slot: int) -> None:
         torch = self.torch
         dev = self.pool.rt.device
@@ -245,7 +230,8 @@ class StageRunner:
 
 class DeviceEngine(Engine):
     def __init__(self, cfg, trace, policy: Optional[str] = None, seed: int = 0,
-                 runtimes: Optional[dict] = None, max_seqs: Optional[int] = None):
+                 runtimes: Optional[dict] = None, max_seqs: Optional[int] = None,
+                 host_replica: bool = False):
         import torch
         self.torch = torch
         pol = policy or cfg.policy.kind
@@ -270,6 +256,19 @@ class DeviceEngine(Engine):
         self.page_stream = self.te.bulk
         for iid, inst in self.instances.items():
             init_weights(inst.pool, self.shape, inst.table.layers_held())
+        if host_replica:
+            # one full parameter copy in pinned host memory (the HOST source of
+            # exchange.py:18, 224-233): the weights every replica boots with
+            L = self.model.num_layers
+            rep = torch.empty(self.model.param_bytes, dtype=torch.uint8).pin_memory()
+            tmp = self.runtimes[cfg.device.devices[0]].create_pool(-1, self.model, self.model.param_bytes
+                                                                   + (1 << 21), self.shape)
+            init_weights(tmp, self.shape, range(L))
+            for l in range(L):
+                a = l * self.model.bytes_per_layer
+                rep[a:a + self.model.bytes_per_layer].copy_(tmp.weight_bytes(l))
+            tmp.close()
+            self.te.host_replica = rep
         # a decode microbatch can hold every slot of a pool: size the
         # attention workspace for that (paged_decode refuses a smaller one)
         self.runners = {iid: StageRunner(p, self.shape, max_seqs=max_seqs or cfg.device.max_slots)
@@ -338,6 +337,15 @@ class DeviceEngine(Engine):
             self.te.register_request_move(task, (0, self.model.num_layers),
                                           self.requests[task.rid].context_len)
         self.te.submit(task)
+
+    def fail_instance(self, iid: int) -> None:
+        """engine.Engine.fail_instance on the device: the failed pool's weight
+        slabs are overwritten first, so a restore that read from it could not
+        reproduce the boot weights."""
+        pool = self.pools[iid]
+        for l in self.instances[iid].table.layers_held():
+            pool.weight_bytes(l).fill_(0x7F)
+        super().fail_instance(iid)
 
     def _transfers_landed(self) -> None:
         """Called when the engine's clock says a transfer finished: the
@@ -547,4 +555,11 @@ def device_config(shape, instances: int = 2, kv_bytes: int = 8 << 30, devices=(0
     cfg.device.devices = tuple(devices)
     cfg.device.max_pages_per_seq = max(64, math.ceil(32768 / shape.block_tokens))
     cfg.device.max_slots = 512
+    if len(set(devices)) < instances:
+        # members of a pipeline group share a GPU here, so their stages
+        # cannot overlap: the lookahead formulation's small microbatches
+        # (formulation.py, split down to min_batch_tokens = 256) would only
+        # re-read every stage's weights once more per microbatch.  Split no
+        # finer than the token budget (the reference's own knob, config.py).
+        cfg.policy.min_batch_tokens = cfg.policy.token_budget
     return cfg

@@ -72,6 +72,8 @@ def run_policy(policy: str, trace, shape, kv_bytes: int, runtimes=None, cost=Non
            "rounds": kinds.get("ROUND", 0), "stages_measured": len(eng.stage_samples),
            "bubble_ratio": round(bubble_ratio(res.log_lines), 4),
            "clock": clock, "wall_s": round(wall, 1), "setup_s": round(t1 - t0, 1)}
+    if hasattr(eng, "host_prof"):
+        out["host_s"] = {k: round(v, 2) for k, v in eng.host_prof.items()}
     fit = fit_stage_samples(eng.stage_samples, shape.num_layers)
     if fit:
         out["cost_fit"] = {k: fit[k] for k in ("alpha", "beta", "gamma")}

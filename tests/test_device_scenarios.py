@@ -1,0 +1,223 @@
+"""Device paths of the drop / restore cycle that the end-to-end runs rarely
+hit (VERDICT r1 "Next 4 and 9"):
+
+* an UNEQUAL merge -- a singleton joins a PP-2 group and a member must fetch
+  a layer it does not hold, whose last other copy sits on a member that
+  drops it (engine.py:762-795, 838-859): the fetch lands before the deferred
+  drop, and the fetched slab is byte-identical;
+* KV bytes of residents DURING serving: every exchange / consolidation flow's
+  pages hash the same on the destination as on the source when it lands;
+* activation priority on the device: a hand-off submitted behind a >= 1 GB
+  KV burst completes long before the burst does (exchange.py:27-28, 81-95);
+* failure restore: a PP-2 member fails, the survivor pulls the missing
+  layers from HOST (or the lowest live holder) and ends byte-identical.
+"""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2412_18169_b200.core import SHAPES, ModelShape  # noqa: E402
+from paper_2412_18169_b200.metrics import collect, parse_line  # noqa: E402
+from paper_2412_18169_b200.traceio import TraceRecord  # noqa: E402
+
+TINY8 = ModelShape("tiny8", num_layers=8, hidden=256, n_q_heads=2, n_kv_heads=1, head_dim=128,
+                   ffn=768, vocab=1024, block_tokens=64)
+MIB = 1 << 20
+
+
+@pytest.fixture(scope="module")
+def rtm():
+    from paper_2412_18169_b200 import build
+    build.build()
+    from paper_2412_18169_b200 import runtime
+    return runtime
+
+
+def slab_hashes(rtm, pool, layers):
+    return {l: rtm.hash_tensor(pool.weight_bytes(l)).item() for l in layers}
+
+
+def drain(eng):
+    while len(eng.evq):
+        t, _, fn = eng.evq.pop()
+        eng.now = max(eng.now, t)
+        fn()
+
+
+def test_unequal_merge_fetch_lands_before_the_deferred_drop(rtm):
+    """{1:(0,4), 2:(4,8)} + {0:(0,8)} -> members (0, 1, 2) with stages
+    0:(0,2), 1:(2,5), 2:(5,8): instance 1 lacks layer 4, whose lowest-id live
+    holder is instance 0 -- which drops it in the same merge, so that drop
+    waits for the fetch."""
+    from paper_2412_18169_b200.planner import plan_drop
+    from paper_2412_18169_b200.serving import DeviceEngine, device_config
+    cfg = device_config(TINY8, instances=3, kv_bytes=2 * MIB)
+    eng = DeviceEngine(cfg, [])
+    boot = slab_hashes(rtm, eng.pools[0], range(8))
+    p1 = plan_drop([eng.groups[1].group, eng.groups[2].group], 1, eng.model)
+    eng._merge_groups(p1.merges[0])
+    drain(eng)
+    g12 = eng.groups[p1.merges[0].gid]
+    assert g12.group.stage_layer_map == {1: (0, 4), 2: (4, 8)}
+    # instance 1's dropped slab of layer 4 now holds KV-pool bytes: poison it,
+    # so only a real fetch can bring layer 4 back
+    pool1 = eng.pools[1]
+    sp = eng.model.bytes_per_layer // pool1.page_bytes
+    head = pool1.info().max_pages - 8 * sp
+    pool1.kv_bytes()[(head + 4 * sp) * pool1.page_bytes:(head + 5 * sp) * pool1.page_bytes].fill_(0x7F)
+    p2 = plan_drop([eng.groups[0].group, g12.group], 1, eng.model)
+    st = p2.merges[0]
+    assert list(st.members) == [0, 1, 2]
+    assert st.stage_layer_map == {0: (0, 2), 1: (2, 5), 2: (5, 8)}
+    n0 = len(eng.log_lines)
+    eng._merge_groups(st)
+    assert 4 in eng.instances[0].table.layers_held()      # deferred: last live copy
+    assert eng.deferred_drops.get(0) == [(4, 5, st.gid)]
+    drain(eng)
+    lines = [parse_line(l) for l in eng.log_lines[n0:]]
+    fetch_done = max(i for i, (t, k, f) in enumerate(lines)
+                     if k == "XFER" and f["task"] == "param_shard" and f["dst"] == "1")
+    late_drop = next(i for i, (t, k, f) in enumerate(lines) if k == "DROP" and f["inst"] == "0"
+                     and i > 0 and lines[i - 1][1] == "XFER")
+    assert fetch_done < late_drop
+    assert 4 not in eng.instances[0].table.layers_held()
+    assert eng.instances[1].table.held_ranges() == [(2, 5)]
+    torch.cuda.synchronize()
+    assert rtm.hash_tensor(pool1.weight_bytes(4)).item() == boot[4]
+    for pool in eng.pools.values():
+        pool.close()
+
+
+def test_resident_kv_identical_across_every_exchange_and_consolidation(rtm):
+    """Mid-serving byte check: at planning time each KV flow's source pages
+    are hashed (position-sensitive, kb_hash_segments); when the flow's last
+    chunk has landed -- before the source is released -- the destination
+    pages must hash the same."""
+    from paper_2412_18169_b200.serving import DeviceEngine, device_config
+
+    class Checked(DeviceEngine):
+        def __init__(self, *a, **kw):
+            self.snap, self.checked = {}, 0
+            super().__init__(*a, **kw)
+
+        def _page_hashes(self, iid, rid, layers, npages):
+            pool = self.pools[iid]
+            slot = self.slots[iid].of[rid]
+            pages = [p for l in range(*layers) for p in pool.block_table(slot, l)[:npages]]
+            idx = torch.tensor(pages, dtype=torch.int64, device="cuda")
+            return rtm.hash_segments(pool.info().kv_base, pool.page_bytes, len(pages),
+                                     index=idx).cpu().tolist()
+
+        def _snap(self):
+            torch.cuda.synchronize()
+            for key, fl in self.te.flows.items():
+                if key not in self.snap and fl.src >= 0 and fl.dst >= 0:
+                    self.snap[key] = self._page_hashes(fl.src, fl.rid, fl.layers, fl.npages)
+
+        def _verify(self):
+            self.te.drain()
+            for key, fl in self.te.flows.items():
+                if key in self.snap and fl.done_chunks == fl.n_chunks:
+                    got = self._page_hashes(fl.dst, fl.rid, fl.layers, fl.npages)
+                    assert got == self.snap.pop(key), key
+                    self.checked += 1
+
+        def _on_exchange_planned(self, *a):
+            super()._on_exchange_planned(*a)
+            self._snap()
+
+        def _on_consolidation_planned(self, *a):
+            super()._on_consolidation_planned(*a)
+            self._snap()
+
+        def _exchange_chunk_done(self, task, when):
+            self._verify()
+            super()._exchange_chunk_done(task, when)
+
+        def _on_consolidated(self, rid, peers):
+            self._verify()
+            super()._on_consolidated(rid, peers)
+
+    shape = SHAPES["tiny"]
+    cfg = device_config(shape, instances=2, kv_bytes=1 << 20)
+    trace = [TraceRecord(1000 * i, 250, 20) for i in range(8)]
+    eng = Checked(cfg, trace)
+    res = eng.run()
+    k = {}
+    for l in res.log_lines:
+        k[parse_line(l)[1]] = k.get(parse_line(l)[1], 0) + 1
+    assert k.get("EXCHANGE", 0) >= 1 and k.get("DISSOLVE", 0) >= 1
+    assert eng.checked >= 2 and not eng.snap
+    assert collect(res.log_lines).finished() == len(trace)
+    for pool in eng.pools.values():
+        pool.close()
+
+
+def test_activation_overtakes_a_1gb_kv_burst(rtm):
+    """The transfer engine's two streams (transfer.py): a KV burst of 1 GiB
+    of pages on the low-priority bulk stream, then an activation hand-off on
+    the high-priority stream.  The copy kernels run one short CTA per 32 KiB
+    piece (kb_copy.cu copy_grid), so the hand-off gets CTA slots as soon as
+    some retire: it lands long before the burst does."""
+    from paper_2412_18169_b200.transfer import SlotTable, TransferEngine
+    shape = ModelShape("llama_pages", num_layers=2, hidden=256, n_q_heads=32, n_kv_heads=8,
+                       head_dim=128, ffn=256, vocab=1024, block_tokens=64)
+    model = shape.spec()
+    npg = 4096                                    # 4096 x 256 KiB = 1 GiB
+    rt = rtm.Runtime(0, max_slots=4, max_pages_per_seq=npg, slack_pages=16)
+    a = rt.create_pool(0, model, model.param_bytes + (1 << 30) + 64 * MIB, shape)
+    b = rt.create_pool(1, model, model.param_bytes + (1 << 30) + 64 * MIB, shape)
+    assert a.grow([(0, 0, 1, npg)]) and b.grow([(0, 0, 1, npg)])
+    te = TransferEngine({0: a, 1: b}, {0: SlotTable(4), 1: SlotTable(4)})
+    act_src = torch.randn((64, 4096), device="cuda").to(torch.bfloat16)
+    act_dst = torch.empty_like(act_src)
+    nbytes = act_src.numel() * 2
+    ev = {k: torch.cuda.Event(enable_timing=True) for k in ("b0", "b1", "a1")}
+    for rep in range(3):  # the last repetition is measured
+        torch.cuda.synchronize()
+        ev["b0"].record(te.bulk)
+        rtm.copy_pages(b, a, [(0, 0, 0, 1, npg, 0, npg)], stream=te.bulk)
+        ev["b1"].record(te.bulk)
+        te.urgent.wait_event(ev["b0"])
+        rtm.copy_bytes(act_dst.data_ptr(), act_src.data_ptr(), nbytes, stream=te.urgent)
+        ev["a1"].record(te.urgent)
+        torch.cuda.synchronize()
+    burst = ev["b0"].elapsed_time(ev["b1"])
+    act = ev["b0"].elapsed_time(ev["a1"])
+    assert torch.equal(act_dst, act_src)
+    assert burst > 0.2, burst                     # ms: 2 GiB of HBM traffic
+    assert act < 0.25 * burst, (act, burst)
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("instances,source", [(2, "host"), (4, "peer")])
+def test_failure_restore_is_byte_exact(rtm, instances, source):
+    """engine.Engine.fail_instance on device pools: a member of a PP-2 group
+    fails (its slabs are poisoned first); the survivor pulls the layers it
+    lacks from HOST (2 instances: no live replica) or from the lowest live
+    holder (4 instances: instance 3), ends holding every layer with the boot
+    weights byte for byte, and serves every request."""
+    from paper_2412_18169_b200.serving import DeviceEngine, device_config
+    cfg = device_config(TINY8, instances=instances, kv_bytes=2 * MIB)
+    cfg.cluster.initial_group_size = 2
+    trace = [TraceRecord(1000 * i, 250, 30) for i in range(6)]
+    eng = DeviceEngine(cfg, trace, host_replica=True)
+    boot = {l: rtm.hash_tensor(eng.te.host_replica[l * eng.model.bytes_per_layer:
+                                                   (l + 1) * eng.model.bytes_per_layer].cuda()
+                               ).item() for l in range(8)}
+    eng.schedule_failure(1, 2_000)
+    res = eng.run()
+    lines = [parse_line(l) for l in res.log_lines]
+    fail_t = next(t for t, k, f in lines if k == "FAIL")
+    srcs = {f["src"] for t, k, f in lines if k == "XFER" and f["task"] == "param_shard"
+            and f["dst"] == "0" and t >= fail_t}
+    assert srcs == ({"-1"} if source == "host" else {"3"})
+    torch.cuda.synchronize()
+    assert eng.instances[0].table.layers_held() == list(range(8))
+    assert slab_hashes(rtm, eng.pools[0], range(8)) == boot
+    assert collect(res.log_lines).finished() == len(trace)
+    for pool in eng.pools.values():
+        pool.close()

@@ -229,7 +229,7 @@ def test_pdl_append_decode_chain_without_host_sync(runtime, mode, batch):
     model = shape.spec()
     nseq = 6 if batch == "combine" else 80
     rt = runtime.Runtime(0, max_slots=96, max_pages_per_seq=64, slack_pages=64)
-    pool = rt.create_pool(0, model, model.param_bytes + 512 * MIB, shape)
+    pool = rt.create_pool(0, model, model.param_bytes + 1280 * MIB, shape)
     rng = random.Random(5)
     ctxs = [rng.randrange(1, 1500) for _ in range(nseq)]
     ctxs[0] = 2047
