@@ -40,6 +40,7 @@ def test_device_engine_overload_cycle(built, policy, clock):
     shape = SHAPES["tiny"]
     cfg = device_config(shape, instances=2, kv_bytes=1 << 20)
     cfg.policy.kind = policy
+    cfg.policy.min_batch_tokens = 256   # the reference default the trace was sized for
     if clock == "sim":
         trace = [TraceRecord(1000 * i, 250, 20) for i in range(8)]
         eng = DeviceEngine(cfg, trace)
