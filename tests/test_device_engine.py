@@ -42,7 +42,9 @@ def test_device_engine_overload_cycle(built, policy, clock):
     cfg.policy.kind = policy
     cfg.policy.min_batch_tokens = 256   # the reference default the trace was sized for
     if clock == "sim":
-        trace = [TraceRecord(1000 * i, 250, 20) for i in range(8)]
+        # outputs long enough that the overload outlasts the monitor's
+        # two-tick debounce whatever the measured stage times are
+        trace = [TraceRecord(1000 * i, 250, 200) for i in range(8)]
         eng = DeviceEngine(cfg, trace)
     else:
         from paper_2412_18169_b200.realtime import WallClockEngine

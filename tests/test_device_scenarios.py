@@ -147,8 +147,8 @@ def test_resident_kv_identical_across_every_exchange_and_consolidation(rtm):
 
     shape = SHAPES["tiny"]
     cfg = device_config(shape, instances=2, kv_bytes=1 << 20)
-    cfg.policy.min_batch_tokens = 256   # the reference default the trace was sized for
-    trace = [TraceRecord(1000 * i, 250, 20) for i in range(8)]
+    # long outputs: the overload outlasts the monitor's two-tick debounce
+    trace = [TraceRecord(1000 * i, 250, 200) for i in range(8)]
     eng = Checked(cfg, trace)
     res = eng.run()
     k = {}

@@ -24,7 +24,8 @@ rng = np.random.default_rng(5)
 MS = int(os.environ.get("KB_PROBE_MAX_SPLITS", "16"))
 APPEND = os.environ.get("KB_PROBE_APPEND", "0") == "1"
 out = {}
-for nseq in (4, 16, 32, 64, 147):
+SIZES = [int(os.environ["KB_PROBE_NSEQ"])] if "KB_PROBE_NSEQ" in os.environ else [4, 16, 32, 64, 147]
+for nseq in SIZES:
     ctx = np.clip(rng.lognormal(np.log(1500), 0.6, nseq), 16, 8000).astype(int)
     slots = list(range(nseq))
     for s, c in zip(slots, ctx):
@@ -61,5 +62,17 @@ for nseq in (4, 16, 32, 64, 147):
         g.replay()
     b.record()
     b.synchronize()
-    out[nseq] = round(a.elapsed_time(b) / 20 / 16 * 1000, 2)  # us per layer
-print(json.dumps({"us_per_layer": out}))
+    us = a.elapsed_time(b) / 20 / 16 * 1000  # per layer
+    # algorithmic bytes per layer: every context token's K and V of every kv
+    # head (2 x 8 x 128 x 2 B) plus q and out rows
+    algo = int(ctx.sum()) * 2 * 8 * 128 * 2 + 2 * nseq * 32 * 128 * 2
+    out[nseq] = {"us_per_layer": round(us, 2), "hbm_gbs": round(algo / us / 1e3, 1)}
+peak = None
+try:
+    peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
+except Exception:
+    pass
+if peak:
+    for v in out.values():
+        v["frac"] = round(v["hbm_gbs"] / peak, 4)
+print(json.dumps({"decode": out, "hbm_peak_gbs": peak}))
