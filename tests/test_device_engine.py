@@ -48,9 +48,10 @@ def test_device_engine_overload_cycle(built, policy, clock):
         eng = DeviceEngine(cfg, trace)
     else:
         from paper_2412_18169_b200.realtime import WallClockEngine
-        # long outputs: the overload must outlast the monitor's two-tick
-        # debounce (200 ms of wall time)
-        trace = [TraceRecord(1000 * i, 250, 400) for i in range(8)]
+        # a steady stream of long requests: the overload must outlast the
+        # monitor's two-tick debounce (200 ms of wall time) however fast the
+        # tiny model decodes
+        trace = [TraceRecord(5000 * i, 250, 600) for i in range(16)]
         eng = WallClockEngine(cfg, trace)
     res = eng.run()
     k = kinds(res.log_lines)
