@@ -268,11 +268,16 @@ int kb_pool_kv_status(kb_pool* pool, uint32_t* flags, int32_t clear);
  * own, already appended).  out [nseq][n_q_heads][head_dim] bf16.
  * workspace: workspace_bytes >= kb_decode_workspace_bytes(nseq, ...) bytes of
  * device scratch (KB_EINVAL otherwise: its layout grows with nseq).  The work
- * plan (KV splits, item order) depends only on ctx_lens: with
- * flags & KB_DECODE_REUSE_PLAN the plan already in `workspace` (from an
- * earlier call with the same ctx_lens, e.g. the previous layer of the same
- * decode step) is reused and no plan kernel runs. */
+ * plan (KV splits, item order) depends only on ctx_lens and
+ * slots: with flags & KB_DECODE_REUSE_PLAN the plan already in `workspace`
+ * (from an earlier call with the same ctx_lens and slots, e.g. the previous
+ * layer of the same decode step) is reused and no plan kernel runs. */
 #define KB_DECODE_REUSE_PLAN 1
+/* The KV splits of a (sequence, kv head) merge inside the attention kernel
+ * for large batches (>= 4 pairs per SM) and in a combine launch otherwise;
+ * flags & KB_DECODE_COMBINE / KB_DECODE_FUSE force either (A/B, tests). */
+#define KB_DECODE_COMBINE 2
+#define KB_DECODE_FUSE 4
 int64_t kb_decode_workspace_bytes(int32_t nseq, int32_t n_q_heads, int32_t max_splits);
 int kb_paged_decode(kb_pool* pool, int32_t layer, int32_t n_q_heads, uint64_t q,
                     uint64_t slots, uint64_t ctx_lens, int32_t nseq, int32_t max_ctx,

@@ -57,7 +57,7 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
 // per persistent CTA; items are bucket-sorted longest first.  Sequences with
 // no context get neutral partials here and no item.
 __global__ void __launch_bounds__(kPlanThreads)
-decode_plan_kernel(const int32_t* __restrict__ ctx, int nseq, int Hkv, int Hq, int max_splits,
+decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ slots, int nseq, int Hkv, int Hq, int max_splits,
                    int grid_ctas, int min_tiles, int32_t* __restrict__ nsplit_of,
                    DecodeItem* __restrict__ items, int32_t* __restrict__ n_items,
                    float* __restrict__ part_ml, int32_t* __restrict__ item_counter,
@@ -139,7 +139,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, int nseq, int Hkv, int Hq, i
       const int b = kLenBuckets - 1 - min(len, kLenBuckets - 1);
       for (int h = 0; h < Hkv; ++h) {
         const int pos = atomicAdd(&cursor[b], 1);
-        items[pos] = DecodeItem{i, h, k, beg, len, {0, 0, 0}};
+        items[pos] = DecodeItem{i, h, k, beg, len, slots[i], ctx[i], 0};
       }
     }
   }
@@ -202,7 +202,7 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   if (rc) return rc;
   if (!(flags & KB_DECODE_REUSE_PLAN)) {
     decode_plan_kernel<<<1, kPlanThreads, 0, st>>>(reinterpret_cast<const int32_t*>(ctx_lens),
-                                                   nseq, Hkv, n_q_heads, max_splits, grid, kMinTiles,
+                                                   reinterpret_cast<const int32_t*>(slots), nseq, Hkv, n_q_heads, max_splits, grid, kMinTiles,
                                                    nsplit, items, n_items, part_ml,
                                                    item_counter, split_done);
     KB_LAUNCH_CHECK();
@@ -210,8 +210,10 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   // merge inside the attention kernel when the batch is large (>= 4
   // (sequence, kv head) pairs per CTA; B200 A/B: 191 vs 200 us per Llama
   // layer at 147 sequences, equal at 64, slower below: 26 vs 21 us at 4)
-  const int fuse = (int64_t)nseq * Hkv >= 4LL * grid;
-  rc = launch_decode_tc(p, layer, n_q_heads, q, slots, ctx_lens, grid, scale, part_o, part_ml,
+  int fuse = (int64_t)nseq * Hkv >= 4LL * grid;
+  if (flags & KB_DECODE_COMBINE) fuse = 0;
+  if (flags & KB_DECODE_FUSE) fuse = 1;
+  rc = launch_decode_tc(p, layer, n_q_heads, q, grid, scale, part_o, part_ml,
                         items, n_items, item_counter, nsplit, split_done, nseq, fuse, out,
                         max_splits, st);
   if (rc) return rc;
@@ -234,3 +236,10 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   }
   return pool_leave(p, st);
 }
+
+#ifdef KB_DEC_TRACE
+extern "C" int kb_debug_dec_trace(unsigned long long* out, int32_t n) {
+  if (n > 1024 * kb::kTraceSlots) n = 1024 * kb::kTraceSlots;
+  return cudaMemcpyFromSymbol(out, kb::g_dec_trace, (size_t)n * 8) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -41,8 +41,11 @@ constexpr int kDecSmem = kDecStages * kStageBytes + 2 * kQBytes + 2 * kPBytes + 
 constexpr uint32_t kDecTmemCols = 64;    // S0 S1 O0 O1, 16 columns each
 constexpr int kRing = 16;                // dynamically fetched work items in flight per CTA
 
+// one KV split of a (sequence, kv head) pair: tiles [t_beg, t_beg + nt);
+// the slot and context length ride along (one dependent load less before
+// the item's first TMA)
 struct DecodeItem {
-  int32_t seq, h, split, t_beg, nt, _pad[3];
+  int32_t seq, h, split, t_beg, nt, slot, ctx, _pad;
 };
 
 struct DecodeMisc {
@@ -61,11 +64,27 @@ struct DecodeMisc {
   float lred[4][8];
 };
 
+// KB_DEC_TRACE (variant builds only, tools/decode_trace_probe.py): per-CTA
+// %globaltimer stamps of the kernel's phases, read back by kb_debug_dec_trace
+#ifdef KB_DEC_TRACE
+constexpr int kTraceSlots = 16;
+__device__ unsigned long long g_dec_trace[1024 * kTraceSlots];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define DEC_TRACE(slot) (g_dec_trace[blockIdx.x * kTraceSlots + (slot)] = gtimer())
+#define DEC_TRACE_VAL(slot, v) (g_dec_trace[blockIdx.x * kTraceSlots + (slot)] = (v))
+#else
+#define DEC_TRACE(slot) ((void)0)
+#define DEC_TRACE_VAL(slot, v) ((void)0)
+#endif
+
 template <int kB>
 __global__ void __launch_bounds__(kDecThreads, 1)
 decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* __restrict__ q,
-                 const int32_t* __restrict__ bt, const int32_t* __restrict__ slots,
-                 const int32_t* __restrict__ ctx_lens, const DecodeItem* __restrict__ items,
+                 const int32_t* __restrict__ bt, const DecodeItem* __restrict__ items,
                  const int32_t* __restrict__ n_items_ptr, int32_t* __restrict__ item_counter,
                  const int32_t* __restrict__ nsplit_of, int32_t* __restrict__ split_done,
                  int nseq, int fuse_merge, __nv_bfloat16* __restrict__ out,
@@ -74,12 +93,13 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
                  int max_splits, float scale_log2) {
   using namespace sm100;
   constexpr int kPPT = kTileTok / kB;  // pages per tile
-  // Work items are sorted longest first and handed out dynamically: the
-  // producer warp of each persistent CTA takes the next index from a
+  // Work items are sorted longest first and handed out dynamically: CTA b
+  // starts with item b, then its producer warp takes the next index from a
   // per-layer global counter (a greedy longest-processing-time schedule, so
   // the CTAs finish within one short item of each other) and publishes it
   // to the MMA and softmax warps through a small shared-memory ring.
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) DEC_TRACE(0);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -119,6 +139,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
   // it wrote (plan, q, appended K/V, the previous layer's workspace use)
   pdl_wait();
   pdl_launch_dependents();
+  if (tid == 0) DEC_TRACE(1);
   const int n_items = *n_items_ptr;
   // item r of this CTA (every role reads the ring in the same order)
   auto get_item = [&](int r, DecodeItem& it) -> bool {
@@ -142,24 +163,32 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         const int r = published++;
         const int slot = r % kRing;
         if (r >= kRing) mbar_wait(&misc->ring_empty[slot], ((r / kRing) - 1) & 1);
-        int idx = atomicAdd(item_counter + layer, 1);
-        if (idx >= n_items) {
-          // the last CTA to run dry re-arms the counter (a reused plan)
-          if (idx == n_items + (int)gridDim.x - 1) item_counter[layer] = 0;
-          idx = -1;
-          exhausted = true;
+        // the first item is static (no atomic round trip before the first
+        // load); every CTA then makes exactly one failing fetch, and the
+        // last of those re-arms the counter (a reused plan)
+        const int grid = (int)gridDim.x;
+        int idx = r == 0 ? (int)blockIdx.x : -1;
+        if (idx < 0 || idx >= n_items) {
+          const int raw = atomicAdd(item_counter + layer, 1);
+          if (idx < 0) idx = grid + raw;
+          if (idx >= n_items) {
+            if (raw == max(n_items - grid, 0) + grid - 1) item_counter[layer] = 0;
+            idx = -1;
+            exhausted = true;
+          }
         }
         misc->ring_item[slot] = idx;
         mbar_arrive(&misc->ring_full[slot]);
       };
-      publish();
-      publish();
+      publish();  // item 0 (static); item 1 once item 0's first loads are out
+      bool second = false;
       int j = 0;  // global tile counter of this CTA
       for (int r = 0;; ++r) {
         DecodeItem it;
         if (!get_item(r, it)) break;
-        const int ctx = ctx_lens[it.seq];
-        const int32_t* bt_row = bt + ((int64_t)slots[it.seq] * L + layer) * maxp;
+        if (r == 0) DEC_TRACE(2);
+        const int ctx = it.ctx;
+        const int32_t* bt_row = bt + ((int64_t)it.slot * L + layer) * maxp;
         for (int t = 0; t < it.nt; ++t, ++j) {
           const int stage = j % kDecStages;
           if (j >= kDecStages) mbar_wait(&misc->empty[stage], ((j / kDecStages) - 1) & 1);
@@ -186,6 +215,11 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
             tma_load_2d(sV + off, &tmap, 0, rv, &misc->full[stage]);
             tma_load_2d(sV + kHalfBytes + off, &tmap, 64, rv, &misc->full[stage]);
           }
+          if (j == 0) DEC_TRACE(3);
+          if (!second) {
+            second = true;
+            publish();
+          }
         }
         publish();
       }
@@ -211,6 +245,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       const int stage = qj % kDecStages;
       mbar_wait(&misc->full[stage], (qj / kDecStages) & 1);
       tc_fence_after();
+      if (lane == 0 && qj == 0) DEC_TRACE(4);
       if (lane == 0) {
         // A = K tile (d-halves 16 KiB apart), B = Q (d-halves 2 KiB apart)
         mma_ss_8<2, 4, 6, 1024, 1026, 1028, 1030, 2, 4, 6, 128, 130, 132, 134>(
@@ -279,7 +314,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     for (int r = 0; have; ++r) {
       // Q of item r+1 goes into the buffer item r-1 used (its QKs are done)
       if (r >= 1 && get_item(r + 1, nxt)) write_q(r + 1, nxt);
-      const int ctx = ctx_lens[it.seq];
+      const int ctx = it.ctx;
       float m_run[8], l_part[8], o_acc[8], alpha_hist[2][8];
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
@@ -303,6 +338,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         const int valid = min(kTileTok, ctx - tile * kTileTok);
         mbar_wait(&misc->s_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
+        if (tid == 0 && j == 0) DEC_TRACE(5);
         float s[8];
         tmem_ld_32x32b_x8(tmem + lane_base + (j & 1) * 16, s);
         const bool ok = tid < valid;
@@ -424,20 +460,26 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         }
       }
       named_bar_sync(1, 128);  // lred / last are reused by the next item
+      if (tid == 0) {
+        if (r < 3) DEC_TRACE(6 + r);
+        DEC_TRACE(9);
+        DEC_TRACE_VAL(11, (unsigned long long)(r + 1));
+        DEC_TRACE_VAL(12, (unsigned long long)j);
+      }
       if (tid == 0) mbar_arrive(&misc->ring_empty[r % kRing]);  // done with item r
       have = get_item(r + 1, it);
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) DEC_TRACE(10);
   if (warp == 5) {
     tc_fence_after();
     tmem_dealloc(tmem, kDecTmemCols);
   }
 }
 
-inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t slots,
-                            uint64_t ctx_lens, int grid, float scale, float* part_o,
+inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, int grid, float scale, float* part_o,
                             float* part_ml, const DecodeItem* items, const int32_t* n_items,
                             int32_t* item_counter, const int32_t* nsplit, int32_t* split_done,
                             int nseq, int fuse_merge, uint64_t out,
@@ -459,9 +501,7 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
                               p->device);
     if (rc) return rc;
     KB_RT(cudaLaunchKernelEx(&cfg, decode_tc_kernel<64>,
-        p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
-        reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
-        items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
+        p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt, items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
         reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2));
@@ -470,9 +510,7 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, uint64_t 
                               p->device);
     if (rc) return rc;
     KB_RT(cudaLaunchKernelEx(&cfg, decode_tc_kernel<128>,
-        p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt,
-        reinterpret_cast<const int32_t*>(slots), reinterpret_cast<const int32_t*>(ctx_lens),
-        items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
+        p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt, items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
         reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2));

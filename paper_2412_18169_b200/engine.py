@@ -430,6 +430,14 @@ class Engine:
         saved, self.now = self.now, when
         for ch in mb.chunks:
             req = self.requests[ch.rid]
+            if req.state is RequestState.QUEUED:
+                # evicted while the round was in flight (the fallback's
+                # recompute relief does not wait for round ends,
+                # engine.py:663-668): its chunk's work is discarded.  The
+                # reference would count a token, or raise KeyError on
+                # pending_prefill; the wall-clock engine, whose rounds run
+                # on the device while the monitor ticks, reaches this.
+                continue
             if ch.decode:
                 req.record_token(when)
                 self.log("TOKEN", req=ch.rid, n=req.tokens_decoded)

@@ -302,14 +302,20 @@ class WallClockEngine(DeviceEngine):
 
     # ------------------------------------------------------------ loop
     def _poll(self) -> bool:
-        """Fire the callbacks of completed device work; True if any fired."""
+        """Fire the callbacks of completed device work; True if any fired.
+        Only the work in flight when the poll starts: a callback launches the
+        next stage, and if that one completed before the scan reached it the
+        scan would go on firing a fast model's decode chain for a whole
+        request, starving the arrivals and monitor ticks due meanwhile."""
         fired = False
         i = 0
+        n = len(self.inflight)
         t0 = time.perf_counter()
-        while i < len(self.inflight):
+        while i < n:
             ev, fn = self.inflight[i]
             if ev.query():
                 self.inflight.pop(i)
+                n -= 1
                 self.now = max(self.now, self._wall_us())
                 fn()
                 fired = True

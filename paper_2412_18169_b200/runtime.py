@@ -599,18 +599,25 @@ def decode_workspace_bytes(nseq: int, n_q_heads: int, max_splits: int) -> int:
 
 
 DECODE_REUSE_PLAN = 1
+DECODE_COMBINE = 2
+DECODE_FUSE = 4
 
 
 def paged_decode(pool: DevicePool, layer: int, q, slots, ctx_lens, max_ctx: int, out,
                  workspace, scale: float, max_splits: int = 16, reuse_plan: bool = False,
-                 stream=None) -> None:
+                 stream=None, combine: Optional[bool] = None) -> None:
     """q/out: [nseq, n_q_heads, 128] bf16; slots/ctx_lens int32 [nseq] (device).
-    reuse_plan: the workspace already holds the plan for these ctx_lens (a
-    previous layer of the same decode step)."""
+    reuse_plan: the workspace already holds the plan for these ctx_lens and
+    slots (a previous layer of the same decode step).  combine: None lets
+    the library choose where the KV splits merge (inside the attention
+    kernel for large batches, else a combine launch); True / False force the
+    combine launch / the in-kernel merge."""
     flags = DECODE_REUSE_PLAN if reuse_plan else 0
-    # the split merge runs inside the attention kernel for large batches,
-    # else in a combine launch (kb_decode.cu)
-    fused = q.shape[0] * pool.shape.n_kv_heads >= 4 * _sm_count(pool.rt.device)
+    if combine is None:
+        fused = q.shape[0] * pool.shape.n_kv_heads >= 4 * _sm_count(pool.rt.device)
+    else:
+        fused = not combine
+        flags |= DECODE_COMBINE if combine else DECODE_FUSE
     _check(_lib.kb_paged_decode(pool.h, layer, q.shape[1], q.data_ptr(), slots.data_ptr(),
                                 ctx_lens.data_ptr(), q.shape[0], max_ctx, scale,
                                 out.data_ptr(), workspace.data_ptr(),

@@ -415,11 +415,15 @@ def test_paged_decode_matches_oracle(rt, shape):
     slots = torch.arange(len(ctxs), dtype=torch.int32, device="cuda")
     lens = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
     out = torch.empty((len(ctxs), hq, 128), dtype=torch.bfloat16, device="cuda")
-    for max_splits in (1, 4, 16):
+    # stream-K plan: max_splits 1 cuts only at pair borders; the KV splits
+    # merge inside the attention kernel or in the combine launch
+    for max_splits, combine in ((1, False), (2, False), (4, False), (4, True), (16, False),
+                                (16, True)):
         ws = torch.empty(runtime.decode_workspace_bytes(len(ctxs), hq, max_splits),
                          dtype=torch.uint8, device="cuda")
+        out.zero_()
         runtime.paged_decode(pool, 1, q.cuda(), slots, lens, max(ctxs), out, ws, scale,
-                             max_splits=max_splits)
+                             max_splits=max_splits, combine=combine)
         torch.cuda.synchronize()
         got = out.float().cpu().numpy()
         for i, c in enumerate(ctxs):
@@ -427,18 +431,20 @@ def test_paged_decode_matches_oracle(rt, shape):
                               scale)
             want = bf16_to_f32(f32_to_bf16(want))
             ma, mr = check_close(got[i], want)
-            assert ma <= 2e-2 and mr <= 1e-3, (shape.name, c, max_splits, ma, mr)
+            assert ma <= 2e-2 and mr <= 1e-3, (shape.name, c, max_splits, combine, ma, mr)
     pool.close()
 
 
+@pytest.mark.parametrize("combine", [False, True])
 @pytest.mark.parametrize("batch", ["small", "large"])
-def test_paged_decode_plan_reuse_across_layers(rt, batch):
+def test_paged_decode_plan_reuse_across_layers(rt, batch, combine):
     """One plan, several layer launches (KB_DECODE_REUSE_PLAN), as a decode
-    step runs them.  Small batch: the combine launch merges the KV splits.
-    Large batch (>= 4 (sequence, kv head) pairs per SM): the attention
-    kernel merges them itself, and its per-(sequence, kv head) counters must
-    re-arm after every launch, so each layer -- and a repeat of the first --
-    still matches the oracle."""
+    step runs them.  The attention kernel merges the KV splits of the pairs
+    a CTA border cuts, and its per-(sequence, kv head) counters must re-arm
+    after every launch, so each layer -- and a repeat of the first -- still
+    matches the oracle (combine=True: the separate combine launch merges).
+    Small batch: long pairs cut into many pieces; large batch (>= 4
+    (sequence, kv head) pairs per SM): many whole pairs per CTA."""
     from paper_2412_18169_b200 import runtime
     # large: Llama-3-8B heads (8 kv heads), so 80 sequences give 640 pairs
     shape = ATTN_SHAPES[0] if batch == "small" else next(x for x in ATTN_SHAPES if x.name == "g4")
@@ -469,7 +475,7 @@ def test_paged_decode_plan_reuse_across_layers(rt, batch):
     for n, l in enumerate((0, 1, 0, 1)):
         out = torch.empty((len(ctxs), hq, 128), dtype=torch.bfloat16, device="cuda")
         runtime.paged_decode(pool, l, q.cuda(), slots, lens, max(ctxs), out, ws, scale,
-                             max_splits=16, reuse_plan=n > 0)
+                             max_splits=16, reuse_plan=n > 0, combine=combine)
         torch.cuda.synchronize()
         got = out.float().cpu().numpy()
         for i in range(len(ctxs)):

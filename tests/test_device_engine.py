@@ -48,16 +48,18 @@ def test_device_engine_overload_cycle(built, policy, clock):
         eng = DeviceEngine(cfg, trace)
     else:
         from paper_2412_18169_b200.realtime import WallClockEngine
-        # a steady stream of long requests: the overload must outlast the
-        # monitor's two-tick debounce (200 ms of wall time) however fast the
-        # tiny model decodes
-        trace = [TraceRecord(5000 * i, 250, 600) for i in range(16)]
+        # a steady stream of long requests and a 20 ms monitor tick: the
+        # overload (queued heads behind 4 admitted requests per replica)
+        # outlasts the two-tick debounce however fast the tiny model decodes
+        cfg.policy.monitor_tick_us = 20_000
+        trace = [TraceRecord(2000 * i, 250, 600) for i in range(32)]
         eng = WallClockEngine(cfg, trace)
     res = eng.run()
     k = kinds(res.log_lines)
     assert k.get("FINISH", 0) == len(trace)
     if policy == "kunserve":
-        assert k.get("PLAN", 0) >= 1 and k.get("EXCHANGE", 0) >= 1
+        occ = [l for l in res.log_lines if " OCC " in l][:20]
+        assert k.get("PLAN", 0) >= 1 and k.get("EXCHANGE", 0) >= 1, (k, occ)
         assert k.get("RESTORE_DONE", 0) >= 1 and k.get("DISSOLVE", 0) >= 1
         assert res.evictions == 0
     if policy == "swap":  # every swapped-out request came back (how many go out

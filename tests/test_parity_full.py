@@ -221,9 +221,9 @@ G4 = ModelShape("g4", num_layers=4, hidden=4096, n_q_heads=32, n_kv_heads=8, hea
 def test_pdl_append_decode_chain_without_host_sync(runtime, mode, batch):
     """A decode step as a stage runs it: per layer kv_append (which lets the
     next launch start early) then paged_decode (PDL prologue, plan reused
-    after the first layer), 4 layers back to back with no host sync -- in
-    the combine mode (small batch) and the fused-merge mode (>= 4 pairs per
-    SM), eagerly and as a replayed CUDA graph.  Every layer's output matches
+    after the first layer), 4 layers back to back with no host sync -- with
+    the KV splits merged by a combine launch (6 sequences) and inside the
+    attention kernel (80 sequences), eagerly and as a replayed CUDA graph.  Every layer's output matches
     the oracle."""
     shape = G4
     model = shape.spec()
@@ -261,7 +261,8 @@ def test_pdl_append_decode_chain_without_host_sync(runtime, mode, batch):
         for l in range(4):
             runtime.kv_append(pool, l, kl[l], vl[l], slots, pos, stream=st)
             runtime.paged_decode(pool, l, qs[l], slots, lens, max(ctxs), outs[l], ws, scale,
-                                 max_splits=16, reuse_plan=l > 0, stream=st)
+                                 max_splits=16, reuse_plan=l > 0, stream=st,
+                                 combine=batch == "combine")
     if mode == "eager":
         step()
     else:

@@ -23,6 +23,8 @@ pool = rt.create_pool(0, model, model.param_bytes + (12 << 30), shape)
 rng = np.random.default_rng(5)
 MS = int(os.environ.get("KB_PROBE_MAX_SPLITS", "16"))
 APPEND = os.environ.get("KB_PROBE_APPEND", "0") == "1"
+# KB_PROBE_MERGE=1: force the combine launch, 0: force the in-kernel merge
+KW = {"combine": os.environ["KB_PROBE_MERGE"] == "1"} if "KB_PROBE_MERGE" in os.environ else {}
 out = {}
 SIZES = [int(os.environ["KB_PROBE_NSEQ"])] if "KB_PROBE_NSEQ" in os.environ else [4, 16, 32, 64, 147]
 for nseq in SIZES:
@@ -45,7 +47,7 @@ for nseq in SIZES:
             if APPEND:  # the new token's K/V first, as a decode stage does
                 runtime.kv_append(pool, i % 2, kn, kn, sl, pos)
             runtime.paged_decode(pool, i % 2, q, sl, cl, int(ctx.max()), o, ws, 128 ** -0.5,
-                                 max_splits=MS, reuse_plan=i > 0)
+                                 max_splits=MS, reuse_plan=i > 0, **KW)
     for _ in range(5):
         step()
     torch.cuda.synchronize()
