@@ -25,6 +25,23 @@ constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per per
 #define KB_DEC_MIN_TILES 2
 #endif
 constexpr int kMinTiles = KB_DEC_MIN_TILES;  // shortest split (128-token tiles)
+#ifndef KB_DEC_UNEVEN
+#define KB_DEC_UNEVEN 0
+#endif
+#ifndef KB_DEC_TSEARCH
+#define KB_DEC_TSEARCH 1
+#endif
+// piece k of a pair of `tiles` tiles cut into s splits of target length T:
+// even (k*tiles/s) or, KB_DEC_UNEVEN, T-long pieces and a short remainder
+__device__ __forceinline__ void piece(int tiles, int s, int T, int k, int& beg, int& len) {
+  if (KB_DEC_UNEVEN && s * T >= tiles) {
+    beg = k * T;
+    len = min(T, tiles - beg);
+  } else {
+    beg = k * tiles / s;
+    len = (k + 1) * tiles / s - beg;
+  }
+}
 
 // Split-KV combine for small batches: one CTA per (sequence, q head),
 // thread = head_dim lane.  Sequences with 0 splits (no context) get a zero
@@ -83,6 +100,33 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
     T = (int)(per > (unsigned long long)min_tiles ? per : min_tiles);
   }
   __syncthreads();
+  // ceil() per sequence makes the item count overshoot kItemsPerCta per CTA;
+  // the few items past grid * kItemsPerCta then run as a third round on a
+  // handful of CTAs (a 6 us tail at 16 sequences).  Warp w counts the items
+  // T + w would give; the smallest T that fits the rounds wins.
+  if (KB_DEC_TSEARCH) {
+    __shared__ long long cnt_w[32];
+    const int w = tid >> 5, lane = tid & 31;
+    const int Tc = T + w;
+    long long c = 0;
+    for (int i = lane; i < nseq; i += 32) {
+      const int tiles = (ctx[i] + kTileTok - 1) / kTileTok;
+      if (tiles) c += min(max((tiles + Tc - 1) / Tc, 1), max_splits);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) cnt_w[w] = c * Hkv;
+    __syncthreads();
+    if (tid == 0) {
+      const long long target = (long long)grid_ctas * kItemsPerCta;
+      for (int k = 0; k < 32; ++k)
+        if (cnt_w[k] <= target) {
+          T += k;
+          break;
+        }
+    }
+    __syncthreads();
+  }
   auto splits_of = [&](int tiles) {
     int s = (tiles + T - 1) / T;
     return s < 1 ? 1 : (s > max_splits ? max_splits : s);
@@ -94,7 +138,8 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
     nsplit_of[i] = tiles == 0 ? 0 : s;
     if (tiles == 0) continue;
     for (int k = 0; k < s; ++k) {
-      const int len = (k + 1) * tiles / s - k * tiles / s;
+      int beg, len;
+      piece(tiles, s, T, k, beg, len);
       atomicAdd(&hist[kLenBuckets - 1 - min(len, kLenBuckets - 1)], Hkv);
     }
   }
@@ -135,7 +180,8 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
     if (tiles == 0) continue;
     const int s = splits_of(tiles);
     for (int k = 0; k < s; ++k) {
-      const int beg = k * tiles / s, len = (k + 1) * tiles / s - beg;
+      int beg, len;
+      piece(tiles, s, T, k, beg, len);
       const int b = kLenBuckets - 1 - min(len, kLenBuckets - 1);
       for (int h = 0; h < Hkv; ++h) {
         const int pos = atomicAdd(&cursor[b], 1);
@@ -215,7 +261,7 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   if (flags & KB_DECODE_FUSE) fuse = 1;
   rc = launch_decode_tc(p, layer, n_q_heads, q, grid, scale, part_o, part_ml,
                         items, n_items, item_counter, nsplit, split_done, nseq, fuse, out,
-                        max_splits, st);
+                        max_splits, (flags & KB_DECODE_REUSE_PLAN) ? 1 : 0, st);
   if (rc) return rc;
   if (!fuse) {
     // programmatic dependent launch: the combine CTAs start while the

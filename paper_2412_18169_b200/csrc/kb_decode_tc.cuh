@@ -37,7 +37,8 @@ constexpr int kStageBytes = 65536;       // K (32 KiB) + V (32 KiB) for 128 toke
 constexpr int kHalfBytes = 16384;        // one 64-wide d-half of a 128-token tile
 constexpr int kQBytes = 4096;            // 16 rows x 128 d bf16, SW128 K-major
 constexpr int kPBytes = 4096;            // 16 rows x 128 tok bf16, SW128 K-major
-constexpr int kDecSmem = kDecStages * kStageBytes + 2 * kQBytes + 2 * kPBytes + 1024 + 1024;
+constexpr int kDecMiscBytes = 2048;
+constexpr int kDecSmem = kDecStages * kStageBytes + 2 * kQBytes + 2 * kPBytes + kDecMiscBytes + 1024;
 constexpr uint32_t kDecTmemCols = 64;    // S0 S1 O0 O1, 16 columns each
 constexpr int kRing = 16;                // dynamically fetched work items in flight per CTA
 
@@ -57,7 +58,7 @@ struct DecodeMisc {
   uint64_t q_full[2];
   uint64_t ring_full[kRing];   // item index published by the producer
   uint64_t ring_empty[kRing];  // MMA warp + softmax done with the item
-  int32_t ring_item[kRing];    // index into the sorted item list, -1 = no more work
+  DecodeItem ring_it[kRing];   // the published items (nt < 0: no more work)
   uint32_t tmem_base;
   int32_t last;  // this CTA finished the last split of its (sequence, kv head)
   float red[2][4][8];
@@ -90,9 +91,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
                  int nseq, int fuse_merge, __nv_bfloat16* __restrict__ out,
                  float* __restrict__ part_o,
                  float* __restrict__ part_ml, int Hkv, int G, int Hq, int L, int maxp, int layer,
-                 int max_splits, float scale_log2) {
+                 int max_splits, float scale_log2, int early_loads) {
   using namespace sm100;
-  constexpr int kPPT = kTileTok / kB;  // pages per tile
   // Work items are sorted longest first and handed out dynamically: CTA b
   // starts with item b, then its producer warp takes the next index from a
   // per-layer global counter (a greedy longest-processing-time schedule, so
@@ -107,6 +107,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
   uint8_t* sQ = smem + kDecStages * kStageBytes;  // two buffers (item parity)
   uint8_t* sP = sQ + 2 * kQBytes;  // two buffers (tile parity)
   DecodeMisc* misc = reinterpret_cast<DecodeMisc*>(sP + 2 * kPBytes);
+  static_assert(sizeof(DecodeMisc) <= kDecMiscBytes, "DecodeMisc outgrew its smem slot");
 
   if (warp == 5) {
     if (lane == 0) {
@@ -134,87 +135,118 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = misc->tmem_base;
-  // launched with programmatic stream serialization: the prologue above
-  // overlapped the previous kernel's tail; everything below may read what
-  // it wrote (plan, q, appended K/V, the previous layer's workspace use)
-  pdl_wait();
-  pdl_launch_dependents();
-  if (tid == 0) DEC_TRACE(1);
-  const int n_items = *n_items_ptr;
-  // item r of this CTA (every role reads the ring in the same order)
+  constexpr int kPPT = kTileTok / kB;  // pages per tile
+  // issue the TMA loads of tile t of item `it` into stage j % kDecStages
+  auto issue_tile = [&](const DecodeItem& it, int t, int j) {
+    const int stage = j % kDecStages;
+    const int tile = it.t_beg + t;
+    const int32_t* bt_row = bt + ((int64_t)it.slot * L + layer) * maxp;
+    int npg = 0;
+    int32_t pages[kPPT];
+#pragma unroll
+    for (int k = 0; k < kPPT; ++k) {
+      const int pi = tile * kPPT + k;
+      pages[k] = (pi * kB < it.ctx) ? bt_row[pi] : -1;
+      npg += pages[k] >= 0;
+    }
+    mbar_arrive_expect_tx(&misc->full[stage], (uint32_t)(npg * kB * 512));
+    uint8_t* sK = smem + stage * kStageBytes;
+    uint8_t* sV = sK + 2 * kHalfBytes;
+#pragma unroll
+    for (int k = 0; k < kPPT; ++k) {
+      if (pages[k] < 0) continue;
+      const int rk = ((pages[k] * 2 + 0) * Hkv + it.h) * kB;
+      const int rv = ((pages[k] * 2 + 1) * Hkv + it.h) * kB;
+      const int off = k * kB * 128;
+      tma_load_2d(sK + off, &tmap, 0, rk, &misc->full[stage]);
+      tma_load_2d(sK + kHalfBytes + off, &tmap, 64, rk, &misc->full[stage]);
+      tma_load_2d(sV + off, &tmap, 0, rv, &misc->full[stage]);
+      tma_load_2d(sV + kHalfBytes + off, &tmap, 64, rv, &misc->full[stage]);
+    }
+  };
+  // item r of this CTA (every role reads the ring in the same order; the
+  // producer copies each item into the ring, so no role loads an item from
+  // global memory at an item border)
   auto get_item = [&](int r, DecodeItem& it) -> bool {
     const int slot = r % kRing;
     mbar_wait(&misc->ring_full[slot], (r / kRing) & 1);
-    const int idx = *reinterpret_cast<volatile int32_t*>(&misc->ring_item[slot]);
-    if (idx < 0) return false;
-    it = items[idx];
-    return true;
+    it = misc->ring_it[slot];
+    return it.nt > 0;
   };
+  // Producer state: items are published two ahead of the loads, so the
+  // softmax can stage the next item's Q early.
+  const bool producer = warp == 4 && lane == 0;
+  int n_items = 0, npre = 0, published = 0;
+  bool exhausted = false;
+  auto publish = [&]() {
+    if (exhausted) return;
+    const int r = published++;
+    const int slot = r % kRing;
+    if (r >= kRing) mbar_wait(&misc->ring_empty[slot], ((r / kRing) - 1) & 1);
+    // the first item is static (no atomic round trip before the first
+    // load); every CTA then makes exactly one failing fetch, and the last
+    // of those re-arms the counter (a reused plan)
+    const int grid = (int)gridDim.x;
+    int idx = r == 0 ? (int)blockIdx.x : -1;
+    if (idx < 0 || idx >= n_items) {
+      const int raw = atomicAdd(item_counter + layer, 1);
+      if (idx < 0) idx = grid + raw;
+      if (idx >= n_items) {
+        if (raw == max(n_items - grid, 0) + grid - 1) item_counter[layer] = 0;
+        idx = -1;
+        exhausted = true;
+      }
+    }
+    DecodeItem v{};
+    v.nt = -1;
+    if (idx >= 0) v = items[idx];
+    misc->ring_it[slot] = v;
+    mbar_arrive(&misc->ring_full[slot]);
+  };
+  // Launched with programmatic stream serialization: the prologue above
+  // overlapped the previous kernel's tail.  With a reused plan
+  // (early_loads) the producer also publishes its static first item and
+  // starts that item's loads before griddepcontrol.wait: the plan, the
+  // block tables and every K/V row but the newest token's were written by
+  // grids that completed before the previous launch could start (only
+  // kv_append, the usual predecessor, writes K/V -- the newest token's row,
+  // which no tile loaded here holds).  q and the counters are read after it.
+  if (early_loads && producer) {
+    n_items = *n_items_ptr;
+    if ((int)blockIdx.x < n_items) {
+      publish();
+      DecodeItem it0;
+      get_item(0, it0);
+      // tiles [0, nsafe) end before the newest token (position ctx - 1)
+      const int nsafe = (it0.ctx - 1) / kTileTok - it0.t_beg;
+      npre = min(min(it0.nt, kDecStages), max(nsafe, 0));
+      for (int t = 0; t < npre; ++t) issue_tile(it0, t, t);
+      if (npre) DEC_TRACE(3);
+    }
+  }
+  // everything below may read what the previous grid wrote (q, the newest
+  // K/V rows, the previous layer's workspace use, a fresh plan)
+  pdl_wait();
+  pdl_launch_dependents();
+  if (tid == 0) DEC_TRACE(1);
+  if (producer && published == 0) n_items = *n_items_ptr;
 
   if (warp == 4) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
-      int published = 0;
-      bool exhausted = false;
-      // fetch the next item index and publish it; two items ahead of the
-      // loads, so the softmax can stage the next item's Q early
-      auto publish = [&]() {
-        if (exhausted) return;
-        const int r = published++;
-        const int slot = r % kRing;
-        if (r >= kRing) mbar_wait(&misc->ring_empty[slot], ((r / kRing) - 1) & 1);
-        // the first item is static (no atomic round trip before the first
-        // load); every CTA then makes exactly one failing fetch, and the
-        // last of those re-arms the counter (a reused plan)
-        const int grid = (int)gridDim.x;
-        int idx = r == 0 ? (int)blockIdx.x : -1;
-        if (idx < 0 || idx >= n_items) {
-          const int raw = atomicAdd(item_counter + layer, 1);
-          if (idx < 0) idx = grid + raw;
-          if (idx >= n_items) {
-            if (raw == max(n_items - grid, 0) + grid - 1) item_counter[layer] = 0;
-            idx = -1;
-            exhausted = true;
-          }
-        }
-        misc->ring_item[slot] = idx;
-        mbar_arrive(&misc->ring_full[slot]);
-      };
-      publish();  // item 0 (static); item 1 once item 0's first loads are out
-      bool second = false;
+      if (published == 0) publish();  // item 0; item 1 once item 0's first loads are out
+      bool second = npre > 0;
+      if (second) publish();
       int j = 0;  // global tile counter of this CTA
       for (int r = 0;; ++r) {
         DecodeItem it;
         if (!get_item(r, it)) break;
         if (r == 0) DEC_TRACE(2);
-        const int ctx = it.ctx;
-        const int32_t* bt_row = bt + ((int64_t)it.slot * L + layer) * maxp;
         for (int t = 0; t < it.nt; ++t, ++j) {
+          if (r == 0 && t < npre) continue;  // issued before griddepcontrol.wait
           const int stage = j % kDecStages;
           if (j >= kDecStages) mbar_wait(&misc->empty[stage], ((j / kDecStages) - 1) & 1);
-          const int tile = it.t_beg + t;
-          int npg = 0;
-          int32_t pages[kPPT];
-#pragma unroll
-          for (int k = 0; k < kPPT; ++k) {
-            const int pi = tile * kPPT + k;
-            pages[k] = (pi * kB < ctx) ? bt_row[pi] : -1;
-            npg += pages[k] >= 0;
-          }
-          mbar_arrive_expect_tx(&misc->full[stage], (uint32_t)(npg * kB * 512));
-          uint8_t* sK = smem + stage * kStageBytes;
-          uint8_t* sV = sK + 2 * kHalfBytes;
-#pragma unroll
-          for (int k = 0; k < kPPT; ++k) {
-            if (pages[k] < 0) continue;
-            const int rk = ((pages[k] * 2 + 0) * Hkv + it.h) * kB;
-            const int rv = ((pages[k] * 2 + 1) * Hkv + it.h) * kB;
-            const int off = k * kB * 128;
-            tma_load_2d(sK + off, &tmap, 0, rk, &misc->full[stage]);
-            tma_load_2d(sK + kHalfBytes + off, &tmap, 64, rk, &misc->full[stage]);
-            tma_load_2d(sV + off, &tmap, 0, rv, &misc->full[stage]);
-            tma_load_2d(sV + kHalfBytes + off, &tmap, 64, rv, &misc->full[stage]);
-          }
+          issue_tile(it, t, j);
           if (j == 0) DEC_TRACE(3);
           if (!second) {
             second = true;
@@ -285,19 +317,26 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     }
   } else {
     // ------------------------------------------------ softmax / epilogue (tid < 128)
-    // sequences with no context have no item: their rows are zero
-    for (int sq = blockIdx.x; sq < nseq; sq += gridDim.x)
-      if (nsplit_of[sq] == 0)
-        for (int h = 0; h < Hq; ++h) out[((int64_t)sq * Hq + h) * 128 + tid] = __float2bfloat16(0.f);
-    auto write_q = [&](int r, const DecodeItem& it) {
+    // Q of an item: G rows (<= 8) x 16 chunks of 16 bytes, two per thread;
+    // loaded into registers early, stored (SW128 K-major) when the buffer
+    // is free, so the global load never sits on the softmax's critical path
+    int4 qv[2];
+    auto load_q = [&](const DecodeItem& it) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int c = tid + k * 128, g = c >> 4, chunk = c & 15;
+        qv[k] = g < G ? reinterpret_cast<const int4*>(
+                            q + ((int64_t)it.seq * Hq + it.h * G + g) * 128)[chunk]
+                      : make_int4(0, 0, 0, 0);
+      }
+    };
+    auto store_q = [&](int r) {
       uint8_t* dst = sQ + (r & 1) * kQBytes;
-      for (int c = tid; c < 16 * 16; c += 128) {
-        const int g = c >> 4, chunk = c & 15;  // 16-byte chunk of 8 d values
-        int4 val = make_int4(0, 0, 0, 0);
-        if (g < G)
-          val = reinterpret_cast<const int4*>(q + ((int64_t)it.seq * Hq + it.h * G + g) * 128)[chunk];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int c = tid + k * 128, g = c >> 4, chunk = c & 15;
         const uint32_t off = (chunk >> 3) * 2048 + g * 128 + ((((chunk & 7) ^ (g & 7)) & 7) << 4);
-        *reinterpret_cast<int4*>(dst + off) = val;
+        *reinterpret_cast<int4*>(dst + off) = qv[k];
       }
       fence_proxy_async_smem();
       mbar_arrive(&misc->q_full[r & 1]);
@@ -306,16 +345,21 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     for (int c = tid; c < 2 * kPBytes / 16; c += 128)
       reinterpret_cast<int4*>(sP)[c] = make_int4(0, 0, 0, 0);
     DecodeItem it, nxt;
-    bool have = get_item(0, it);
-    if (have) write_q(0, it);
-    if (have && get_item(1, nxt)) write_q(1, nxt);
+    bool have = get_item(0, it), nhave = false;
+    if (have) {
+      load_q(it);
+      store_q(0);
+    }
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     int j = 0;
     for (int r = 0; have; ++r) {
-      // Q of item r+1 goes into the buffer item r-1 used (its QKs are done)
-      if (r >= 1 && get_item(r + 1, nxt)) write_q(r + 1, nxt);
+      // Q of item r+1 goes into the buffer item r-1 used (its QKs are done):
+      // the item is read from the ring after this item's first tile (the
+      // producer publishes it once this item's loads are out, so the
+      // softmax never waits on it), Q loaded then and stored one tile later
+      int q_state = 0;  // 0: item r+1 not read yet, 1: Q loaded, 2: stored / none
       const int ctx = it.ctx;
-      float m_run[8], l_part[8], o_acc[8], alpha_hist[2][8];
+      float m_run[8], l_part[8], o_acc[8], alpha0[8], alpha1[8];  // alpha by tile parity
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
         m_run[g] = -INFINITY;
@@ -331,7 +375,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         float ov[8];
         tmem_ld_32x32b_x8(tmem + lane_base + 32 + (x & 1) * 16, ov);
 #pragma unroll
-        for (int g = 0; g < 8; ++g) o_acc[g] = o_acc[g] * alpha_hist[x & 1][g] + ov[g];
+        for (int g = 0; g < 8; ++g) o_acc[g] = o_acc[g] * ((x & 1) ? alpha1[g] : alpha0[g]) + ov[g];
       };
       for (int t = 0; t < it.nt; ++t, ++j) {
         const int tile = it.t_beg + t;
@@ -373,7 +417,10 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
             alpha = exp2f(m_run[g] - m_new);
             p[g] = exp2f(s[g] - m_new);
           }
-          alpha_hist[j & 1][g] = alpha;
+          if (j & 1)
+            alpha1[g] = alpha;
+          else
+            alpha0[g] = alpha;
           l_part[g] = l_part[g] * alpha + p[g];
           m_run[g] = m_new;
         }
@@ -402,6 +449,22 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           *reinterpret_cast<__half*>(pbuf + sw128_offset(g, tid & 63)) = __float2half_rn(p[g]);
         fence_proxy_async_smem();
         mbar_arrive(&misc->p_full[j & 1]);
+        if (q_state == 1) {
+          store_q(r + 1);
+          q_state = 2;
+        }
+        if (q_state == 0) {
+          nhave = get_item(r + 1, nxt);
+          q_state = 2;
+          if (nhave) {
+            load_q(nxt);
+            q_state = 1;
+            if (t == it.nt - 1) {  // a one-tile item: store right away
+              store_q(r + 1);
+              q_state = 2;
+            }
+          }
+        }
       }
       if (it.nt >= 2) fold(j - 2);
       fold(j - 1);
@@ -467,8 +530,13 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         DEC_TRACE_VAL(12, (unsigned long long)j);
       }
       if (tid == 0) mbar_arrive(&misc->ring_empty[r % kRing]);  // done with item r
-      have = get_item(r + 1, it);
+      it = nxt;  // item r+1, read from the ring during item r
+      have = nhave;
     }
+    // sequences with no context have no item: their rows are zero
+    for (int sq = blockIdx.x; sq < nseq; sq += gridDim.x)
+      if (nsplit_of[sq] == 0)
+        for (int h = 0; h < Hq; ++h) out[((int64_t)sq * Hq + h) * 128 + tid] = __float2bfloat16(0.f);
   }
   tc_fence_before();
   __syncthreads();
@@ -483,7 +551,7 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, int grid,
                             float* part_ml, const DecodeItem* items, const int32_t* n_items,
                             int32_t* item_counter, const int32_t* nsplit, int32_t* split_done,
                             int nseq, int fuse_merge, uint64_t out,
-                            int max_splits, cudaStream_t st) {
+                            int max_splits, int early_loads, cudaStream_t st) {
   const int Hkv = p->m.n_kv_heads, B = p->m.block_tokens;
   const float scale_log2 = scale * 1.4426950408889634f;
   cudaLaunchAttribute pdl[1];
@@ -504,7 +572,7 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, int grid,
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt, items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
         reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
-        Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2));
+        Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2, early_loads));
   } else {
     int rc = ensure_smem_attr(reinterpret_cast<const void*>(decode_tc_kernel<128>), kDecSmem,
                               p->device);
@@ -513,7 +581,7 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, int grid,
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt, items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
         reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
-        Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2));
+        Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2, early_loads));
   }
   KB_LAUNCH_CHECK();
   return KB_OK;

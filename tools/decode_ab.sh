@@ -10,5 +10,7 @@ for m in 0 1; do
   echo "== _kb.so combine=$m forced" >> gpurun_out/${TAG}_decode_ab.log
   KB_PROBE_MERGE=$m timeout 300 python tools/decode_batch_probe.py >> gpurun_out/${TAG}_decode_ab.log 2>&1
 done
+echo "== _kb.so append first" >> gpurun_out/${TAG}_decode_ab.log
+KB_PROBE_APPEND=1 timeout 300 python tools/decode_batch_probe.py >> gpurun_out/${TAG}_decode_ab.log 2>&1
 KB_PROBE_SIZES=16,147 timeout 300 python tools/decode_trace_probe.py > gpurun_out/${TAG}_trace.log 2>&1
 cat gpurun_out/${TAG}_decode_ab.log gpurun_out/${TAG}_trace.log | grep -v "^\["
