@@ -352,6 +352,102 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     }
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     int j = 0;
+    // Running state of the current item and of the previous ("pending")
+    // item, whose epilogue is deferred until the next item's first P is
+    // out: the tensor core and the TMA loads never wait on an item border.
+    float m_run[8], l_part[8], o_acc[8], alpha0[8], alpha1[8];  // alpha by tile parity
+    float pm[8], pl[8], po[8];
+    bool pend = false;
+    DecodeItem pit{};
+    int pr = 0;
+    // O of tile x is folded two tiles later (or at the item's end), so the
+    // softmax never waits on the P.V it has just released:
+    //   acc = acc * alpha_x + O_x,  alpha_x = exp2(m_{x-1} - m_x)
+    auto fold = [&](int x, float (&acc)[8]) {
+      mbar_wait(&misc->o_full[x & 1], (x >> 1) & 1);
+      tc_fence_after();
+      float ov[8];
+      tmem_ld_32x32b_x8(tmem + lane_base + 32 + (x & 1) * 16, ov);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) acc[g] = acc[g] * ((x & 1) ? alpha1[g] : alpha0[g]) + ov[g];
+    };
+    // the pending item's epilogue (its O fully folded): normalise or write
+    // the split partials, merge (fused mode), release its ring slot
+    auto finalize = [&]() {
+      // l = sum over the 128 token lanes
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        float v = pl[g];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) misc->lred[warp][g] = v;
+      }
+      named_bar_sync(1, 128);
+      const int ns = nsplit_of[pit.seq];
+      for (int g = 0; g < G; ++g) {
+        const float l = misc->lred[0][g] + misc->lred[1][g] + misc->lred[2][g] + misc->lred[3][g];
+        const int64_t hrow = (int64_t)pit.seq * Hq + pit.h * G + g;
+        if (ns == 1) {  // no merge needed
+          out[hrow * 128 + tid] = __float2bfloat16(l > 0.f ? po[g] / l : 0.f);
+        } else {
+          const int64_t row = hrow * max_splits + pit.split;
+          part_o[row * 128 + tid] = po[g];
+          if (tid == 0) {
+            part_ml[row * 2] = pm[g];
+            part_ml[row * 2 + 1] = l;
+          }
+        }
+      }
+      if (ns > 1 && fuse_merge) {
+        // Split-KV merge, fused: the CTA that finishes the last split of
+        // (sequence, kv head) merges all of them (threadfence-reduction
+        // pattern) -- no combine launch per layer.  It re-arms the counter
+        // for the next layer's launch.  (Chosen for large batches only: the
+        // fence + counter per split item costs more than a combine launch
+        // when the items are short.)
+        __threadfence();
+        named_bar_sync(1, 128);
+        int32_t* done = split_done + pit.seq * Hkv + pit.h;
+        if (tid == 0) misc->last = atomicAdd(done, 1) == ns - 1;
+        named_bar_sync(1, 128);
+        if (misc->last) {
+          __threadfence();
+          for (int g = 0; g < G; ++g) {
+            const int64_t base = ((int64_t)pit.seq * Hq + pit.h * G + g) * max_splits;
+            float mstar = -INFINITY;
+            for (int s = 0; s < ns; ++s) mstar = fmaxf(mstar, __ldcg(part_ml + (base + s) * 2));
+            float l = 0.f, o = 0.f;
+            for (int s = 0; s < ns; ++s) {
+              const float ms = __ldcg(part_ml + (base + s) * 2);
+              const float w = ms == -INFINITY ? 0.f : exp2f(ms - mstar);
+              l += w * __ldcg(part_ml + (base + s) * 2 + 1);
+              o += w * __ldcg(part_o + (base + s) * 128 + tid);
+            }
+            out[(base / max_splits) * 128 + tid] = __float2bfloat16(l > 0.f ? o / l : 0.f);
+          }
+          if (tid == 0) *done = 0;
+        }
+      }
+      named_bar_sync(1, 128);  // lred / last are reused by the next item
+      if (tid == 0) {
+        if (pr < 3) DEC_TRACE(6 + pr);
+        DEC_TRACE(9);
+        DEC_TRACE_VAL(11, (unsigned long long)(pr + 1));
+        mbar_arrive(&misc->ring_empty[pr % kRing]);  // done with item pr
+      }
+      pend = false;
+    };
+    auto to_pending = [&](int r) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        pm[g] = m_run[g];
+        pl[g] = l_part[g];
+        po[g] = o_acc[g];
+      }
+      pit = it;
+      pr = r;
+      pend = true;
+    };
     for (int r = 0; have; ++r) {
       // Q of item r+1 goes into the buffer item r-1 used (its QKs are done):
       // the item is read from the ring after this item's first tile (the
@@ -359,24 +455,12 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       // softmax never waits on it), Q loaded then and stored one tile later
       int q_state = 0;  // 0: item r+1 not read yet, 1: Q loaded, 2: stored / none
       const int ctx = it.ctx;
-      float m_run[8], l_part[8], o_acc[8], alpha0[8], alpha1[8];  // alpha by tile parity
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
         m_run[g] = -INFINITY;
         l_part[g] = 0.f;
         o_acc[g] = 0.f;
       }
-      // O of tile x is folded two tiles later (or at the item's end), so the
-      // softmax never waits on the P.V it has just released:
-      //   o_acc = o_acc * alpha_x + O_x,  alpha_x = exp2(m_{x-1} - m_x)
-      auto fold = [&](int x) {
-        mbar_wait(&misc->o_full[x & 1], (x >> 1) & 1);
-        tc_fence_after();
-        float ov[8];
-        tmem_ld_32x32b_x8(tmem + lane_base + 32 + (x & 1) * 16, ov);
-#pragma unroll
-        for (int g = 0; g < 8; ++g) o_acc[g] = o_acc[g] * ((x & 1) ? alpha1[g] : alpha0[g]) + ov[g];
-      };
       for (int t = 0; t < it.nt; ++t, ++j) {
         const int tile = it.t_beg + t;
         const int valid = min(kTileTok, ctx - tile * kTileTok);
@@ -402,7 +486,11 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         }
         named_bar_sync(1, 128);
         // O of tile j-2 (same TMEM O / P buffers as tile j): fold it first
-        if (t >= 2) fold(j - 2);
+        // (the pending item's second-to-last tile at this item's start)
+        if (t >= 2)
+          fold(j - 2, o_acc);
+        else if (t == 0 && pend && pit.nt >= 2)
+          fold(j - 2, po);
         float p[8];
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
@@ -441,14 +529,19 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           }
         }
         // P^T -> SW128 K-major image in buffer j&1, fp16 (rows 8..15 stay
-        // zero).  PV of tile j-2 (same buffer) is done: it was folded above,
-        // or at the previous item's end.
+        // zero).  PV of tile j-2 (same buffer) is done: it was folded above.
         uint8_t* pbuf = sP + (j & 1) * kPBytes + (tid >> 6) * 2048;
 #pragma unroll
         for (int g = 0; g < 8; ++g)
           *reinterpret_cast<__half*>(pbuf + sw128_offset(g, tid & 63)) = __float2half_rn(p[g]);
         fence_proxy_async_smem();
         mbar_arrive(&misc->p_full[j & 1]);
+        // the previous item's last O, then its epilogue, while P.V of this
+        // tile runs
+        if (t == 0 && pend) {
+          fold(j - 1, po);
+          finalize();
+        }
         if (q_state == 1) {
           store_q(r + 1);
           q_state = 2;
@@ -466,70 +559,13 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           }
         }
       }
-      if (it.nt >= 2) fold(j - 2);
-      fold(j - 1);
-      // l = sum over the 128 token lanes
-#pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        float v = l_part[g];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) misc->lred[warp][g] = v;
+      if (tid == 0) DEC_TRACE_VAL(12, (unsigned long long)j);
+      to_pending(r);
+      if (!nhave) {  // the CTA's last item: no next P to hide the epilogue behind
+        if (it.nt >= 2) fold(j - 2, po);
+        fold(j - 1, po);
+        finalize();
       }
-      named_bar_sync(1, 128);
-      const int ns = nsplit_of[it.seq];
-      for (int g = 0; g < G; ++g) {
-        const float l = misc->lred[0][g] + misc->lred[1][g] + misc->lred[2][g] + misc->lred[3][g];
-        const int64_t hrow = (int64_t)it.seq * Hq + it.h * G + g;
-        if (ns == 1) {  // no merge needed
-          out[hrow * 128 + tid] = __float2bfloat16(l > 0.f ? o_acc[g] / l : 0.f);
-        } else {
-          const int64_t row = hrow * max_splits + it.split;
-          part_o[row * 128 + tid] = o_acc[g];
-          if (tid == 0) {
-            part_ml[row * 2] = m_run[g];
-            part_ml[row * 2 + 1] = l;
-          }
-        }
-      }
-      if (ns > 1 && fuse_merge) {
-        // Split-KV merge, fused: the CTA that finishes the last split of
-        // (sequence, kv head) merges all of them (threadfence-reduction
-        // pattern) -- no combine launch per layer.  It re-arms the counter
-        // for the next layer's launch.  (Chosen for large batches only: the
-        // fence + counter per split item costs more than a combine launch
-        // when the items are short.)
-        __threadfence();
-        named_bar_sync(1, 128);
-        int32_t* done = split_done + it.seq * Hkv + it.h;
-        if (tid == 0) misc->last = atomicAdd(done, 1) == ns - 1;
-        named_bar_sync(1, 128);
-        if (misc->last) {
-          __threadfence();
-          for (int g = 0; g < G; ++g) {
-            const int64_t base = ((int64_t)it.seq * Hq + it.h * G + g) * max_splits;
-            float mstar = -INFINITY;
-            for (int s = 0; s < ns; ++s) mstar = fmaxf(mstar, __ldcg(part_ml + (base + s) * 2));
-            float l = 0.f, o = 0.f;
-            for (int s = 0; s < ns; ++s) {
-              const float ms = __ldcg(part_ml + (base + s) * 2);
-              const float w = ms == -INFINITY ? 0.f : exp2f(ms - mstar);
-              l += w * __ldcg(part_ml + (base + s) * 2 + 1);
-              o += w * __ldcg(part_o + (base + s) * 128 + tid);
-            }
-            out[(base / max_splits) * 128 + tid] = __float2bfloat16(l > 0.f ? o / l : 0.f);
-          }
-          if (tid == 0) *done = 0;
-        }
-      }
-      named_bar_sync(1, 128);  // lred / last are reused by the next item
-      if (tid == 0) {
-        if (r < 3) DEC_TRACE(6 + r);
-        DEC_TRACE(9);
-        DEC_TRACE_VAL(11, (unsigned long long)(r + 1));
-        DEC_TRACE_VAL(12, (unsigned long long)j);
-      }
-      if (tid == 0) mbar_arrive(&misc->ring_empty[r % kRing]);  // done with item r
       it = nxt;  // item r+1, read from the ring during item r
       have = nhave;
     }
