@@ -319,6 +319,7 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
     launches = sum(1 + (hi - lo) * (1 if q.shape[0] * pool.shape.n_kv_heads >= 4 * 148 else 2)
                    for pool, lo, hi, q, *_ in work)
     gbs = algo_bytes / (ms / 1e3) / 1e9
+    stage = decode_stage_measure(work[0], shape, hbm_peak)
     return {"value": round(nres / (ms / 1e3), 1), "unit": "tok/s",
             "tokens_per_step": nres, "ms_per_token_step": round(ms, 4),
             "note": "attention only, one token per resident through 32 layers",
@@ -326,7 +327,53 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
                          "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
                          "traffic": (_traffic("decode_tc_kernel") or {}).get(
                              "dram_bytes_per_launch")},
-            "launches_per_step": launches}
+            "launches_per_step": launches,
+            "stage16": stage}
+
+
+def decode_stage_measure(member, shape, hbm_peak: float, nseq: int = 16):
+    """A pipeline stage's decode: the first `nseq` residents of one member
+    through its stage's layers, replayed as a CUDA graph (as the serving
+    engine replays decode-only stages), device time per layer."""
+    import torch
+    from paper_2412_18169_b200 import runtime
+    pool, lo, hi, q, slots, ctx, mx, out, _ = member
+    q, slots, ctx, out = q[:nseq], slots[:nseq], ctx[:nseq], out[:nseq]
+    Hq = shape.n_q_heads
+    ws = torch.empty(runtime.decode_workspace_bytes(nseq, Hq, 16), dtype=torch.uint8,
+                     device="cuda")
+    st = torch.cuda.Stream()
+    mx = int(ctx.max())
+
+    def step():
+        for l in range(lo, hi):
+            runtime.paged_decode(pool, l, q, slots, ctx, mx, out, ws, 128 ** -0.5,
+                                 max_splits=16, reuse_plan=l > lo, stream=st)
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            step()
+    st.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        step()
+    pool.stream_begin(st)
+    reps = 20
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        g.replay()
+        a.record(st)
+        for _ in range(reps):
+            g.replay()
+        b.record(st)
+    pool.stream_end(st)
+    b.synchronize()
+    us = a.elapsed_time(b) * 1e3 / reps / (hi - lo)
+    per_layer = int(ctx.sum().item()) * shape.kv_bytes_per_token_layer + 2 * nseq * Hq * 256
+    gbs = per_layer / (us / 1e6) / 1e9
+    return {"sequences": nseq, "layers": hi - lo, "us_per_layer": round(us, 2),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak,
+                         "unit": "GB/s", "frac": round(gbs / hbm_peak, 4)},
+            "note": "CUDA-graph replay of one stage's decode (16 layers), device time"}
 
 
 def nvlink_measure(rt, shape, args, pp: int = 2) -> dict:
@@ -395,7 +442,10 @@ def _summary(line: dict) -> dict:
     return {"payload_gbs_same_gpu_proxy": line["value"], "e2e_gbs": line["e2e"]["value"],
             "copy_pages_frac": line["roofline"]["frac"],
             "param_pull_frac": line["roofline_param_pull"]["frac"],
-            "decode_frac": dec.get("frac"), "prefill_frac": pre.get("frac"),
+            "decode_frac": dec.get("frac"),
+            "decode_stage16_frac": (((line.get("paged_decode") or {}).get("stage16") or {})
+                                    .get("roofline") or {}).get("frac"),
+            "prefill_frac": pre.get("frac"),
             "parity": line["parity"]["weights_bit_exact"] and line["parity"]["kv_bit_exact"],
             "ttft_clock": t.get("clock"), "ttft": pol,
             "criterion_4": t.get("criterion_4"),

@@ -334,3 +334,64 @@ def test_block_tokens_128_decode_and_prefill(runtime):
         ma, mr = check_close(op.float().cpu().numpy(), want)
         assert ma <= 2e-2 and mr <= 1e-3, ("prefill", kv_splits, ma, mr)
     pool.close()
+
+
+@pytest.mark.parametrize("devs", [(0, 0), (0, 1)], ids=["same_gpu", "two_gpus"])
+def test_two_runtimes_in_one_process(runtime, devs):
+    """One process driving two Runtimes (DeviceConfig.devices): pools on
+    each, KV pages copied from the first pool into the second (a peer read
+    when they sit on different GPUs), then decode and prefill on the second
+    device -- the shared-memory opt-in of the ~210 KB attention kernels is
+    per device, so the second device's launches must carry their own.
+    The two-GPU case skips on a one-GPU box."""
+    da, db = devs
+    if max(devs) >= torch.cuda.device_count():
+        pytest.skip("needs a second GPU")
+    shape = ModelShape("g4", num_layers=2, hidden=4096, n_q_heads=32, n_kv_heads=8, head_dim=128,
+                       ffn=1024, vocab=1024, block_tokens=64)
+    model = shape.spec()
+    peers_a = [db] if db != da else []
+    peers_b = [da] if db != da else []
+    rt_a = runtime.Runtime(da, peers=peers_a, max_slots=8, max_pages_per_seq=64, slack_pages=64)
+    rt_b = runtime.Runtime(db, peers=peers_b, max_slots=8, max_pages_per_seq=64, slack_pages=64)
+    pa = rt_a.create_pool(0, model, model.param_bytes + 64 * MIB, shape)
+    pb = rt_b.create_pool(1, model, model.param_bytes + 64 * MIB, shape)
+    g = torch.Generator().manual_seed(21)
+    ctx, hkv, hq = 1000, shape.n_kv_heads, shape.n_q_heads
+    npg = (ctx + 63) // 64
+    k = torch.randn((ctx, hkv, 128), generator=g).to(torch.bfloat16)
+    v = torch.randn((ctx, hkv, 128), generator=g).to(torch.bfloat16)
+    with torch.cuda.device(da):
+        assert pa.grow([(2, 0, 1, npg)])
+        n = ctx
+        runtime.kv_append(pa, 0, k.cuda(), v.cuda(), torch.full((n,), 2, dtype=torch.int32, device="cuda"),
+                          torch.arange(n, dtype=torch.int32, device="cuda"))
+        torch.cuda.synchronize()
+    with torch.cuda.device(db):
+        assert pb.grow([(5, 0, 1, npg)])
+        # (src slot, dst slot, layer lo, layer hi, pages per layer, flat lo, flat hi)
+        runtime.copy_pages(pb, pa, [(2, 5, 0, 1, npg, 0, npg)])
+        torch.cuda.synchronize()
+        dev = lambda xs: torch.tensor(xs, dtype=torch.int32, device="cuda")  # noqa: E731
+        q = torch.randn((1, hq, 128), generator=g).to(torch.bfloat16)
+        out = torch.empty((1, hq, 128), dtype=torch.bfloat16, device="cuda")
+        ws = torch.empty(runtime.decode_workspace_bytes(1, hq, 8), dtype=torch.uint8, device="cuda")
+        runtime.paged_decode(pb, 0, q.cuda(), dev([5]), dev([ctx]), ctx, out, ws, 128 ** -0.5,
+                             max_splits=8)
+        c = 200
+        qp = torch.randn((c, hq, 128), generator=g).to(torch.bfloat16)
+        op = torch.empty((c, hq, 128), dtype=torch.bfloat16, device="cuda")
+        runtime.paged_prefill(pb, 0, qp.cuda(), dev([5]), dev([0]), dev([c]), dev([ctx - c]), c, op,
+                              128 ** -0.5, kv_splits=2)
+        torch.cuda.synchronize()
+        assert out.device.index == db
+    want = bf16_to_f32(f32_to_bf16(decode_ref(q[0].float().numpy(), k.float().numpy(),
+                                              v.float().numpy(), 128 ** -0.5)))
+    ma, mr = check_close(out[0].float().cpu().numpy(), want)
+    assert ma <= 2e-2 and mr <= 1e-3, (ma, mr)
+    wantp = bf16_to_f32(f32_to_bf16(prefill_ref(qp.float().numpy(), k.float().numpy(),
+                                                v.float().numpy(), ctx - c, 128 ** -0.5)))
+    pa_, pr_ = check_close(op.float().cpu().numpy(), wantp)
+    assert pa_ <= 2e-2 and pr_ <= 1e-3, (pa_, pr_)
+    pb.close()
+    pa.close()
