@@ -103,7 +103,7 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 }
 // pairs i with i % kEmuEvery == kEmuEvery - 1 use exp2_fma2
 #ifndef KB_PF_EMU_EVERY
-#define KB_PF_EMU_EVERY 6
+#define KB_PF_EMU_EVERY 5
 #endif
 constexpr int kEmuEvery = KB_PF_EMU_EVERY;
 // (Issuing the QK of keys 64-127 early -- those S columns never hold P --
@@ -542,12 +542,27 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         store_half(H0{});  // P again with the new reference
         rs = take_rs();
       }
+#ifdef KB_PF_ST_REORDER
+      // keys 64-127 computed before P of keys 0-63 is published: the
+      // tcgen05.wait::st of the first half's stores then finds them done
+      uint32_t w_hi[32];
+      if (full_tile) p_half(std::false_type{}, H1{}, w_hi);
+      else p_half(std::true_type{}, H1{}, w_hi);
+      const float rs_hi = take_rs();
+      l_run += rs;
+      publish(&misc->p_lo[t]);
+      rs = rs_hi;
+      const bool ovf = fast && __any_sync(0xffffffffu, !(rs <= kSumBound));
+      if (!ovf) tmem_st_32x32b_x32(s_addr + 32, w_hi);
+      if (ovf) {
+#else
       l_run += rs;
       publish(&misc->p_lo[t]);
       // keys 64-127 (the P.V of keys 0-63 may already be running)
       store_half(H1{});
       rs = take_rs();
       if (fast && __any_sync(0xffffffffu, !(rs <= kSumBound))) {
+#endif
         // rare: O already holds this tile's first-half P.V under the old
         // reference -- let it land, then rescale everything so far
         const float xmax = half_xmax(H1{});
