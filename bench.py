@@ -132,6 +132,30 @@ def dist_env():
     return ws, rank, local
 
 
+def arm_config(kv_gib: float, residents: int, ws: int) -> dict:
+    """The workload both arms report (the reference arm times a bounded
+    sample of it, described in its cpu_baseline.sample)."""
+    return {"workload": "llama3_8b bf16, 2 replicas per GPU -> 1 PP-2 group; "
+                        "ShareGPT-shaped residents at 90% KV; drop+exchange+"
+                        "restore+consolidate per step",
+            "model": "llama3_8b", "replicas_per_gpu": 2,
+            "kv_budget_gib_per_replica": kv_gib,
+            "residents": residents, "parallelism": f"pp2 x{ws} (replica pairs)",
+            "l2": "inputs larger than L2 (GB-scale moves per step)"}
+
+
+def host_residents(kv_gib: float) -> dict:
+    """The GPU arm's resident list (cycle.resident_tokens over two host
+    instances with the same KV budget): {rid: tokens}."""
+    from paper_2412_18169_b200 import memory
+    from paper_2412_18169_b200.core import SHAPES
+    from paper_2412_18169_b200.cycle import resident_tokens
+    model = SHAPES["llama3_8b"].spec()
+    caps = {i: memory.build_instance(i, model, model.param_bytes + int(kv_gib * (1 << 30)),
+                                     900_000_000_000).kv.capacity_tokens for i in range(2)}
+    return resident_tokens(caps)[0]
+
+
 def run_reference(args) -> None:
     """CPU arm: the reference's path executed by the oracle port on host cores."""
     ws, rank, _ = dist_env()
@@ -139,11 +163,10 @@ def run_reference(args) -> None:
         return
     from oracle.cpu_cycle import CpuCycle
     from paper_2412_18169_b200.core import SHAPES
-    from paper_2412_18169_b200.traceio import synth_burst
     shape = SHAPES["llama3_8b"]
     model = shape.spec()
-    res = [r.input_len for r in synth_burst(10_000.0, 4.0, 16.0, 0.0, 10_000.0, 1660, 373,
-                                            seed=3)[:32]]
+    full = host_residents(args.kv_gib)
+    res = [full[r] for r in sorted(full)[:32]]  # the sample: the first 32 residents
     cyc = CpuCycle(model.bytes_per_layer, shape.page_bytes, shape.block_tokens, 2,
                    model.num_layers, res, model.kv_bytes_per_token)
     for _ in range(max(1, args.warmup)):
@@ -155,14 +178,14 @@ def run_reference(args) -> None:
         moved += r["bytes"]
     dt = time.perf_counter() - t0
     gbs = moved / dt / 1e9
-    sample = (f"2 of 32 Llama-3-8B layer slabs + {len(res)} ShareGPT residents' pages per step, "
-              f"control plane at full size, numpy copies on {cyc.threads} threads")
+    sample = (f"2 of 32 Llama-3-8B layer slabs + the first {len(res)} of the {len(full)} "
+              f"residents' pages per step, control plane at full size, numpy copies on "
+              f"{cyc.threads} threads")
     line = {"metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "impl": "reference",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": "llama3_8b x2 replicas overload cycle (CPU sample)",
-                       "parallelism": "replicas"},
+            "config": arm_config(args.kv_gib, len(full), ws),
             "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": cyc.threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -650,13 +673,7 @@ def main():
                             "device-timed step); at N=1 a SAME-GPU HBM PROXY -- both replicas "
                             "share one B200, so no byte crosses NVLink; cross-GPU numbers are "
                             "nvlink_* (N>1)"),
-            "config": {"workload": "llama3_8b bf16, 2 replicas per GPU -> 1 PP-2 group; "
-                                   "ShareGPT-shaped residents at 90% KV; drop+exchange+"
-                                   "restore+consolidate per step",
-                       "model": "llama3_8b", "replicas_per_gpu": 2,
-                       "kv_budget_gib_per_replica": args.kv_gib,
-                       "residents": len(cyc.tokens), "parallelism": f"pp2 x{ws} (replica pairs)",
-                       "l2": "inputs larger than L2 (GB-scale moves per step)"},
+            "config": arm_config(args.kv_gib, len(cyc.tokens), ws),
             "breakdown": {"payload_bytes_per_step": r0.payload_bytes,
                           "payload": {"kv_exchange": r0.payload_kv_exchange,
                                       "param_restore": r0.payload_param,

@@ -84,6 +84,35 @@ class CycleReport:
         return self.bytes_kv_exchange + self.bytes_param + self.bytes_kv_consolidate
 
 
+def resident_tokens(capacity_tokens: dict, fill: float = 0.9, seed: int = 3,
+                    input_mean: int = 1660):
+    """The bench's residents: a ShareGPT-shaped trace (traceio.synth_burst)
+    dealt round-robin to the replicas until each is `fill` full (host-only;
+    the CPU reference arm samples the same list).  Returns ({rid: tokens},
+    {rid: home replica})."""
+    trace = synth_burst(10_000.0, 4.0, 16.0, 0.0, 10_000.0, input_mean, 373, seed=seed)
+    tokens: dict[int, int] = {}
+    home: dict[int, int] = {}
+    used = {i: 0 for i in capacity_tokens}
+    full = {i: False for i in capacity_tokens}
+    ids = sorted(capacity_tokens)
+    rid = 0
+    for rec in trace:
+        if all(full.values()):
+            break
+        iid = ids[rid % len(ids)]
+        rid += 1
+        if full[iid]:
+            continue
+        if used[iid] + rec.input_len > fill * capacity_tokens[iid]:
+            full[iid] = True
+            continue
+        tokens[rid] = rec.input_len
+        home[rid] = iid
+        used[iid] += rec.input_len
+    return tokens, home
+
+
 class OverloadCycle:
     """Replicas (one per entry of `runtimes`; several may share a GPU), each
     filled to `fill` of its KV budget with ShareGPT-shaped residents; every
@@ -107,24 +136,10 @@ class OverloadCycle:
         self.pools = {i: inst.pool for i, inst in self.instances.items()}
         self.slots = {i: SlotTable(runtimes[i].max_slots) for i in self.instances}
         self.te = TransferEngine(self.pools, self.slots, timing=True)
-        trace = synth_burst(10_000.0, 4.0, 16.0, 0.0, 10_000.0, input_mean, 373, seed=seed)
-        self.tokens: dict[int, int] = {}
-        self.home: dict[int, int] = {}
-        full = {i: False for i in self.instances}
-        rid = 0
-        for rec in trace:
-            if all(full.values()):
-                break
-            iid = rid % len(self.instances)
-            rid += 1
-            if full[iid]:
-                continue
-            inst = self.instances[iid]
-            if inst.kv.used_tokens + rec.input_len > fill * inst.kv.capacity_tokens:
-                full[iid] = True
-                continue
-            self.tokens[rid] = rec.input_len
-            self.home[rid] = iid
+        self.tokens, self.home = resident_tokens(
+            {i: inst.kv.capacity_tokens for i, inst in self.instances.items()}, fill, seed,
+            input_mean)
+        for rid in sorted(self.tokens):
             self._admit(rid)
         self.transient = set(sorted(self.tokens)[1::2])
         for iid, pool in self.pools.items():
