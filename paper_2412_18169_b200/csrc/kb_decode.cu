@@ -50,8 +50,12 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml,
                                       const int32_t* __restrict__ nsplit_of,
                                       __nv_bfloat16* __restrict__ out, int Hq, int max_splits) {
-  sm100::pdl_wait();  // the attention kernel's partials
+  // the next launch (the following layer's attention) may start its
+  // prologue and its plan-safe early loads at once: they touch nothing this
+  // grid or the attention grid before it writes, and its own
+  // griddepcontrol.wait orders the rest after this grid
   sm100::pdl_launch_dependents();
+  sm100::pdl_wait();  // the attention kernel's partials
   const int sh = blockIdx.x;  // seq * Hq + head
   const int seq = sh / Hq;
   const int ns = nsplit_of[seq];
