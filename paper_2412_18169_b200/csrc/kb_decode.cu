@@ -73,6 +73,40 @@ __global__ void decode_combine_kernel(const float* __restrict__ part_o,
   out[(int64_t)sh * 128 + threadIdx.x] = __float2bfloat16(l > 0.f ? o / l : 0.f);
 }
 
+// KB_DEC_REFINE: hand the item budget T leaves unused to the sequences with
+// the longest pieces (one more split each).  Measured slower on B200 (r2y:
+// 16 sequences 25.9 vs 25.6 us per layer, 4 sequences up to +2.5 us over
+// three context draws) -- off; kept for A/B.
+#ifndef KB_DEC_REFINE
+#define KB_DEC_REFINE 0
+#endif
+
+// Block-wide inclusive scan (1024 threads); warp_sum is 32 ints of smem.
+__device__ __forceinline__ int block_incl_scan(int v, int* warp_sum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = warp_sum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_sum[lane] = t;
+  }
+  __syncthreads();
+  const int r = (w ? warp_sum[w - 1] : 0) + x;
+  __syncthreads();  // warp_sum is reused by the next call
+  return r;
+}
+
 // Work items: sequence i is cut into s_i = clamp(ceil(tiles_i / T), 1,
 // max_splits) splits per kv head, T chosen so the items spread ~kItemsPerCta
 // per persistent CTA; items are bucket-sorted longest first.  Sequences with
@@ -135,11 +169,76 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
     int s = (tiles + T - 1) / T;
     return s < 1 ? 1 : (s > max_splits ? max_splits : s);
   };
+  // split counts per sequence (no context: no item, 0 splits -- the
+  // attention kernel writes a zero row)
   for (int i = tid; i < nseq; i += blockDim.x) {
     const int tiles = (ctx[i] + kTileTok - 1) / kTileTok;
-    const int s = splits_of(tiles);
-    // no context: no item; the attention kernel writes a zero row (0 splits)
-    nsplit_of[i] = tiles == 0 ? 0 : s;
+    nsplit_of[i] = tiles == 0 ? 0 : splits_of(tiles);
+  }
+  __syncthreads();
+  if (KB_DEC_REFINE) {
+    // The item budget T leaves under grid * kItemsPerCta (the counts move in
+    // steps of Hkv per sequence, so a T one smaller overshoots) goes to the
+    // sequences whose pieces are longest: one more split each, longest
+    // first, ties by index -- shorter last items, a tighter LPT tail.
+    __shared__ unsigned long long cnt_all;
+    __shared__ int thr, take, carry;
+    __shared__ int scan_ws[32];
+    if (tid == 0) {
+      cnt_all = 0;
+      carry = 0;
+    }
+    __syncthreads();
+    unsigned long long c = 0;
+    for (int i = tid; i < nseq; i += blockDim.x) {
+      const int tiles = (ctx[i] + kTileTok - 1) / kTileTok, sp = nsplit_of[i];
+      c += sp;
+      if (tiles >= 2 && sp < max_splits && sp < tiles)
+        atomicAdd(&hist[min((tiles + sp - 1) / sp, kLenBuckets - 1)], 1);
+    }
+    atomicAdd(&cnt_all, c);
+    __syncthreads();
+    if (tid == 0) {
+      const long long target = (long long)grid_ctas * kItemsPerCta;
+      const long long cnt = (long long)cnt_all * Hkv;
+      const long long extra = cnt <= target ? (target - cnt) / Hkv : 0;
+      thr = 1 << 30;
+      take = 0;
+      long long acc = 0;
+      for (int L = kLenBuckets - 1; L >= 2 && extra > 0; --L) {
+        if (acc + hist[L] >= extra) {
+          thr = L;
+          take = (int)(extra - acc);
+          break;
+        }
+        acc += hist[L];
+      }
+      if (extra > 0 && thr == (1 << 30)) thr = 1;  // every eligible sequence
+    }
+    __syncthreads();
+    hist[tid] = 0;  // re-armed for the item histogram below
+    for (int base = 0; base < nseq; base += blockDim.x) {
+      const int i = base + tid;
+      int L = 0, sp = 0;
+      bool elig = false;
+      if (i < nseq) {
+        const int tiles = (ctx[i] + kTileTok - 1) / kTileTok;
+        sp = nsplit_of[i];
+        elig = tiles >= 2 && sp < max_splits && sp < tiles;
+        L = elig ? (tiles + sp - 1) / sp : 0;
+        L = min(L, kLenBuckets - 1);
+      }
+      const int f = elig && L == thr;
+      const int incl = block_incl_scan(f, scan_ws);
+      if (elig && (L > thr || (f && carry + incl - 1 < take))) nsplit_of[i] = sp + 1;
+      __syncthreads();
+      if (tid == kPlanThreads - 1) carry += incl;
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < nseq; i += blockDim.x) {
+    const int tiles = (ctx[i] + kTileTok - 1) / kTileTok;
+    const int s = nsplit_of[i];
     if (tiles == 0) continue;
     for (int k = 0; k < s; ++k) {
       int beg, len;
@@ -182,7 +281,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
   for (int i = tid; i < nseq; i += blockDim.x) {
     const int tiles = (ctx[i] + kTileTok - 1) / kTileTok;
     if (tiles == 0) continue;
-    const int s = splits_of(tiles);
+    const int s = nsplit_of[i];
     for (int k = 0; k < s; ++k) {
       int beg, len;
       piece(tiles, s, T, k, beg, len);

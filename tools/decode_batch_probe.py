@@ -20,7 +20,7 @@ shape = ModelShape("g4", num_layers=2, hidden=4096, n_q_heads=32, n_kv_heads=8, 
 rt = runtime.Runtime(0, max_slots=256, max_pages_per_seq=128, slack_pages=256)
 model = shape.spec()
 pool = rt.create_pool(0, model, model.param_bytes + (12 << 30), shape)
-rng = np.random.default_rng(5)
+rng = np.random.default_rng(int(os.environ.get("KB_PROBE_SEED", "5")))
 MS = int(os.environ.get("KB_PROBE_MAX_SPLITS", "16"))
 APPEND = os.environ.get("KB_PROBE_APPEND", "0") == "1"
 # KB_PROBE_MERGE=1: force the combine launch, 0: force the in-kernel merge
