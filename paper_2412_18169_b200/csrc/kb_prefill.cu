@@ -357,6 +357,11 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       const long long tw0 = clock64();
 #endif
       mbar_wait(&misc->s_full[t], j & 1);
+      // observe the previous tile's pv_lo phase (complete: its P.V ran before
+      // this QK on the in-order tensor pipe).  Only the rare rescale path
+      // needs the barrier, but every phase is waited so that no arrival
+      // lands on a completed, unobserved phase (compute-sanitizer synccheck)
+      if (j > 0) mbar_wait(&misc->pv_lo[t], (j - 1) & 1);
 #ifdef KB_PF_TIMING
       const long long tw1 = clock64();
       t_wait += tw1 - tw0;
@@ -603,6 +608,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 #endif
     // epilogue: O_t / l -> bf16 rows, or the split's partial (O, m, l)
     mbar_wait(&misc->o_done[t], 0);
+    mbar_wait(&misc->pv_lo[t], (nt - 1) & 1);  // the last tile's phase, for synccheck
     tc_fence_after();
     if (splits > 1) {
       const int64_t u = ((int64_t)blockIdx.x * Hq + hq) * splits + split;
