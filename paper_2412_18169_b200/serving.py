@@ -29,6 +29,7 @@ pool: kb_copy_pages).
 
 from __future__ import annotations
 
+import collections
 import gc
 
 import math
@@ -110,7 +111,12 @@ class StageRunner:
     # are copied into the graph's static buffers before each replay.  Block
     # tables are read on device at replay time, so pages grown since capture
     # are seen.  Removes the per-launch host overhead from measured stage time.
+    # Graphs of exact batch sizes are kept least-recently-used, at most
+    # max_graphs of them (each holds a private pool for its intermediates,
+    # outside the KV budget); the padded graphs of the wall-clock engine are
+    # pinned.
     graphs_enabled = True
+    max_graphs = 48
 
     def prepare_decode_graph(self, lo: int, hi: int, x, batch: dict) -> None:
         """Capture the (layers, batch size) graph if it does not exist yet.
@@ -119,9 +125,14 @@ class StageRunner:
         torch = self.torch
         key = (lo, hi, batch["n"])
         if not hasattr(self, "_graphs"):
-            self._graphs = {}
+            self._graphs = collections.OrderedDict()
+            self._pinned = set()
         if key in self._graphs:
+            self._graphs.move_to_end(key)
             return
+        while len(self._graphs) - len(self._pinned) >= self.max_graphs:
+            old = next(k for k in self._graphs if k not in self._pinned)
+            del self._graphs[old]  # its graph and private memory pool go with it
         self.run(lo, hi, x.clone(), batch)  # warm-up: lazy attributes, cuBLAS handles
         st = {"x": x.clone(), "slots": batch["slots"].clone(), "pos": batch["pos"].clone(),
               "d_slots": batch["d_slots"].clone(), "d_ctx": batch["d_ctx"].clone(),
@@ -171,6 +182,7 @@ class StageRunner:
              "d_rows": torch.arange(n_pad, dtype=torch.int64, device=f"cuda:{dev}")}
         x = torch.zeros((n_pad, self.shape.hidden), dtype=torch.bfloat16, device=f"cuda:{dev}")
         self.prepare_decode_graph(lo, hi, x, b)
+        self._pinned.add((lo, hi, n_pad))
 
     def run_padded_decode(self, lo: int, hi: int, x, batch: dict, n_pad: int):
         """Replay the (lo, hi, n_pad) graph for the first batch["n"] rows of

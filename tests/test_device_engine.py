@@ -92,3 +92,27 @@ def test_device_engine_overload_cycle(built, policy, clock):
     assert eng.stage_samples and all(s[-1] >= 1 for s in eng.stage_samples)
     for pool in eng.pools.values():
         pool.close()
+
+
+def test_decode_graph_cache_is_bounded(built):
+    """Exact-size decode graphs are kept least-recently-used (each holds a
+    private memory pool outside the KV budget): a run with many distinct
+    decode batch sizes never holds more than max_graphs of them."""
+    from paper_2412_18169_b200.serving import DeviceEngine, device_config
+    shape = SHAPES["tiny"]
+    cfg = device_config(shape, instances=2, kv_bytes=4 << 20)
+    cfg.policy.kind = "recompute"
+    trace = [TraceRecord(3000 * i, 60 + 7 * i, 40 + 13 * (i % 5)) for i in range(12)]
+    eng = DeviceEngine(cfg, trace)
+    for r in eng.runners.values():
+        r.max_graphs = 3
+    res = eng.run()
+    assert kinds(res.log_lines).get("FINISH", 0) == len(trace)
+    sizes = set()
+    for r in eng.runners.values():
+        g = getattr(r, "_graphs", {})
+        assert len(g) - len(getattr(r, "_pinned", ())) <= 3
+        sizes |= {k[2] for k in g}
+    assert sizes  # graphs were used
+    for pool in eng.pools.values():
+        pool.close()
