@@ -599,6 +599,7 @@ def main():
     cyc.auto_refill = False
     e2e_s = 0.0
     e2e_steps = []
+    e2e_dev = []  # the same steps' device span (first to last event of the cycle)
     gc.collect()
     gc.disable()
     e_payload = 0
@@ -608,11 +609,16 @@ def main():
         torch.cuda.synchronize()
         h0 = runtime.H2D_BYTES[0]
         t0 = time.perf_counter()
-        r = cyc.step(burst=burst)
-        res.copy_(cyc.home_first_pages(), non_blocking=True)
+        # the result read-back is queued right behind the cycle's last device
+        # operation; the step's host-side accounting overlaps the device tail
+        # (light: no per-launch kernel timing -- that is the device-timed
+        # loop's instrumentation, not part of a cycle)
+        r = cyc.step(burst=burst, light=True,
+                     on_enqueued=lambda: res.copy_(cyc.home_first_pages(), non_blocking=True))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i >= args.warmup:
+            e2e_dev.append(round(r.ms["total"], 2))
             e2e_steps.append(round(dt * 1e3, 2))
             e2e_s += dt
             e_payload += r.payload_bytes
@@ -719,6 +725,7 @@ def main():
                     "h2d_bytes_per_step": int(sum(h2d) / max(1, len(h2d))),
                     "d2h_bytes_per_step": res.numel() * 4 + 16 * 2,
                     "ms_per_step": e2e_steps,
+                    "device_span_ms_per_step": e2e_dev,
                     "input": "queued burst per replica -> plan_drop -> C-ABI descriptors "
                              "(grows, page moves, releases, slab ranges)"},
             "gpu_launches": launches,
