@@ -395,3 +395,54 @@ def test_two_runtimes_in_one_process(runtime, devs):
     assert pa_ <= 2e-2 and pr_ <= 1e-3, (pa_, pr_)
     pb.close()
     pa.close()
+
+
+@pytest.mark.parametrize("case", ["one_long_sequence", "whole_pair_items", "mixed"])
+@pytest.mark.parametrize("combine", [True, False])
+def test_decode_plan_extremes(runtime, case, combine):
+    """Decode plans at their extremes, each layer run three times on one
+    plan (the item counter and split counters must re-arm): one 20k-token
+    sequence cut into 32+ KV splits per kv head (max_splits 64), 96
+    sequences whose items are whole 8-tile pairs (one split each: more
+    items than 2 per CTA), and a ragged mix from 5 to 9,000 tokens; with
+    the combine launch and with the in-kernel merge."""
+    shape = G4
+    model = shape.spec()
+    rng = random.Random(11)
+    if case == "one_long_sequence":
+        ctxs, max_splits = [20000], 64
+    elif case == "whole_pair_items":
+        ctxs, max_splits = [1000 + rng.randrange(-20, 20) for _ in range(96)], 16
+    else:
+        ctxs, max_splits = [rng.choice([5, 300, 1200, 4000, 9000]) for _ in range(24)], 16
+    nseq = len(ctxs)
+    rt = runtime.Runtime(0, max_slots=128, max_pages_per_seq=512, slack_pages=64)
+    pool = rt.create_pool(0, model, model.param_bytes + 2048 * MIB, shape)
+    hkv, hq, B = shape.n_kv_heads, shape.n_q_heads, shape.block_tokens
+    g = torch.Generator().manual_seed(17)
+    kv = {}
+    for i, c in enumerate(ctxs):
+        assert pool.grow([(i, 0, 1, (c + B - 1) // B)])
+        k = torch.randn((c, hkv, 128), generator=g).to(torch.bfloat16)
+        v = torch.randn((c, hkv, 128), generator=g).to(torch.bfloat16)
+        _append(runtime, pool, 0, k, v, i, 0)
+        kv[i] = (k.float().numpy(), v.float().numpy())
+    torch.cuda.synchronize()
+    q = torch.randn((nseq, hq, 128), generator=g).to(torch.bfloat16)
+    slots = torch.arange(nseq, dtype=torch.int32, device="cuda")
+    lens = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    ws = torch.empty(runtime.decode_workspace_bytes(nseq, hq, max_splits), dtype=torch.uint8,
+                     device="cuda")
+    scale = 128 ** -0.5
+    want = [bf16_to_f32(f32_to_bf16(decode_ref(q[i].float().numpy(), *kv[i], scale)))
+            for i in range(nseq)]
+    for n in range(3):
+        out = torch.zeros((nseq, hq, 128), dtype=torch.bfloat16, device="cuda")
+        runtime.paged_decode(pool, 0, q.cuda(), slots, lens, max(ctxs), out, ws, scale,
+                             max_splits=max_splits, reuse_plan=n > 0, combine=combine)
+        torch.cuda.synchronize()
+        got = out.float().cpu().numpy()
+        for i in range(nseq):
+            ma, mr = check_close(got[i], want[i])
+            assert ma <= 2e-2 and mr <= 1e-3, (case, combine, n, ctxs[i], ma, mr)
+    pool.close()
