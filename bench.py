@@ -354,6 +354,64 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
             "stage16": stage}
 
 
+def decode_batch_sweep(rt, hbm_peak: float, sizes=(4, 16, 32, 64, 147), seed: int = 5) -> dict:
+    """tools/decode_batch_probe.py's measurement inside the bench line:
+    Llama-3-8B heads, ShareGPT-like contexts (lognormal around 1,500
+    tokens), 16 layer launches per CUDA-graph replay over one plan, device
+    time per layer at each batch size."""
+    import numpy as np
+    import torch
+    from paper_2412_18169_b200 import runtime
+    from paper_2412_18169_b200.core import ModelShape
+    shape = ModelShape("g4", num_layers=2, hidden=4096, n_q_heads=32, n_kv_heads=8,
+                       head_dim=128, ffn=1024, vocab=1024, block_tokens=64)
+    rt2 = runtime.Runtime(rt.device, max_slots=256, max_pages_per_seq=128, slack_pages=256)
+    model = shape.spec()
+    pool = rt2.create_pool(0, model, model.param_bytes + (12 << 30), shape)
+    rng = np.random.default_rng(seed)
+    out = {}
+    for nseq in sizes:
+        ctx = np.clip(rng.lognormal(np.log(1500), 0.6, nseq), 16, 8000).astype(int)
+        for s_, c in enumerate(ctx):
+            pool.release([s_], 0, 2)
+            assert pool.grow([(s_, 0, 2, (int(c) + 63) // 64)])
+        q = torch.randn((nseq, 32, 128), device="cuda").to(torch.bfloat16)
+        o = torch.empty_like(q)
+        sl = torch.arange(nseq, dtype=torch.int32, device="cuda")
+        cl = torch.tensor(ctx, dtype=torch.int32, device="cuda")
+        ws = torch.empty(runtime.decode_workspace_bytes(nseq, 32, 16), dtype=torch.uint8,
+                         device="cuda")
+        mx = int(ctx.max())
+
+        def step():
+            for i in range(16):
+                runtime.paged_decode(pool, i % 2, q, sl, cl, mx, o, ws, 128 ** -0.5,
+                                     max_splits=16, reuse_plan=i > 0)
+        for _ in range(5):
+            step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(20):
+            g.replay()
+        b.record()
+        b.synchronize()
+        us = a.elapsed_time(b) / 20 / 16 * 1000
+        algo = int(ctx.sum()) * 2 * 8 * 128 * 2 + 2 * nseq * 32 * 128 * 2
+        gbs = algo / us / 1e3
+        out[str(nseq)] = {"us_per_layer": round(us, 2), "hbm_gbs": round(gbs, 1),
+                          "frac": round(gbs / hbm_peak, 4)}
+    pool.close()
+    return {"seed": seed, "sizes": out,
+            "note": "tools/decode_batch_probe.py in-line: 16 layer launches per graph replay "
+                    "over one plan, two alternating layers' pools"}
+
+
 def decode_stage_measure(member, shape, hbm_peak: float, nseq: int = 16):
     """A pipeline stage's decode: the first `nseq` residents of one member
     through its stage's layers, replayed as a CUDA graph (as the serving
@@ -468,6 +526,9 @@ def _summary(line: dict) -> dict:
             "decode_frac": dec.get("frac"),
             "decode_stage16_frac": (((line.get("paged_decode") or {}).get("stage16") or {})
                                     .get("roofline") or {}).get("frac"),
+            "decode_sweep_frac": {k: v["frac"] for k, v in
+                                  (((line.get("paged_decode") or {}).get("batch_sweep") or {})
+                                   .get("sizes") or {}).items()},
             "prefill_frac": pre.get("frac"),
             "parity": line["parity"]["weights_bit_exact"] and line["parity"]["kv_bit_exact"],
             "ttft_clock": t.get("clock"), "ttft": pol,
@@ -630,6 +691,7 @@ def main():
     cyc.close()
     _, tensor_peak, _ = load_peaks()
     prefill = prefill_measure(rt, tensor_peak or 1590.0)
+    dec["batch_sweep"] = decode_batch_sweep(rt, hbm_peak)
 
     sweep = copy_sweep(rt) if ws == 1 else None
     # P99 TTFT: the reference's scheduler on real pools, KunServe vs the
