@@ -13,11 +13,17 @@
 // S and O live in TMEM (double-buffered); the online softmax runs on 4
 // warps, one token (for S) and one head_dim lane (for O) per thread.
 //
-// Scheduling: a one-CTA plan kernel splits long sequences so every work
-// item has at most T tiles (T balances total work over the persistent grid)
-// and orders items longest first; each CTA strides through the item list
-// and its TMA -> MMA -> softmax pipeline runs continuously across items, so
-// HBM streaming never drains between sequences.
+// Scheduling: a one-CTA plan kernel (kb_decode.cu) splits long sequences so
+// every work item has at most T tiles -- T balancing the work over two items
+// per persistent CTA -- and orders items longest first.  CTA b starts with
+// item b, then fetches the next index from a per-layer counter (greedy
+// longest-processing-time); the producer copies each item into a
+// shared-memory ring for the MMA and softmax warps.  The TMA -> MMA ->
+// softmax pipeline runs continuously across items (the next item's Q is
+// staged one tile into the current one, and an item's epilogue runs after
+// the next item's first P is out), so HBM streaming never drains between
+// sequences.  With a reused plan the first item's loads start before
+// griddepcontrol.wait.
 //
 // Warp roles (192 threads): 0-3 softmax / epilogue, 4 TMA producer,
 // 5 MMA issuer + TMEM owner.
@@ -40,7 +46,7 @@ constexpr int kPBytes = 4096;            // 16 rows x 128 tok bf16, SW128 K-majo
 constexpr int kDecMiscBytes = 2048;
 constexpr int kDecSmem = kDecStages * kStageBytes + 2 * kQBytes + 2 * kPBytes + kDecMiscBytes + 1024;
 constexpr uint32_t kDecTmemCols = 64;    // S0 S1 O0 O1, 16 columns each
-constexpr int kRing = 16;                // dynamically fetched work items in flight per CTA
+constexpr int kRing = 16;                // work items published ahead per CTA
 
 // one KV split of a (sequence, kv head) pair: tiles [t_beg, t_beg + nt);
 // the slot and context length ride along (one dependent load less before
