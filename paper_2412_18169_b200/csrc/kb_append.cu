@@ -27,8 +27,9 @@ namespace kb {
 // A row whose max is a normal fp16 keeps every element within 2^-11 of M
 // (subnormal elements err by <= 2^-25 <= 2^-11 M), the same bound the normal
 // range gives -- so small entries next to normal ones are fine.  The append
-// kernel ORs the flags into the pool's sticky status word (pinned host
-// memory), which kb_pool_kv_status reports and the host raises on.
+// kernel sets the flags' sticky words (pinned, mapped host memory; one word
+// per flag, plain stores), which kb_pool_kv_status reports and the host
+// raises on.
 __device__ __forceinline__ int4 bf16x8_to_f16x8(int4 v) {
   uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
 #pragma unroll
@@ -82,7 +83,14 @@ __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __rest
   const uint32_t bad = !which ? 0u
                        : (m >= 0x4780u ? KB_KV_V_OVERFLOW : 0u) |
                              (m > 0u && m < 0x3880u ? KB_KV_V_UNDERFLOW : 0u);
-  if (lane == 16 && bad) atomicOr_system(status, bad);  // rare: one write per offending row
+  // rare: one store per offending row, one word per flag -- plain stores of
+  // the same value (no read-modify-write: atomics on pinned host memory are
+  // not native over PCIe)
+  if (lane == 16 && bad) {
+    volatile uint32_t* st = status;
+    if (bad & KB_KV_V_OVERFLOW) st[0] = 1u;
+    if (bad & KB_KV_V_UNDERFLOW) st[1] = 1u;
+  }
 }
 
 }  // namespace kb
@@ -115,7 +123,10 @@ extern "C" int kb_pool_kv_status(kb_pool* p, uint32_t* flags, int32_t clear) {
   if (!p || !flags) return fail(KB_EINVAL, "null argument");
   if (p->view) return refuse_view();
   volatile uint32_t* h = p->h_status;
-  *flags = *h;
-  if (clear) *h = 0;
+  *flags = (h[0] ? KB_KV_V_OVERFLOW : 0u) | (h[1] ? KB_KV_V_UNDERFLOW : 0u);
+  if (clear) {
+    h[0] = 0;
+    h[1] = 0;
+  }
   return KB_OK;
 }

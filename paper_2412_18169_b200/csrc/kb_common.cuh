@@ -121,8 +121,9 @@ struct kb_pool {
   void* d_scratch = nullptr;
   int64_t scratch_bytes = 0;
   int32_t* h_pinned = nullptr;  // small pinned readback buffer
-  // sticky KV status (KB_KV_V_* bits), pinned + mapped: appends OR into it
-  // from the device, the host reads it without a copy (kb_pool_kv_status)
+  // sticky KV status, pinned + mapped: word 0 = a V value overflowed fp16,
+  // word 1 = a V row underflowed; appends set them from the device with
+  // plain stores, the host reads them without a copy (kb_pool_kv_status)
   uint32_t* h_status = nullptr;
   uint32_t* d_status = nullptr;
   cudaStream_t own_stream = nullptr;

@@ -617,7 +617,8 @@ extern "C" int kb_pool_create(int32_t device, const kb_model_desc* model, int64_
   if (cudaHostAlloc(&p->h_status, 64, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->d_status), p->h_status, 0) != cudaSuccess)
     return bail(fail(KB_ECUDA, "cudaHostAlloc(status) failed"));
-  *p->h_status = 0;
+  p->h_status[0] = 0;  // KB_KV_V_OVERFLOW seen
+  p->h_status[1] = 0;  // KB_KV_V_UNDERFLOW seen
   if (cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(KB_ECUDA, "cudaStreamCreate failed"));
   if (cudaEventCreateWithFlags(&p->counts_ev, cudaEventDisableTiming) != cudaSuccess ||
