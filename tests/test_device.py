@@ -325,6 +325,9 @@ def test_baseline_moves_through_the_transfer_engine(rt):
     pages = [a.block_table(sa, l) for l in range(2)]
     want = torch.randint(0, 256, (10, a.page_bytes), dtype=torch.uint8, device="cuda")
     kv_a[torch.tensor(pages[0] + pages[1], device="cuda")] = want
+    # the transfer engine copies on its own streams: the bytes must have landed
+    # (the engines launch transfers only after observing the writers' events)
+    torch.cuda.synchronize()
     nbytes = tokens * model.kv_bytes_per_token
     out = TransferTask(1, TaskKind.KVCACHE_CHUNK, 0, HOST, nbytes, rid=rid)
     te.register_request_move(out, (0, 2), tokens)
