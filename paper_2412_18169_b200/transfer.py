@@ -100,6 +100,14 @@ class TransferEngine:
     pools: iid -> DevicePool; slots: iid -> SlotTable; host_replica: optional
     pinned host tensor holding one full parameter copy (layer l at
     l * bytes_per_layer) for HOST-sourced restores.
+
+    Ordering contract: copies run on the engine's own streams (bulk, urgent,
+    meta) and are ordered after the pools' page-table operations
+    (kb::pool_enter), not after arbitrary work on other streams -- the bytes
+    a task moves must have landed before it is submitted (the engines submit
+    only after observing the writers' completion events; a caller that just
+    wrote pages on its own stream synchronizes first).  Waiting on the
+    caller's stream here would serialize KV exchange behind serving compute.
     """
 
     def __init__(self, pools: dict, slots: dict, host_replica=None, timing: bool = False):
