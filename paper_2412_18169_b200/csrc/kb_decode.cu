@@ -21,6 +21,14 @@ constexpr int kLenBuckets = 1024;
 #define KB_DEC_ITEMS_PER_CTA 2  // swept 1-8 on B200 with dynamic fetching: 1-2 best
 #endif
 constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per persistent CTA
+// ...except when the batch has 1.5-2.4 (sequence, kv head) pairs per CTA:
+// two rounds then leave the pairs nearly unsplit and their lognormal lengths
+// unbalanced; three items per CTA split the long ones (B200 sweep over four
+// context draws, r3p: 32 sequences +1 to +9 pt of HBM, 40 about even; two
+// stay better at <= 24 and >= 48 sequences)
+#ifndef KB_DEC_ADAPT_IPC
+#define KB_DEC_ADAPT_IPC 1
+#endif
 #ifndef KB_DEC_MIN_TILES
 #define KB_DEC_MIN_TILES 2
 #endif
@@ -122,6 +130,9 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
   __shared__ unsigned long long total_tiles;
   __shared__ int T;
   const int tid = threadIdx.x;
+  const long long pairs = (long long)nseq * Hkv;
+  const int ipc = (KB_DEC_ADAPT_IPC && 2 * pairs >= 3LL * grid_ctas && 5 * pairs <= 12LL * grid_ctas)
+                      ? 3 : kItemsPerCta;
   if (tid == 0) total_tiles = 0;
   for (int i = tid; i < kMaxLayers; i += blockDim.x) item_counter[i] = 0;
   for (int i = tid; i < nseq * Hkv; i += blockDim.x) split_done[i] = 0;
@@ -133,8 +144,8 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
   __syncthreads();
   if (tid == 0) {
     const unsigned long long work = total_tiles * (unsigned long long)Hkv;
-    const unsigned long long per = (work + (unsigned long long)grid_ctas * kItemsPerCta - 1) /
-                                   ((unsigned long long)grid_ctas * kItemsPerCta);
+    const unsigned long long per = (work + (unsigned long long)grid_ctas * ipc - 1) /
+                                   ((unsigned long long)grid_ctas * ipc);
     T = (int)(per > (unsigned long long)min_tiles ? per : min_tiles);
   }
   __syncthreads();
@@ -156,7 +167,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
     if (lane == 0) cnt_w[w] = c * Hkv;
     __syncthreads();
     if (tid == 0) {
-      const long long target = (long long)grid_ctas * kItemsPerCta;
+      const long long target = (long long)grid_ctas * ipc;
       for (int k = 0; k < 32; ++k)
         if (cnt_w[k] <= target) {
           T += k;
@@ -199,7 +210,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
     atomicAdd(&cnt_all, c);
     __syncthreads();
     if (tid == 0) {
-      const long long target = (long long)grid_ctas * kItemsPerCta;
+      const long long target = (long long)grid_ctas * ipc;
       const long long cnt = (long long)cnt_all * Hkv;
       const long long extra = cnt <= target ? (target - cnt) / Hkv : 0;
       thr = 1 << 30;

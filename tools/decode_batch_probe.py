@@ -26,7 +26,8 @@ APPEND = os.environ.get("KB_PROBE_APPEND", "0") == "1"
 # KB_PROBE_MERGE=1: force the combine launch, 0: force the in-kernel merge
 KW = {"combine": os.environ["KB_PROBE_MERGE"] == "1"} if "KB_PROBE_MERGE" in os.environ else {}
 out = {}
-SIZES = [int(os.environ["KB_PROBE_NSEQ"])] if "KB_PROBE_NSEQ" in os.environ else [4, 16, 32, 64, 147]
+SIZES = ([int(x) for x in os.environ["KB_PROBE_NSEQ"].split(",")] if "KB_PROBE_NSEQ" in os.environ
+         else [4, 16, 32, 64, 147])
 for nseq in SIZES:
     ctx = np.clip(rng.lognormal(np.log(1500), 0.6, nseq), 16, 8000).astype(int)
     slots = list(range(nseq))
