@@ -29,6 +29,13 @@ constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per per
 #ifndef KB_DEC_ADAPT_IPC
 #define KB_DEC_ADAPT_IPC 1
 #endif
+// ...and one item per CTA below half a pair per CTA (<= 9 Llama sequences:
+// the items are then whole pairs of similar length, and a second round only
+// adds a merge; r3r: +2 to +6 pt at 4-8 sequences, 2 items stay better at
+// 12-24).  Twice the items-per-CTA target there, an A/B knob:
+#ifndef KB_DEC_TINY_IPC_X2
+#define KB_DEC_TINY_IPC_X2 2
+#endif
 #ifndef KB_DEC_MIN_TILES
 #define KB_DEC_MIN_TILES 2
 #endif
@@ -131,8 +138,11 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
   __shared__ int T;
   const int tid = threadIdx.x;
   const long long pairs = (long long)nseq * Hkv;
-  const int ipc = (KB_DEC_ADAPT_IPC && 2 * pairs >= 3LL * grid_ctas && 5 * pairs <= 12LL * grid_ctas)
-                      ? 3 : kItemsPerCta;
+  // items per CTA, doubled (the small-batch knob allows halves)
+  const int ipc2 = !KB_DEC_ADAPT_IPC ? 2 * kItemsPerCta
+                   : (2 * pairs >= 3LL * grid_ctas && 5 * pairs <= 12LL * grid_ctas) ? 6
+                   : (2 * pairs < (long long)grid_ctas) ? KB_DEC_TINY_IPC_X2
+                   : 2 * kItemsPerCta;
   if (tid == 0) total_tiles = 0;
   for (int i = tid; i < kMaxLayers; i += blockDim.x) item_counter[i] = 0;
   for (int i = tid; i < nseq * Hkv; i += blockDim.x) split_done[i] = 0;
@@ -144,8 +154,8 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
   __syncthreads();
   if (tid == 0) {
     const unsigned long long work = total_tiles * (unsigned long long)Hkv;
-    const unsigned long long per = (work + (unsigned long long)grid_ctas * ipc - 1) /
-                                   ((unsigned long long)grid_ctas * ipc);
+    const unsigned long long tgt = ((unsigned long long)grid_ctas * ipc2 + 1) / 2;
+    const unsigned long long per = (work + tgt - 1) / tgt;
     T = (int)(per > (unsigned long long)min_tiles ? per : min_tiles);
   }
   __syncthreads();
@@ -167,7 +177,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
     if (lane == 0) cnt_w[w] = c * Hkv;
     __syncthreads();
     if (tid == 0) {
-      const long long target = (long long)grid_ctas * ipc;
+      const long long target = ((long long)grid_ctas * ipc2 + 1) / 2;
       for (int k = 0; k < 32; ++k)
         if (cnt_w[k] <= target) {
           T += k;
@@ -210,7 +220,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
     atomicAdd(&cnt_all, c);
     __syncthreads();
     if (tid == 0) {
-      const long long target = (long long)grid_ctas * ipc;
+      const long long target = ((long long)grid_ctas * ipc2 + 1) / 2;
       const long long cnt = (long long)cnt_all * Hkv;
       const long long extra = cnt <= target ? (target - cnt) / Hkv : 0;
       thr = 1 << 30;
