@@ -195,9 +195,13 @@ def run_reference(args) -> None:
 
 def copy_sweep(rt, iters: int = 5) -> dict:
     """Config 5 on one GPU: KV-block migration (scattered 256 KiB pages named
-    by block tables) and layer restore (contiguous slab ranges) from 64 KiB
-    to 2 GiB.  Same-GPU copies read and write HBM, so the payload roofline
-    is HBM/2; NVLink (peer pools) is 900 GB/s per direction nominal."""
+    by block tables) and layer restore (contiguous slab ranges) at 64 KiB x
+    2^k up to 2 GiB (16 points).  Same-GPU copies read and write HBM, so the
+    payload roofline is half the copy bandwidth; NVLink (peer pools) is 900
+    GB/s per direction nominal.  The sources hold a deterministic pattern of
+    (page, offset), and after the sweep every copied byte is checked on the
+    device: each page's position-sensitive hash against its source page's,
+    each slab's against its source slab's."""
     import torch
     from paper_2412_18169_b200 import runtime
     from paper_2412_18169_b200.core import SHAPES
@@ -209,6 +213,15 @@ def copy_sweep(rt, iters: int = 5) -> dict:
     pb = shape.page_bytes
     npg = (2 << 30) // pb
     assert a.grow([(0, 0, 1, npg)]) and b.grow([(0, 0, 1, npg)])
+    # f(page, offset): int32 words = golden-ratio hash of their global index
+    kv = a.kv_bytes().view(torch.int32)
+    kv.copy_((torch.arange(kv.numel(), dtype=torch.int64, device="cuda") * 2654435761 % (1 << 31))
+             .to(torch.int32))
+    for l in range(5):
+        w = a.weight_bytes(l).view(torch.int32)
+        w.copy_((torch.arange(w.numel(), dtype=torch.int64, device="cuda") * 40503 + l)
+                .remainder(1 << 31).to(torch.int32))
+    torch.cuda.synchronize()
     b.drop_layers(0, 5)
     b.restore_begin(0, 5)  # a 5-slab (2.19 GB) pull target
     out = {"pages": [], "slabs": []}
@@ -232,11 +245,28 @@ def copy_sweep(rt, iters: int = 5) -> dict:
             ms = ev0.elapsed_time(ev1) / iters
             moved = n * pb if kind == "pages" else size
             out[kind].append([size, round(moved / (ms / 1e3) / 1e9, 1)])
-        size *= 4
+        size *= 2
     b.restore_complete(0, 5)
+    torch.cuda.synchronize()
+    # every byte of the largest point (2 GiB of pages, 2 GiB of slabs)
+    pa = torch.tensor(a.block_table(0, 0), dtype=torch.int64, device="cuda")
+    pb_ = torch.tensor(b.block_table(0, 0), dtype=torch.int64, device="cuda")
+    ha = runtime.hash_segments(a.info().kv_base, pb, npg, index=pa)
+    hb = runtime.hash_segments(b.info().kv_base, pb, npg, index=pb_)
+    pages_ok = bool(torch.equal(ha, hb))
+    rem = 2 << 30
+    slabs_ok = True
+    for l in range(5):
+        nb = min(rem, model.bytes_per_layer)
+        if nb <= 0:
+            break
+        slabs_ok &= bool(torch.equal(runtime.hash_tensor(a.weight_bytes(l)[:nb]),
+                                     runtime.hash_tensor(b.weight_bytes(l)[:nb])))
+        rem -= nb
     a.close()
     b.close()
     out["unit"] = "payload GB/s (same GPU: read + write HBM)"
+    out["verified"] = {"pages_2GiB_hash_equal": pages_ok, "slabs_2GiB_hash_equal": slabs_ok}
     return out
 
 
