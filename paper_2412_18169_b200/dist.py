@@ -308,17 +308,22 @@ class ActChannel:
 
 def nvlink_sweep(rt, max_bytes: int = 2 << 30, iters: int = 5) -> dict:
     """Config 5 across GPUs: every rank pulls contiguous byte ranges (64 KiB
-    to `max_bytes`, x4 steps) from its partner's (rank ^ 1) device buffer
+    x 2^k up to `max_bytes`) from its partner's (rank ^ 1) device buffer
     through a CUDA-IPC mapping with the repo's copy kernel -- the transfer a
     layer restore makes -- both directions at once.  Returns
-    [[bytes, GB/s per direction], ...] with the time max-reduced over ranks."""
+    [[bytes, GB/s per direction], ...] with the time max-reduced over ranks.
+    The buffers hold a (rank, offset) pattern; every byte of the largest
+    point is checked against the owner's position-sensitive hash."""
     import torch
     import torch.distributed as dist
-    from .runtime import IpcBuffer, copy_bytes
+    from .runtime import IpcBuffer, copy_bytes, hash_tensor
     rank, world = dist.get_rank(), dist.get_world_size()
     peer = rank ^ 1
     mine = IpcBuffer.allocate(rt.device, max_bytes)
-    mine.tensor().fill_(rank & 0xFF)
+    words = mine.tensor().view(torch.int32)
+    words.copy_((torch.arange(words.numel(), dtype=torch.int64, device=words.device) * 2654435761
+                 + rank).remainder(1 << 31).to(torch.int32))
+    my_hash = int(hash_tensor(mine.tensor()).item())
     objs = [None] * world
     dist.all_gather_object(objs, mine.export())
     theirs = IpcBuffer.open(rt.device, objs[peer], max_bytes) if peer < world else None
@@ -343,9 +348,11 @@ def nvlink_sweep(rt, max_bytes: int = 2 << 30, iters: int = 5) -> dict:
             ms = 0.0
         ms = max_over_ranks(ms, device=dev)
         out.append([size, round(size / (ms / 1e3) / 1e9, 1) if ms > 0 else None])
-        size *= 4
+        size *= 2
     torch.cuda.synchronize(rt.device)
-    ok = bool((dst[:64] == (peer & 0xFF)).all().item()) if theirs is not None else True
+    hashes = [None] * world
+    dist.all_gather_object(hashes, my_hash)
+    ok = (int(hash_tensor(dst).item()) == hashes[peer]) if theirs is not None else True
     dist.barrier()
     if theirs is not None:
         theirs.close()

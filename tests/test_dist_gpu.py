@@ -216,3 +216,27 @@ def test_eight_rank_pp2_cycle_bit_exact():
         assert d["param"] == 16 * SLAB["llama3_8b"]
     pipe = res[0]["pipe"]
     assert pipe["groups"] == 4 and pipe["handoff_bit_exact"]
+
+
+def _sweep_rank(rank, world, port, q):
+    _init(rank, world, port)
+    import torch.distributed as dist
+    from paper_2412_18169_b200 import build
+    build.build()
+    from paper_2412_18169_b200 import runtime
+    from paper_2412_18169_b200.dist import nvlink_sweep
+    rt = runtime.Runtime(0)
+    res = nvlink_sweep(rt, max_bytes=16 << 20, iters=2)
+    dist.destroy_process_group()
+    q.put((rank, res))
+
+
+def test_nvlink_sweep_two_ranks_bytes_checked():
+    """Config 5 across ranks (here two ranks on one GPU): 64 KiB x 2^k up to
+    16 MiB pulled from the partner's CUDA-IPC-mapped buffer, every byte of
+    the largest point checked against the owner's hash of its pattern."""
+    res = _spawn(_sweep_rank, 2)
+    for r in (0, 1):
+        sizes = [s for s, _ in res[r]["sizes_gbs"]]
+        assert sizes == [(64 << 10) << k for k in range(9)]
+        assert res[r]["bytes_checked"] is True
