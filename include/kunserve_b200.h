@@ -271,7 +271,15 @@ int kb_pool_kv_status(kb_pool* pool, uint32_t* flags, int32_t clear);
  * plan (KV splits, item order) depends only on ctx_lens and
  * slots: with flags & KB_DECODE_REUSE_PLAN the plan already in `workspace`
  * (from an earlier call with the same ctx_lens and slots, e.g. the previous
- * layer of the same decode step) is reused and no plan kernel runs. */
+ * layer of the same decode step) is reused and no plan kernel runs.  Such a
+ * launch (programmatic dependent launch) reads the plan, the block tables
+ * and every K/V row but each sequence's newest token BEFORE its
+ * griddepcontrol.wait: those must have been written by work that completed
+ * before the immediately preceding kernel on `stream` started -- true for
+ * any ordinary kernel, memcpy or event wait in between; of this library's
+ * kernels that let their successor start early, kv_append writes only the
+ * newest token's row and decode / combine write only their outputs and
+ * workspace.  q, slots and ctx_lens are read after the wait. */
 #define KB_DECODE_REUSE_PLAN 1
 /* The KV splits of a (sequence, kv head) merge inside the attention kernel
  * for large batches (>= 4 pairs per SM) and in a combine launch otherwise;
