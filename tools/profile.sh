@@ -9,9 +9,13 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" --csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --decode-iters 2 --no-ttft \
     > gpurun_out/ncu_launch_$TAG.log 2>&1
 echo launches_rc=$?
-# copy_pages: skip the setup/warm-up launches, capture two bulk exchange launches
+# skip the setup / warm-up launches: copy_pages -> two bulk exchange
+# launches, copy_flat -> two 2 GB slab pulls (launches 0-21 of the cycle's
+# copy_flat are the restores' runs; later ones are small hand-off copies)
 for KN in copy_pages_kernel copy_flat_kernel decode_tc_kernel; do
-  ncu --set full --clock-control none --import-source on -k regex:$KN -s 40 -c 2 \
+  SKIP=40
+  [ "$KN" = copy_flat_kernel ] && SKIP=4
+  ncu --set full --clock-control none --import-source on -k regex:$KN -s $SKIP -c 2 \
       -o gpurun_out/prof_${TAG}_$KN \
       python bench.py --steps 1 --warmup 3 --no-cpu-baseline --decode-iters 1 --no-ttft \
       > gpurun_out/ncu_full_${TAG}_$KN.log 2>&1
