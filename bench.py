@@ -803,7 +803,11 @@ def main():
                                     "frac": round(pk_achieved / hbm_peak, 4),
                                     "frac_vs_spec_7700": round(pk_achieved / 7700.0, 4),
                                     "kernel": "copy_flat_kernel (slab pulls)",
-                                    "kernel_ms_per_step": round(pk_ms / args.steps, 3)},
+                                    "kernel_ms_per_step": round(pk_ms / args.steps, 3),
+                                    "traffic": (_traffic("copy_flat_kernel") or {}).get(
+                                        "dram_bytes_per_launch"),
+                                    "traffic_source": (_traffic("copy_flat_kernel") or {}).get(
+                                        "source")},
             "paged_decode": dec,
             "paged_prefill": prefill,
             "copy_sweep": sweep,
