@@ -213,7 +213,12 @@ class OverloadCycle:
             cell.append(self.slots[iid].of[rid] * self.L * self._maxp(iid))  # layer 0, page 0
         for iid, (pos, cell) in per_pool.items():
             bt = self._bt_view(iid).reshape(-1)
-            out[torch.tensor(pos, device="cuda")] = bt[torch.tensor(cell, device="cuda")]
+            # index vectors through pinned memory, copied asynchronously: a
+            # pageable H2D copy would block the host until the stream (queued
+            # behind the whole cycle) drained
+            dev = lambda xs: torch.tensor(xs, dtype=torch.int64).pin_memory().to(  # noqa: E731
+                "cuda", non_blocking=True)
+            out[dev(pos)] = bt[dev(cell)]
         return out
 
     def _maxp(self, iid) -> int:
