@@ -106,6 +106,14 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 #define KB_PF_EMU_EVERY 5
 #endif
 constexpr int kEmuEvery = KB_PF_EMU_EVERY;
+// P key pairs published with p_lo (the rest with p_hi): 48 = keys 0-95, so
+// only the P.V of keys 96-127 (two K=16 steps) and the next QK separate a
+// tile's softmax from the next one (32 = halves, the round-1 split)
+#ifndef KB_PF_PSPLIT
+#define KB_PF_PSPLIT 48
+#endif
+constexpr int kPSplit = KB_PF_PSPLIT;
+static_assert(kPSplit == 32 || kPSplit == 48, "P publish split: 32 or 48 pairs");
 // (Issuing the QK of keys 64-127 early -- those S columns never hold P --
 // as N=64 MMAs measured 52% against 67%: the half-width MMAs re-read Q for
 // every half and double the QK instruction count.)
@@ -115,6 +123,17 @@ constexpr int kEmuEvery = KB_PF_EMU_EVERY;
 // (Strictly alternating the two tiles' exponential passes through an
 // mbarrier token measured 64.4% vs 65.7% without: the pass is latency-bound
 // per warp, not only MUFU-bound.)
+
+// kSteps K=16 steps of O (+)= P.V: P (fp16 pairs) from TMEM columns 8m
+// onward, V rows 16m onward (the SW128 MN-major descriptor advances 2 KiB,
+// 128 in 16-byte units, per 16 rows)
+template <int kSteps>
+__device__ __forceinline__ void mma_ts_steps(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t acc_first) {
+#pragma unroll
+  for (int m = 0; m < kSteps; ++m)
+    sm100::mma_f16_ts(tmem_d, tmem_a + 8 * m, bdesc + 128 * m, idesc, m == 0 ? acc_first : 1u);
+}
 
 struct PrefillMisc {
   uint64_t full[kPfStages];
@@ -139,7 +158,13 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
   using namespace sm100;
   constexpr int kPPT = kPfTile / kB;
   const int hq = blockIdx.y;
+#ifndef KB_PF_LIGHT_FIRST
+  // the causal row tiles furthest down see the most keys: dispatch them first
+  const int seq = blockIdx.x / mtiles, mt = mtiles - 1 - (int)(blockIdx.x % mtiles);
+#else
   const int seq = blockIdx.x / mtiles, mt = blockIdx.x % mtiles;  // mt: 256-row CTA tile
+#endif
+  const int64_t unit_x = (int64_t)seq * mtiles + mt;  // partials index (prefill_combine_kernel)
   const int split = blockIdx.z, splits = gridDim.z;
   const int h = hq / (Hq / Hkv);
   const int qlen = q_len[seq], pre = prefix[seq], qo = q_off[seq];
@@ -155,7 +180,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
   const int nt = (int)((int64_t)(split + 1) * nt_all / splits) - j0;
   if (nt <= 0) {
     if (splits > 1 && threadIdx.x < 2 * kPfTile) {  // empty split: l = 0
-      const int64_t u = ((int64_t)blockIdx.x * Hq + hq) * splits + split;
+      const int64_t u = (unit_x * Hq + hq) * splits + split;
       float* ml = reinterpret_cast<float*>(part + (int64_t)gridDim.x * Hq * splits * 2 * kPfTile * 256) +
                   (u * 2 * kPfTile + threadIdx.x) * 2;
       ml[0] = -INFINITY;
@@ -288,14 +313,15 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 #endif
       if (lane == 0) {
         // 16-key group m: P (fp16 pairs) at TMEM column 8m, V rows 16m..16m+15
-        mma_ts_k64(tm + 256 + t * 128, tm + t * 128, vdesc, kIdPV, j > 0 ? 1u : 0u);
+        mma_ts_steps<kPSplit / 8>(tm + 256 + t * 128, tm + t * 128, vdesc, kIdPV, j > 0 ? 1u : 0u);
         mma_commit(&misc->pv_lo[t]);
       }
       __syncwarp();
       mbar_wait(&misc->p_hi[t], j & 1);
       tc_fence_after();
       if (lane == 0) {
-        mma_ts_k64(tm + 256 + t * 128, tm + t * 128 + 32, vdesc + 512, kIdPV, 1u);
+        mma_ts_steps<(64 - kPSplit) / 8>(tm + 256 + t * 128, tm + t * 128 + kPSplit,
+                                         vdesc + 16 * kPSplit, kIdPV, 1u);
         // O_t is read only by the epilogue: signal once, after the last tile
         if (j == nt - 1) mma_commit(&misc->o_done[t]);
         if (t == 1) mma_commit(&misc->empty[stage]);
@@ -458,46 +484,52 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         fence_proxy_async_smem();
       }
       // pass 2: P = exp2(S*scale - m_ref) as fp16 pairs (the V cache is
-      // fp16, kb_append.cu), written over S: the 64 keys of S half hh land in
-      // P columns [32hh, 32hh + 32) -- columns whose S values were consumed.
+      // fp16, kb_append.cu), written over S: key pair p lands in P column p
+      // (columns [0, 64)) -- columns whose S values were consumed.  The first
+      // kPSplit pairs are published together (p_lo: their P.V starts), the
+      // rest after (p_hi), so only the tail's P.V and the next QK sit between
+      // this tile's softmax and the next one.
       float2 rs2[4] = {};  // four partial sums: no 64-long dependent add chain
       const bool live = m_ref != -INFINITY;
       const float2 sc2 = make_float2(scale_log2, scale_log2);
       float2 nm2 = make_float2(-m_ref, -m_ref);
       // one straight-line body per case: unmasked tiles carry no selects
-      auto p_half = [&](auto masked, auto half, uint32_t (&w)[32]) {
+      auto p_chunk = [&](auto masked, auto p0, auto np, auto& w) {
         constexpr bool kMasked = decltype(masked)::value;
-        constexpr int hh = decltype(half)::value;
+        constexpr int P0 = decltype(p0)::value, NP = decltype(np)::value;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int col = 2 * i;  // 0..63 within the half
-          const float2 sv = make_float2(__uint_as_float(sr[2 * hh + (col >> 5)][col & 31]),
-                                        __uint_as_float(sr[2 * hh + (col >> 5)][(col & 31) + 1]));
+        for (int i = 0; i < NP; ++i) {
+          const int p = P0 + i;
+          const int col = 2 * p;  // key within the tile
+          const float2 sv = make_float2(__uint_as_float(sr[col >> 5][col & 31]),
+                                        __uint_as_float(sr[col >> 5][(col & 31) + 1]));
           const float2 xv = ffma2(sv, sc2, nm2);
           float2 v;
-          if (i % kEmuEvery == kEmuEvery - 1) {
+          if ((p & 31) % kEmuEvery == kEmuEvery - 1) {
             v = exp2_fma2(xv);
           } else {
             v.x = fast_exp2(xv.x);
             v.y = fast_exp2(xv.y);
           }
           if (kMasked) {
-            const int key = kbase + hh * 64 + col;
+            const int key = kbase + col;
             const bool ok0 = row_ok && key <= qpos && live, ok1 = row_ok && key + 1 <= qpos && live;
             v.x = ok0 ? v.x : 0.f;
             v.y = ok1 ? v.y : 0.f;
           }
-          rs2[i & 3] = fadd2(rs2[i & 3], v);
+          rs2[p & 3] = fadd2(rs2[p & 3], v);
           const __half2 hp = __floats2half2_rn(v.x, v.y);
           w[i] = *reinterpret_cast<const uint32_t*>(&hp);
         }
       };
-      auto store_half = [&](auto half) {
-        constexpr int hh = decltype(half)::value;
-        uint32_t w[32];
-        if (full_tile) p_half(std::false_type{}, half, w);
-        else p_half(std::true_type{}, half, w);
-        tmem_st_32x32b_x32(s_addr + 32 * hh, w);
+      auto store_chunk = [&](auto p0, auto np) {
+        constexpr int P0 = decltype(p0)::value, NP = decltype(np)::value;
+        static_assert(NP == 16 || NP == 32, "P chunks are 16 or 32 columns");
+        uint32_t w[NP];
+        if (full_tile) p_chunk(std::false_type{}, p0, np, w);
+        else p_chunk(std::true_type{}, p0, np, w);
+        if constexpr (NP == 32) tmem_st_32x32b_x32(s_addr + P0, w);
+        else tmem_st_32x32b_x16(s_addr + P0, w);
       };
       auto take_rs = [&]() {
         const float r = (rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y) + (rs2[2].x + rs2[2].y) +
@@ -511,31 +543,41 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         tc_fence_before();
         mbar_arrive(bar);
       };
-      using H0 = std::integral_constant<int, 0>;
-      using H1 = std::integral_constant<int, 1>;
-      // max of x = s*scale - m_ref over one half's valid columns (registers)
-      auto half_xmax = [&](auto half) {
-        constexpr int hh = decltype(half)::value;
+      using I0 = std::integral_constant<int, 0>;
+      using I16 = std::integral_constant<int, 16>;
+      using I32 = std::integral_constant<int, 32>;
+      using I48 = std::integral_constant<int, 48>;
+      // the two publish groups: pairs [0, kPSplit) and [kPSplit, 64)
+      auto store_lo = [&]() {
+        store_chunk(I0{}, I32{});
+        if constexpr (kPSplit == 48) store_chunk(I32{}, I16{});
+      };
+      auto store_hi = [&]() {
+        if constexpr (kPSplit == 48) store_chunk(I48{}, I16{});
+        else store_chunk(I32{}, I32{});
+      };
+      // max of x = s*scale - m_ref over the valid keys [k0, k1) (registers)
+      auto range_xmax = [&](auto k0c, auto k1c) {
+        constexpr int K0 = decltype(k0c)::value, K1 = decltype(k1c)::value;
         float m = -INFINITY;
 #pragma unroll
-        for (int c = 2 * hh; c < 2 * hh + 2; ++c)
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const bool ok = full_tile || (row_ok && (kbase + c * 32 + i) <= qpos);
-            m = fmaxf(m, ok ? __uint_as_float(sr[c][i]) : -INFINITY);
-          }
+        for (int k = K0; k < K1; ++k) {
+          const bool ok = full_tile || (row_ok && (kbase + k) <= qpos);
+          m = fmaxf(m, ok ? __uint_as_float(sr[k >> 5][k & 31]) : -INFINITY);
+        }
         return m * scale_log2 - m_ref;
       };
-      // Fast path overflow guard: a half's row sum above 2^14 means some P
+      using KS = std::integral_constant<int, 2 * kPSplit>;
+      using K128 = std::integral_constant<int, 128>;
+      // Fast path overflow guard: a group's row sum above 2^14 means some P
       // may have left the lazily-rescaled range (and fp16's, at 2^16): take
       // the real max then, rescale, and recompute.  No per-element max
       // tracking; the comparison also catches inf / NaN sums.
       constexpr float kSumBound = 16384.f;
-      // keys 0-63
-      store_half(H0{});
+      store_lo();
       float rs = take_rs();
       if (fast && __any_sync(0xffffffffu, !(rs <= kSumBound))) {  // rare
-        const float xmax = half_xmax(H0{});
+        const float xmax = range_xmax(I0{}, KS{});
         const bool need = !(rs <= kSumBound);
         const float alpha = need ? exp2f(-xmax) : 1.f;  // 2^(m_ref - (m_ref + xmax))
         rescale_o(alpha);
@@ -544,33 +586,18 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
           m_ref += xmax;
         }
         nm2 = make_float2(-m_ref, -m_ref);
-        store_half(H0{});  // P again with the new reference
+        store_lo();  // P again with the new reference
         rs = take_rs();
       }
-#ifdef KB_PF_ST_REORDER
-      // keys 64-127 computed before P of keys 0-63 is published: the
-      // tcgen05.wait::st of the first half's stores then finds them done
-      uint32_t w_hi[32];
-      if (full_tile) p_half(std::false_type{}, H1{}, w_hi);
-      else p_half(std::true_type{}, H1{}, w_hi);
-      const float rs_hi = take_rs();
       l_run += rs;
       publish(&misc->p_lo[t]);
-      rs = rs_hi;
-      const bool ovf = fast && __any_sync(0xffffffffu, !(rs <= kSumBound));
-      if (!ovf) tmem_st_32x32b_x32(s_addr + 32, w_hi);
-      if (ovf) {
-#else
-      l_run += rs;
-      publish(&misc->p_lo[t]);
-      // keys 64-127 (the P.V of keys 0-63 may already be running)
-      store_half(H1{});
+      // the remaining keys (the P.V of the first group may already be running)
+      store_hi();
       rs = take_rs();
       if (fast && __any_sync(0xffffffffu, !(rs <= kSumBound))) {
-#endif
-        // rare: O already holds this tile's first-half P.V under the old
+        // rare: O already holds this tile's first-group P.V under the old
         // reference -- let it land, then rescale everything so far
-        const float xmax = half_xmax(H1{});
+        const float xmax = range_xmax(KS{}, K128{});
         const bool need = !(rs <= kSumBound);
         mbar_wait(&misc->pv_lo[t], j & 1);
         tc_fence_after();
@@ -589,7 +616,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
           m_ref += xmax;
         }
         nm2 = make_float2(-m_ref, -m_ref);
-        store_half(H1{});
+        store_hi();
         rs = take_rs();
       }
       l_run += rs;
@@ -611,7 +638,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
     mbar_wait(&misc->pv_lo[t], (nt - 1) & 1);  // the last tile's phase, for synccheck
     tc_fence_after();
     if (splits > 1) {
-      const int64_t u = ((int64_t)blockIdx.x * Hq + hq) * splits + split;
+      const int64_t u = (unit_x * Hq + hq) * splits + split;
       const int prow = t * kPfTile + r;  // row within the CTA's 256
       // partial O normalised by its own l, as fp16 (|O/l| <= max |v|; the
       // combine re-weights by l * 2^(m - M))
