@@ -106,11 +106,12 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 #define KB_PF_EMU_EVERY 5
 #endif
 constexpr int kEmuEvery = KB_PF_EMU_EVERY;
-// P key pairs published with p_lo (the rest with p_hi): 48 = keys 0-95, so
-// only the P.V of keys 96-127 (two K=16 steps) and the next QK separate a
-// tile's softmax from the next one (32 = halves, the round-1 split)
+// P key pairs published with p_lo (the rest with p_hi): 32 = halves; 48 =
+// keys 0-95 first, so only the P.V of keys 96-127 and the next QK separate
+// a tile's softmax from the next one -- measured 0.5% slower on the config-4
+// layer (the loop is bound by the softmax, not by that tail; r4 pf_ab)
 #ifndef KB_PF_PSPLIT
-#define KB_PF_PSPLIT 48
+#define KB_PF_PSPLIT 32
 #endif
 constexpr int kPSplit = KB_PF_PSPLIT;
 static_assert(kPSplit == 32 || kPSplit == 48, "P publish split: 32 or 48 pairs");
