@@ -184,7 +184,8 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
   const bool producer = warp == 4 && lane == 0;
   int n_items = 0, npre = 0, published = 0;
   bool exhausted = false;
-  auto publish = [&]() {
+  // pre: the static first item, when the caller already loaded it
+  auto publish = [&](const DecodeItem* pre = nullptr) {
     if (exhausted) return;
     const int r = published++;
     const int slot = r % kRing;
@@ -205,7 +206,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     }
     DecodeItem v{};
     v.nt = -1;
-    if (idx >= 0) v = items[idx];
+    if (idx >= 0) v = pre ? *pre : items[idx];
     misc->ring_it[slot] = v;
     mbar_arrive(&misc->ring_full[slot]);
   };
@@ -218,9 +219,15 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
   // kv_append, the usual predecessor, writes K/V -- the newest token's row,
   // which no tile loaded here holds).  q and the counters are read after it.
   if (early_loads && producer) {
+    // the item count and the static first item load together (one global
+    // round trip less before the first TMA); the plan never holds more than
+    // nseq * Hkv * max_splits items, so the speculative read stays in it
+    const bool spec = (int)blockIdx.x < nseq * Hkv * max_splits;
+    DecodeItem first{};
+    if (spec) first = items[blockIdx.x];
     n_items = *n_items_ptr;
     if ((int)blockIdx.x < n_items) {
-      publish();
+      publish(spec ? &first : nullptr);
       DecodeItem it0;
       get_item(0, it0);
       // tiles [0, nsafe) end before the newest token (position ctx - 1)

@@ -114,6 +114,11 @@ constexpr int kEmuEvery = KB_PF_EMU_EVERY;
 #define KB_PF_PSPLIT 32
 #endif
 constexpr int kPSplit = KB_PF_PSPLIT;
+#ifdef KB_PF_THREAD_ARRIVE
+constexpr int kPArrivals = 128;  // every softmax thread arrives on p_lo / p_hi
+#else
+constexpr int kPArrivals = 4;    // one elected lane per softmax warp
+#endif
 static_assert(kPSplit == 32 || kPSplit == 48, "P publish split: 32 or 48 pairs");
 // (Issuing the QK of keys 64-127 early -- those S columns never hold P --
 // as N=64 MMAs measured 52% against 67%: the half-width MMAs re-read Q for
@@ -135,6 +140,23 @@ __device__ __forceinline__ void mma_ts_steps(uint32_t tmem_d, uint32_t tmem_a, u
   for (int m = 0; m < kSteps; ++m)
     sm100::mma_f16_ts(tmem_d, tmem_a + 8 * m, bdesc + 128 * m, idesc, m == 0 ? acc_first : 1u);
 }
+
+#ifdef KB_PF_TRACE
+// per-tile clock64 stamps of one CTA (grid (0,0,0)), printed at its end:
+// [t][j][slot] -- 0 S ready (softmax), 1 p_lo published, 2 p_hi published,
+// 3 MMA saw p_lo, 4 PV_lo issued, 5 MMA saw p_hi, 6 PV_hi issued,
+// 7 QK(t, j) issued
+__device__ long long g_pft[2][128][8];
+#define PFT(slot, t, j)                                                                   \
+  do {                                                                                    \
+    if (lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 128) \
+      g_pft[t][j][slot] = clock64();                                                      \
+  } while (0)
+#else
+#define PFT(slot, t, j) \
+  do {                  \
+  } while (0)
+#endif
 
 struct PrefillMisc {
   uint64_t full[kPfStages];
@@ -205,8 +227,8 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       }
       for (int t = 0; t < 2; ++t) {
         mbar_init(&misc->s_full[t], 1);
-        mbar_init(&misc->p_lo[t], 128);
-        mbar_init(&misc->p_hi[t], 128);
+        mbar_init(&misc->p_lo[t], kPArrivals);
+        mbar_init(&misc->p_hi[t], kPArrivals);
         mbar_init(&misc->pv_lo[t], 1);
         mbar_init(&misc->o_done[t], 1);
       }
@@ -292,6 +314,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         mma_commit(&misc->s_full[t]);
       }
       __syncwarp();
+      PFT(7, t, j);
 #ifdef KB_PF_TIMING
       w_iqk += clock64() - ci;
 #endif
@@ -305,6 +328,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       const long long c0 = clock64();
 #endif
       mbar_wait(&misc->p_lo[t], j & 1);
+      PFT(3, t, j);
 #ifdef KB_PF_TIMING
       w_p += clock64() - c0;
 #endif
@@ -318,7 +342,9 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         mma_commit(&misc->pv_lo[t]);
       }
       __syncwarp();
+      PFT(4, t, j);
       mbar_wait(&misc->p_hi[t], j & 1);
+      PFT(5, t, j);
       tc_fence_after();
       if (lane == 0) {
         mma_ts_steps<(64 - kPSplit) / 8>(tm + 256 + t * 128, tm + t * 128 + kPSplit,
@@ -328,6 +354,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         if (t == 1) mma_commit(&misc->empty[stage]);
       }
       __syncwarp();
+      PFT(6, t, j);
 #ifdef KB_PF_TIMING
       w_ipv += clock64() - ci;
 #endif
@@ -389,6 +416,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       // needs the barrier, but every phase is waited so that no arrival
       // lands on a completed, unobserved phase (compute-sanitizer synccheck)
       if (j > 0) mbar_wait(&misc->pv_lo[t], (j - 1) & 1);
+      if ((warp & 3) == 0) PFT(0, t, j);
 #ifdef KB_PF_TIMING
       const long long tw1 = clock64();
       t_wait += tw1 - tw0;
@@ -542,7 +570,14 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       auto publish = [&](uint64_t* bar) {
         tmem_st_wait();
         tc_fence_before();
+#ifdef KB_PF_THREAD_ARRIVE
         mbar_arrive(bar);
+#else
+        // one arrive per warp once every lane's stores have landed (128
+        // single-thread arrives on one barrier serialise in the SYNCS unit)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar);
+#endif
       };
       using I0 = std::integral_constant<int, 0>;
       using I16 = std::integral_constant<int, 16>;
@@ -592,6 +627,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       }
       l_run += rs;
       publish(&misc->p_lo[t]);
+      if ((warp & 3) == 0) PFT(1, t, j);
       // the remaining keys (the P.V of the first group may already be running)
       store_hi();
       rs = take_rs();
@@ -625,6 +661,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       t_c += clock64();
 #endif
       publish(&misc->p_hi[t]);
+      if ((warp & 3) == 0) PFT(2, t, j);
 #ifdef KB_PF_TIMING
       t_soft += clock64() - tw1;
 #endif
@@ -688,6 +725,17 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
     tc_fence_after();
     tmem_dealloc(tmem, kPfTmemCols);
   }
+#ifdef KB_PF_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    __threadfence();
+    const long long b = g_pft[0][0][0];
+    for (int j = 0; j < min(nt, 128); ++j)
+      for (int t = 0; t < 2; ++t)
+        printf("pft %d %d %lld %lld %lld %lld %lld %lld %lld %lld\n", j, t, g_pft[t][j][0] - b,
+               g_pft[t][j][1] - b, g_pft[t][j][2] - b, g_pft[t][j][3] - b, g_pft[t][j][4] - b,
+               g_pft[t][j][5] - b, g_pft[t][j][6] - b, g_pft[t][j][7] - b);
+  }
+#endif
 }
 
 // Merge the KV splits of every (sequence, 256-row tile, q head) unit:
