@@ -308,11 +308,17 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 #ifdef KB_PF_TIMING
       const long long ci = clock64();
 #endif
+#ifdef KB_PF_LANE0_MMA
       if (lane == 0) {
         mma_ss_k128(tm + t * 128, sw128_desc(smem_u32(sQ + t * kPfQ), 16, 1024),
                     sw128_desc(smem_u32(smem + stage * kPfKV), 16, 1024), kIdQK);
         mma_commit(&misc->s_full[t]);
       }
+#else
+      mma_ss_k128_w(tm + t * 128, sw128_desc(smem_u32(sQ + t * kPfQ), 16, 1024),
+                    sw128_desc(smem_u32(smem + stage * kPfKV), 16, 1024), kIdQK);
+      mma_commit_w(&misc->s_full[t]);
+#endif
       __syncwarp();
       PFT(7, t, j);
 #ifdef KB_PF_TIMING
@@ -336,16 +342,26 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 #ifdef KB_PF_TIMING
       const long long ci = clock64();
 #endif
+#ifdef KB_PF_LANE0_MMA
       if (lane == 0) {
         // 16-key group m: P (fp16 pairs) at TMEM column 8m, V rows 16m..16m+15
         mma_ts_steps<kPSplit / 8>(tm + 256 + t * 128, tm + t * 128, vdesc, kIdPV, j > 0 ? 1u : 0u);
         mma_commit(&misc->pv_lo[t]);
       }
+#else
+      if constexpr (kPSplit == 32) {
+        mma_ts_k64_w(tm + 256 + t * 128, tm + t * 128, vdesc, kIdPV, j > 0 ? 1u : 0u);
+      } else if (lane == 0) {
+        mma_ts_steps<kPSplit / 8>(tm + 256 + t * 128, tm + t * 128, vdesc, kIdPV, j > 0 ? 1u : 0u);
+      }
+      mma_commit_w(&misc->pv_lo[t]);
+#endif
       __syncwarp();
       PFT(4, t, j);
       mbar_wait(&misc->p_hi[t], j & 1);
       PFT(5, t, j);
       tc_fence_after();
+#ifdef KB_PF_LANE0_MMA
       if (lane == 0) {
         mma_ts_steps<(64 - kPSplit) / 8>(tm + 256 + t * 128, tm + t * 128 + kPSplit,
                                          vdesc + 16 * kPSplit, kIdPV, 1u);
@@ -353,6 +369,17 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
         if (j == nt - 1) mma_commit(&misc->o_done[t]);
         if (t == 1) mma_commit(&misc->empty[stage]);
       }
+#else
+      if constexpr (kPSplit == 32) {
+        mma_ts_k64_w(tm + 256 + t * 128, tm + t * 128 + kPSplit, vdesc + 16 * kPSplit, kIdPV, 1u);
+      } else if (lane == 0) {
+        mma_ts_steps<(64 - kPSplit) / 8>(tm + 256 + t * 128, tm + t * 128 + kPSplit,
+                                         vdesc + 16 * kPSplit, kIdPV, 1u);
+      }
+      // O_t is read only by the epilogue: signal once, after the last tile
+      if (j == nt - 1) mma_commit_w(&misc->o_done[t]);
+      if (t == 1) mma_commit_w(&misc->empty[stage]);
+#endif
       __syncwarp();
       PFT(6, t, j);
 #ifdef KB_PF_TIMING
