@@ -37,7 +37,7 @@ import time
 from typing import Optional
 
 from . import runtime
-from .core import RequestState
+from .core import Microbatch, RequestState
 from .exchange import TaskKind
 from .serving import DeviceEngine
 
@@ -255,6 +255,20 @@ class WallClockEngine(DeviceEngine):
             self._stage_done(gid, rnd, k, s, start, end)
         finally:
             self._act_key = None
+
+    def _complete_microbatch(self, grun, mb, when) -> None:
+        """A request the monitor stalled while its round ran on the device
+        (a KV exchange, swap-out, migration or consolidation planned at a
+        tick mid-round) gets no credit for that round's chunk: its KV is
+        moving, and it runs the step again after RESUME (the append rewrites
+        the same position).  The reference's event clock never stalls a
+        request inside its own round; without this a stalled request whose
+        last token lands would go STALLED -> FINISHED (illegal, core.py)."""
+        keep = [ch for ch in mb.chunks
+                if self.requests[ch.rid].state is not RequestState.STALLED]
+        if len(keep) != len(mb.chunks):
+            mb = Microbatch(mb.mbid, keep)
+        super()._complete_microbatch(grun, mb, when)
 
     def _act_copied(self, gid, rnd, k, s, ca, ce, dev) -> None:
         """The hand-off after stage s of microbatch k landed: the reference's

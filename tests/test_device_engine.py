@@ -116,3 +116,40 @@ def test_decode_graph_cache_is_bounded(built):
     assert sizes  # graphs were used
     for pool in eng.pools.values():
         pool.close()
+
+
+def test_wall_engine_discards_chunks_of_requests_stalled_mid_round(built):
+    """The wall-clock monitor can stall a request (KV exchange / swap-out /
+    migration planned at a tick) while its round still runs on the device.
+    Its chunk earns nothing when the round lands -- no token, no
+    STALLED -> FINISHED -- and the others in the microbatch complete."""
+    from paper_2412_18169_b200.core import Chunk, Microbatch, Request, RequestState
+    from paper_2412_18169_b200.realtime import WallClockEngine
+    from paper_2412_18169_b200.serving import device_config
+    shape = SHAPES["tiny"]
+    cfg = device_config(shape, instances=2, kv_bytes=1 << 20)
+    cfg.policy.kind = "kunserve"
+    trace = [TraceRecord(0, 40, 1), TraceRecord(0, 40, 1)]
+    eng = WallClockEngine(cfg, trace, precapture_depths=())
+    grun = next(iter(eng.groups.values()))
+    a, b = 0, 1
+    ra, rb = Request(a, 0, 40, 1), Request(b, 0, 40, 1)
+    eng.requests.update({a: ra, b: rb})
+    for r in (ra, rb):
+        r.home_instance = grun.group.member_instances[0]
+        r.set_state(RequestState.PREFILLING)
+        r.tokens_prefilled = r.input_len
+        r.set_state(RequestState.DECODING)
+        r.first_token_us = 0
+    ra.set_state(RequestState.STALLED)
+    eng.pending_prefill = {a: ra.input_len, b: rb.input_len}
+    grun.active |= {a, b}
+    for rid, r in ((a, ra), (b, rb)):
+        assert eng.group_alloc(grun, rid, r.input_len + 1)
+    mb = Microbatch(0, [Chunk(a, 1, ra.input_len, decode=True),
+                        Chunk(b, 1, rb.input_len, decode=True)])
+    eng._complete_microbatch(grun, mb, 1000)
+    assert ra.state is RequestState.STALLED and ra.tokens_decoded == 0
+    assert rb.state is RequestState.FINISHED and rb.tokens_decoded == 1
+    for pool in eng.pools.values():
+        pool.close()
