@@ -257,15 +257,19 @@ class WallClockEngine(DeviceEngine):
             self._act_key = None
 
     def _complete_microbatch(self, grun, mb, when) -> None:
-        """A request the monitor stalled while its round ran on the device
-        (a KV exchange, swap-out, migration or consolidation planned at a
-        tick mid-round) gets no credit for that round's chunk: its KV is
-        moving, and it runs the step again after RESUME (the append rewrites
-        the same position).  The reference's event clock never stalls a
-        request inside its own round; without this a stalled request whose
-        last token lands would go STALLED -> FINISHED (illegal, core.py)."""
+        """A request the monitor stalled or moved while its round ran on
+        the device (a KV exchange, swap-out, migration or consolidation
+        planned at a tick mid-round) gets no credit for that round's chunk:
+        its KV is moving, and it runs the step again after RESUME (the append
+        rewrites the same position) -- in its new group if it migrated, so a
+        chunk counts only while the request is still one of this group's.
+        The reference's event clock never changes a request inside its own
+        round; without this a stalled request whose last token lands would
+        go STALLED -> FINISHED (illegal, core.py), and a migrated one would
+        be finished against its old group's allocation."""
         keep = [ch for ch in mb.chunks
-                if self.requests[ch.rid].state is not RequestState.STALLED]
+                if self.requests[ch.rid].state is not RequestState.STALLED
+                and ch.rid in grun.active]
         if len(keep) != len(mb.chunks):
             mb = Microbatch(mb.mbid, keep)
         super()._complete_microbatch(grun, mb, when)

@@ -146,10 +146,19 @@ def test_wall_engine_discards_chunks_of_requests_stalled_mid_round(built):
     grun.active |= {a, b}
     for rid, r in ((a, ra), (b, rb)):
         assert eng.group_alloc(grun, rid, r.input_len + 1)
+    # c migrated to another group mid-round: no longer one of grun's
+    c = 2
+    rc = Request(c, 0, 40, 1)
+    eng.requests[c] = rc
+    rc.set_state(RequestState.PREFILLING)
+    rc.tokens_prefilled = rc.input_len
+    rc.set_state(RequestState.DECODING)
     mb = Microbatch(0, [Chunk(a, 1, ra.input_len, decode=True),
-                        Chunk(b, 1, rb.input_len, decode=True)])
+                        Chunk(b, 1, rb.input_len, decode=True),
+                        Chunk(c, 1, rc.input_len, decode=True)])
     eng._complete_microbatch(grun, mb, 1000)
     assert ra.state is RequestState.STALLED and ra.tokens_decoded == 0
     assert rb.state is RequestState.FINISHED and rb.tokens_decoded == 1
+    assert rc.state is RequestState.DECODING and rc.tokens_decoded == 0
     for pool in eng.pools.values():
         pool.close()
