@@ -628,19 +628,28 @@ def paged_decode(pool: DevicePool, layer: int, q, slots, ctx_lens, max_ctx: int,
 
 def prefill_splits(nseq: int, n_q_heads: int, max_q_len: int, max_kv_len: int,
                    n_sm: int = 148) -> int:
-    """KV splits for one prefill launch (1..8): the best wave fill of the
-    grid (one 256-row CTA per SM) minus 3% per extra split (each split adds a
-    pipeline ramp and combine traffic), keeping >= 16 key tiles per split.
-    Config 4 (Qwen2.5-14B 32k, 2048-token chunks) sweeps to 4 (B200, r1)."""
+    """KV splits for one prefill launch (1..8), keeping >= 16 key tiles per
+    split.  Score = wave fill of the grid (one 256-row CTA per SM) x the
+    share of a split's time spent streaming: each CTA pays a ramp worth
+    ~6.5 key tiles (Q load, pipeline fill, O epilogue, partial write, its
+    share of the combine launch), an unsplit CTA ~2 (no partials, no
+    combine).  Fitted to the r4 B200 per-chunk sweep of config 4
+    (tools/pf_split_sweep.py: 1 split up to 4k keys, 2 to ~13k, 3 to ~17k,
+    4 beyond)."""
     units = nseq * -(-max_q_len // 256) * n_q_heads
     tiles = -(-max_kv_len // 128)
-    best, best_score = 1, units / (n_sm * -(-units // n_sm))
+
+    def score(s: int) -> float:
+        waves = units * s / (n_sm * -(-(units * s) // n_sm))
+        per = tiles / s
+        return waves * per / (per + (2.0 if s == 1 else 6.5))
+    best, best_score = 1, score(1)
     for s in range(2, 9):
         if tiles < 16 * s:
             break
-        score = units * s / (n_sm * -(-(units * s) // n_sm)) - 0.03 * (s - 1)
-        if score > best_score:
-            best, best_score = s, score
+        sc = score(s)
+        if sc > best_score:
+            best, best_score = s, sc
     return best
 
 
