@@ -13,6 +13,8 @@ hit (VERDICT r1 "Next 4 and 9"):
   layers from HOST (or the lowest live holder) and ends byte-identical.
 """
 
+import os
+
 import pytest
 
 torch = pytest.importorskip("torch")
@@ -161,6 +163,8 @@ def test_resident_kv_identical_across_every_exchange_and_consolidation(rtm):
         pool.close()
 
 
+@pytest.mark.skipif(os.environ.get("KB_SANITIZER") == "1",
+                    reason="a timing claim: compute-sanitizer serialises and slows every launch")
 def test_activation_overtakes_a_1gb_kv_burst(rtm):
     """The transfer engine's two streams (transfer.py): a KV burst of 1 GiB
     of pages on the low-priority bulk stream, then an activation hand-off on
@@ -224,6 +228,9 @@ def test_failure_restore_is_byte_exact(rtm, instances, source):
     torch.cuda.synchronize()
     assert eng.instances[0].table.layers_held() == list(range(8))
     assert slab_hashes(rtm, eng.pools[0], range(8)) == boot
-    assert collect(res.log_lines).finished() == len(trace)
+    if os.environ.get("KB_SANITIZER") != "1":
+        # the clock runs on measured stage times, which compute-sanitizer
+        # inflates ~100x: the trace then outlasts the run's end
+        assert collect(res.log_lines).finished() == len(trace)
     for pool in eng.pools.values():
         pool.close()
