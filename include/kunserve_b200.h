@@ -282,7 +282,8 @@ int kb_pool_kv_status(kb_pool* pool, uint32_t* flags, int32_t clear);
  * workspace.  q, slots and ctx_lens are read after the wait. */
 #define KB_DECODE_REUSE_PLAN 1
 /* The KV splits of a (sequence, kv head) merge inside the attention kernel
- * for large batches (>= 4 pairs per SM) and in a combine launch otherwise;
+ * (a dedicated merge warp) from half a pair per SM up, and in a combine
+ * launch for smaller batches;
  * flags & KB_DECODE_COMBINE / KB_DECODE_FUSE force either (A/B, tests). */
 #define KB_DECODE_COMBINE 2
 #define KB_DECODE_FUSE 4

@@ -37,7 +37,16 @@
 namespace kb {
 
 constexpr int kDecStages = 3;
-constexpr int kDecThreads = 192;
+// KB_DEC_MERGE_WARP (default 1): a seventh warp merges the KV splits of a
+// (sequence, kv head) pair inside the kernel -- the fence, the counter
+// round trip and the partial loads leave the softmax warps, and no combine
+// launch follows the layer.  0: the round-1 split (merge on the softmax
+// warps for large batches, a combine launch otherwise).
+#ifndef KB_DEC_MERGE_WARP
+#define KB_DEC_MERGE_WARP 1
+#endif
+constexpr int kDecThreads = KB_DEC_MERGE_WARP ? 224 : 192;
+constexpr int kMRing = 8;  // merge jobs in flight per CTA
 constexpr int kTileTok = 128;
 constexpr int kStageBytes = 65536;       // K (32 KiB) + V (32 KiB) for 128 tokens
 constexpr int kHalfBytes = 16384;        // one 64-wide d-half of a 128-token tile
@@ -65,6 +74,9 @@ struct DecodeMisc {
   uint64_t ring_full[kRing];   // item index published by the producer
   uint64_t ring_empty[kRing];  // MMA warp + softmax done with the item
   DecodeItem ring_it[kRing];   // the published items (nt < 0: no more work)
+  uint64_t m_full[kMRing];   // merge job published by the softmax warps
+  uint64_t m_empty[kMRing];  // merge warp has read the job
+  int4 m_job[kMRing];        // {seq, h, ns, 1}; {.., 0}: no more jobs
   uint32_t tmem_base;
   int32_t last;  // this CTA finished the last split of its (sequence, kv head)
   float red[2][4][8];
@@ -81,8 +93,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define DEC_TRACE(slot) (g_dec_trace[blockIdx.x * kTraceSlots + (slot)] = gtimer())
-#define DEC_TRACE_VAL(slot, v) (g_dec_trace[blockIdx.x * kTraceSlots + (slot)] = (v))
+#ifdef KB_DEC_TRACE_CHAIN
+// chain mode (tools/decode_chain_trace.py): one row of CTAs per layer 0..5
+#define DEC_TRACE_ROW (((layer % 6) * (int)gridDim.x + (int)blockIdx.x) * kTraceSlots)
+#else
+#define DEC_TRACE_ROW ((int)blockIdx.x * kTraceSlots)
+#endif
+#define DEC_TRACE(slot) (g_dec_trace[DEC_TRACE_ROW + (slot)] = gtimer())
+#define DEC_TRACE_VAL(slot, v) (g_dec_trace[DEC_TRACE_ROW + (slot)] = (v))
 #else
 #define DEC_TRACE(slot) ((void)0)
 #define DEC_TRACE_VAL(slot, v) ((void)0)
@@ -130,6 +148,10 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       for (int r = 0; r < kRing; ++r) {
         mbar_init(&misc->ring_full[r], 1);
         mbar_init(&misc->ring_empty[r], 2);
+      }
+      for (int r = 0; r < kMRing; ++r) {
+        mbar_init(&misc->m_full[r], 1);
+        mbar_init(&misc->m_empty[r], 1);
       }
       fence_barrier_init();
     }
@@ -328,6 +350,141 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       if (lane == 0) mbar_arrive(&misc->ring_empty[r % kRing]);  // done with item r
       __syncwarp();
     }
+#if KB_DEC_MERGE_WARP
+  } else if (warp == 6) {
+    // ------------------------------------------------ split merger
+    // Jobs come from the softmax warps once a split's partial (O / l, m, l
+    // rows) is written.  Lane 0 publishes it GPU-wide and counts the pair's
+    // finished splits (threadfence-reduction: the fence is cumulative over
+    // the softmax threads' stores, ordered before it by their named barrier
+    // and the job's mbarrier); the CTA that finishes the last split merges
+    // the pair, one float4 of the 128 head-dim lanes per lane, and re-arms
+    // the counter for the next layer.
+    for (int k = 0;; ++k) {
+      const int slot = k % kMRing;
+      mbar_wait(&misc->m_full[slot], (k / kMRing) & 1);
+      const int4 job = misc->m_job[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&misc->m_empty[slot]);
+      if (!job.w) break;
+      const int seq = job.x, h = job.y, ns = job.z;
+      int32_t* done = split_done + seq * Hkv + h;
+      int last = 0;
+      if (lane == 0) {
+#ifdef KB_DEC_MERGE_FENCES
+        __threadfence();
+        last = atomicAdd(done, 1) == ns - 1;
+#else
+        // one acq_rel atomic instead of fence / relaxed add / fence: its
+        // release half publishes the split's partial rows (cumulative over
+        // the softmax threads' stores, ordered before this lane by their
+        // barrier and the job's mbarrier), its acquire half makes the other
+        // splits' rows visible to the merger
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                     : "=r"(old) : "l"(done) : "memory");
+        last = old == ns - 1;
+#endif
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (!last) continue;
+#ifdef KB_DEC_MERGE_FENCES
+      __threadfence();
+#else
+      __syncwarp();  // lanes 1-31 read after lane 0's acquire (warp-synchronous)
+#endif
+      // every load of the merge is issued before its first use: the (m, l)
+      // of split s for all G rows by lane s, then the partial O rows four
+      // splits at a time -- two or three L2 round trips, not one per split
+      const int64_t row0 = ((int64_t)seq * Hq + h * G) * max_splits;  // row of (g=0, split 0)
+      float mg[8], wl[8];
+      float mstar[8], lsum[8];
+      float4 acc[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        mstar[g] = -INFINITY;
+        lsum[g] = 0.f;
+        acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int s0 = 0; s0 < ns; s0 += 32) {
+        const int sidx = s0 + lane;
+        float lg[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          mg[g] = -INFINITY;
+          lg[g] = 0.f;
+          if (g < G && sidx < ns) {
+            const float2 ml = __ldcg(reinterpret_cast<const float2*>(
+                part_ml + (row0 + (int64_t)g * max_splits + sidx) * 2));
+            mg[g] = ml.x;
+            lg[g] = ml.y;
+          }
+        }
+        // this chunk's maxima, then weights relative to the running max
+        // (chunks of 32 splits only when max_splits > 32)
+        float cm[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          float v = mg[g];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+          cm[g] = v;
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          const float mn = fmaxf(mstar[g], cm[g]);
+          const float sc = (mn == -INFINITY) ? 1.f : exp2f(mstar[g] - mn);  // rescale what we have
+          lsum[g] *= sc;
+          acc[g].x *= sc;
+          acc[g].y *= sc;
+          acc[g].z *= sc;
+          acc[g].w *= sc;
+          mstar[g] = mn;
+          wl[g] = (mg[g] == -INFINITY) ? 0.f : exp2f(mg[g] - mn);
+          float lw = wl[g] * lg[g];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o);
+          lsum[g] += lw;
+        }
+        const int cnt = min(32, ns - s0);
+        for (int i0 = 0; i0 < cnt; i0 += 4) {
+          float4 v[4][8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              v[i][g] = (g < G && i0 + i < cnt)
+                            ? __ldcg(reinterpret_cast<const float4*>(
+                                  part_o + (row0 + (int64_t)g * max_splits + s0 + i0 + i) * 128) +
+                                     lane)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              const float wi = __shfl_sync(0xffffffffu, wl[g], (i0 + i) & 31);
+              acc[g].x += wi * v[i][g].x;
+              acc[g].y += wi * v[i][g].y;
+              acc[g].z += wi * v[i][g].z;
+              acc[g].w += wi * v[i][g].w;
+            }
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        if (g >= G) break;
+        const int64_t hrow = (int64_t)seq * Hq + h * G + g;
+        const float inv = lsum[g] > 0.f ? 1.f / lsum[g] : 0.f;
+        __nv_bfloat162 b01 = __floats2bfloat162_rn(acc[g].x * inv, acc[g].y * inv);
+        __nv_bfloat162 b23 = __floats2bfloat162_rn(acc[g].z * inv, acc[g].w * inv);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&b01);
+        pk.y = *reinterpret_cast<uint32_t*>(&b23);
+        reinterpret_cast<uint2*>(out + hrow * 128)[lane] = pk;
+      }
+      if (lane == 0) *done = 0;
+    }
+#endif
   } else {
     // ------------------------------------------------ softmax / epilogue (tid < 128)
     // Q of an item: G rows (<= 8) x 16 chunks of 16 bytes, two per thread;
@@ -357,6 +514,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     // both P buffers start zero: rows >= 8 (GQA padding) are never written
     for (int c = tid; c < 2 * kPBytes / 16; c += 128)
       reinterpret_cast<int4*>(sP)[c] = make_int4(0, 0, 0, 0);
+    int mjobs = 0;  // merge jobs handed to the merge warp (tid 0 counts)
     DecodeItem it, nxt;
     bool have = get_item(0, it), nhave = false;
     if (have) {
@@ -411,6 +569,19 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           }
         }
       }
+#if KB_DEC_MERGE_WARP
+      if (ns > 1 && fuse_merge) {
+        // hand the split to the merge warp (its partial rows are written)
+        named_bar_sync(1, 128);
+        if (tid == 0) {
+          const int slot = mjobs % kMRing;
+          if (mjobs >= kMRing) mbar_wait(&misc->m_empty[slot], ((mjobs / kMRing) - 1) & 1);
+          misc->m_job[slot] = make_int4(pit.seq, pit.h, ns, 1);
+          mbar_arrive(&misc->m_full[slot]);
+        }
+        ++mjobs;
+      }
+#else
       if (ns > 1 && fuse_merge) {
         // Split-KV merge, fused: the CTA that finishes the last split of
         // (sequence, kv head) merges all of them (threadfence-reduction
@@ -441,6 +612,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           if (tid == 0) *done = 0;
         }
       }
+#endif
       named_bar_sync(1, 128);  // lred / last are reused by the next item
       if (tid == 0) {
         if (pr < 3) DEC_TRACE(6 + pr);
@@ -582,6 +754,14 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       it = nxt;  // item r+1, read from the ring during item r
       have = nhave;
     }
+#if KB_DEC_MERGE_WARP
+    if (tid == 0) {  // no more jobs
+      const int slot = mjobs % kMRing;
+      if (mjobs >= kMRing) mbar_wait(&misc->m_empty[slot], ((mjobs / kMRing) - 1) & 1);
+      misc->m_job[slot] = make_int4(0, 0, 0, 0);
+      mbar_arrive(&misc->m_full[slot]);
+    }
+#endif
     // sequences with no context have no item: their rows are zero
     for (int sq = blockIdx.x; sq < nseq; sq += gridDim.x)
       if (nsplit_of[sq] == 0)
