@@ -141,6 +141,26 @@ __device__ __forceinline__ void mma_ts_steps(uint32_t tmem_d, uint32_t tmem_a, u
     sm100::mma_f16_ts(tmem_d, tmem_a + 8 * m, bdesc + 128 * m, idesc, m == 0 ? acc_first : 1u);
 }
 
+#ifdef KB_PF_CTA_TRACE
+// per-CTA %globaltimer stamps of one launch (tools/pf_cta_trace.py): 0 entry,
+// 1 first S seen (softmax warp 0), 2 last P published (warp 0), 3 exit; 4 SM id
+__device__ unsigned long long g_pf_cta[8192][5];
+__device__ __forceinline__ unsigned long long pf_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PF_CTA(slot)                                                                       \
+  do {                                                                                     \
+    const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);  \
+    if (cta_ < 8192) g_pf_cta[cta_][slot] = pf_gtimer();                                   \
+  } while (0)
+#else
+#define PF_CTA(slot) \
+  do {               \
+  } while (0)
+#endif
+
 #ifdef KB_PF_TRACE
 // per-tile clock64 stamps of one CTA (grid (0,0,0)), printed at its end:
 // [t][j][slot] -- 0 S ready (softmax), 1 p_lo published, 2 p_hi published,
@@ -212,6 +232,15 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
     return;
   }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) PF_CTA(0);
+#ifdef KB_PF_CTA_TRACE
+  if (tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const unsigned cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (cta_ < 8192) g_pf_cta[cta_][4] = smid;
+  }
+#endif
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -444,6 +473,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
       // lands on a completed, unobserved phase (compute-sanitizer synccheck)
       if (j > 0) mbar_wait(&misc->pv_lo[t], (j - 1) & 1);
       if ((warp & 3) == 0) PFT(0, t, j);
+      if (tid == 0 && j == 0) PF_CTA(1);
 #ifdef KB_PF_TIMING
       const long long tw1 = clock64();
       t_wait += tw1 - tw0;
@@ -689,6 +719,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
 #endif
       publish(&misc->p_hi[t]);
       if ((warp & 3) == 0) PFT(2, t, j);
+      if (tid == 0 && j == nt - 1) PF_CTA(2);
 #ifdef KB_PF_TIMING
       t_soft += clock64() - tw1;
 #endif
@@ -748,6 +779,7 @@ prefill_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16*
   }
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) PF_CTA(3);
   if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, kPfTmemCols);
@@ -888,3 +920,10 @@ extern "C" int kb_paged_prefill(kb_pool* p, int32_t layer, int32_t n_q_heads, ui
   }
   return pool_leave(p, st);
 }
+
+#ifdef KB_PF_CTA_TRACE
+extern "C" int kb_debug_pf_cta_trace(unsigned long long* out, int32_t n) {
+  if (n > 8192 * 5) n = 8192 * 5;
+  return cudaMemcpyFromSymbol(out, kb::g_pf_cta, (size_t)n * 8) == cudaSuccess ? 0 : -1;
+}
+#endif
