@@ -400,19 +400,12 @@ extern "C" int kb_paged_decode(kb_pool* p, int32_t layer, int32_t n_q_heads, uin
   #ifndef KB_DEC_FUSE_MIN_PAIRS_PER_SM_X4
 #define KB_DEC_FUSE_MIN_PAIRS_PER_SM_X4 2
 #endif
-// merge inside the attention kernel when the batch is large (>= 4
-  // (sequence, kv head) pairs per CTA; B200 A/B: 191 vs 200 us per Llama
-  // layer at 147 sequences, equal at 64, slower below: 26 vs 21 us at 4)
-#if KB_DEC_MERGE_WARP
   // the merge warp makes the in-kernel merge cheap: it wins from about half
   // a (sequence, kv head) pair per SM up (r4 A/B against the combine launch,
   // us per Llama layer: 64 sequences 72.6 vs 76.2, 32: 36.1 vs 37.4, 16:
   // 25.2 vs 25.5); below, the few pairs' last merges sit in the kernel's
   // tail, where the combine launch is cheaper (4 sequences: 10.8 vs 11.8)
   int fuse = (int64_t)nseq * Hkv >= (int64_t)KB_DEC_FUSE_MIN_PAIRS_PER_SM_X4 * grid / 4;
-#else
-  int fuse = (int64_t)nseq * Hkv >= 4LL * grid;
-#endif
   if (flags & KB_DECODE_COMBINE) fuse = 0;
   if (flags & KB_DECODE_FUSE) fuse = 1;
   rc = launch_decode_tc(p, layer, n_q_heads, q, grid, scale, part_o, part_ml,

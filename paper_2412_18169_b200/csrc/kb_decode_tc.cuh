@@ -37,15 +37,14 @@
 namespace kb {
 
 constexpr int kDecStages = 3;
-// KB_DEC_MERGE_WARP (default 1): a seventh warp merges the KV splits of a
-// (sequence, kv head) pair inside the kernel -- the fence, the counter
-// round trip and the partial loads leave the softmax warps, and no combine
-// launch follows the layer.  0: the round-1 split (merge on the softmax
-// warps for large batches, a combine launch otherwise).
-#ifndef KB_DEC_MERGE_WARP
-#define KB_DEC_MERGE_WARP 1
-#endif
-constexpr int kDecThreads = KB_DEC_MERGE_WARP ? 224 : 192;
+// Two instantiations per page size: kMW (the batch merges its KV splits in
+// the kernel) adds a seventh warp that does the merging -- the fence, the
+// counter round trip and the partial loads leave the softmax warps, and no
+// combine launch follows the layer; without it (small batches, where a
+// combine launch is cheaper than merges in the kernel's tail) the CTA keeps
+// its six warps and register budget (r4: the 224-thread build was 2-6%
+// slower at 4-16 sequences in combine mode).
+constexpr int dec_threads(bool mw) { return mw ? 224 : 192; }
 constexpr int kMRing = 8;  // merge jobs in flight per CTA
 constexpr int kTileTok = 128;
 constexpr int kStageBytes = 65536;       // K (32 KiB) + V (32 KiB) for 128 tokens
@@ -106,8 +105,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define DEC_TRACE_VAL(slot, v) ((void)0)
 #endif
 
-template <int kB>
-__global__ void __launch_bounds__(kDecThreads, 1)
+template <int kB, bool kMW>
+__global__ void __launch_bounds__(dec_threads(kMW), 1)
 decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* __restrict__ q,
                  const int32_t* __restrict__ bt, const DecodeItem* __restrict__ items,
                  const int32_t* __restrict__ n_items_ptr, int32_t* __restrict__ item_counter,
@@ -350,8 +349,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       if (lane == 0) mbar_arrive(&misc->ring_empty[r % kRing]);  // done with item r
       __syncwarp();
     }
-#if KB_DEC_MERGE_WARP
-  } else if (warp == 6) {
+  } else if (kMW && warp == 6) {
     // ------------------------------------------------ split merger
     // Jobs come from the softmax warps once a split's partial (O / l, m, l
     // rows) is written.  Lane 0 publishes it GPU-wide and counts the pair's
@@ -484,7 +482,6 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       }
       if (lane == 0) *done = 0;
     }
-#endif
   } else {
     // ------------------------------------------------ softmax / epilogue (tid < 128)
     // Q of an item: G rows (<= 8) x 16 chunks of 16 bytes, two per thread;
@@ -569,8 +566,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           }
         }
       }
-#if KB_DEC_MERGE_WARP
-      if (ns > 1 && fuse_merge) {
+      if (kMW && ns > 1) {
         // hand the split to the merge warp (its partial rows are written)
         named_bar_sync(1, 128);
         if (tid == 0) {
@@ -581,38 +577,6 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         }
         ++mjobs;
       }
-#else
-      if (ns > 1 && fuse_merge) {
-        // Split-KV merge, fused: the CTA that finishes the last split of
-        // (sequence, kv head) merges all of them (threadfence-reduction
-        // pattern) -- no combine launch per layer.  It re-arms the counter
-        // for the next layer's launch.  (Chosen for large batches only: the
-        // fence + counter per split item costs more than a combine launch
-        // when the items are short.)
-        __threadfence();
-        named_bar_sync(1, 128);
-        int32_t* done = split_done + pit.seq * Hkv + pit.h;
-        if (tid == 0) misc->last = atomicAdd(done, 1) == ns - 1;
-        named_bar_sync(1, 128);
-        if (misc->last) {
-          __threadfence();
-          for (int g = 0; g < G; ++g) {
-            const int64_t base = ((int64_t)pit.seq * Hq + pit.h * G + g) * max_splits;
-            float mstar = -INFINITY;
-            for (int s = 0; s < ns; ++s) mstar = fmaxf(mstar, __ldcg(part_ml + (base + s) * 2));
-            float l = 0.f, o = 0.f;
-            for (int s = 0; s < ns; ++s) {
-              const float ms = __ldcg(part_ml + (base + s) * 2);
-              const float w = ms == -INFINITY ? 0.f : exp2f(ms - mstar);
-              l += w * __ldcg(part_ml + (base + s) * 2 + 1);
-              o += w * __ldcg(part_o + (base + s) * 128 + tid);
-            }
-            out[(base / max_splits) * 128 + tid] = __float2bfloat16(l > 0.f ? o / l : 0.f);
-          }
-          if (tid == 0) *done = 0;
-        }
-      }
-#endif
       named_bar_sync(1, 128);  // lred / last are reused by the next item
       if (tid == 0) {
         if (pr < 3) DEC_TRACE(6 + pr);
@@ -754,14 +718,12 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       it = nxt;  // item r+1, read from the ring during item r
       have = nhave;
     }
-#if KB_DEC_MERGE_WARP
-    if (tid == 0) {  // no more jobs
+    if (kMW && tid == 0) {  // no more jobs
       const int slot = mjobs % kMRing;
       if (mjobs >= kMRing) mbar_wait(&misc->m_empty[slot], ((mjobs / kMRing) - 1) & 1);
       misc->m_job[slot] = make_int4(0, 0, 0, 0);
       mbar_arrive(&misc->m_full[slot]);
     }
-#endif
     // sequences with no context have no item: their rows are zero
     for (int sq = blockIdx.x; sq < nseq; sq += gridDim.x)
       if (nsplit_of[sq] == 0)
@@ -788,30 +750,25 @@ inline int launch_decode_tc(kb_pool* p, int layer, int Hq, uint64_t q, int grid,
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kDecThreads);
+  cfg.blockDim = dim3(dec_threads(fuse_merge != 0));
   cfg.dynamicSmemBytes = kDecSmem;
   cfg.stream = st;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  if (B == 64) {
-    int rc = ensure_smem_attr(reinterpret_cast<const void*>(decode_tc_kernel<64>), kDecSmem,
-                              p->device);
+  auto go = [&](auto kernel) -> int {
+    int rc = ensure_smem_attr(reinterpret_cast<const void*>(kernel), kDecSmem, p->device);
     if (rc) return rc;
-    KB_RT(cudaLaunchKernelEx(&cfg, decode_tc_kernel<64>,
+    KB_RT(cudaLaunchKernelEx(&cfg, kernel,
         p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt, items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
         reinterpret_cast<__nv_bfloat16*>(out), part_o,
         part_ml, Hkv,
         Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2, early_loads));
-  } else {
-    int rc = ensure_smem_attr(reinterpret_cast<const void*>(decode_tc_kernel<128>), kDecSmem,
-                              p->device);
-    if (rc) return rc;
-    KB_RT(cudaLaunchKernelEx(&cfg, decode_tc_kernel<128>,
-        p->kv_tmap, reinterpret_cast<const __nv_bfloat16*>(q), p->d_bt, items, n_items, item_counter, nsplit, split_done, nseq, fuse_merge,
-        reinterpret_cast<__nv_bfloat16*>(out), part_o,
-        part_ml, Hkv,
-        Hq / Hkv, Hq, p->m.num_layers, p->maxp, layer, max_splits, scale_log2, early_loads));
-  }
+    return KB_OK;
+  };
+  int rc;
+  if (B == 64) rc = fuse_merge ? go(decode_tc_kernel<64, true>) : go(decode_tc_kernel<64, false>);
+  else rc = fuse_merge ? go(decode_tc_kernel<128, true>) : go(decode_tc_kernel<128, false>);
+  if (rc) return rc;
   KB_LAUNCH_CHECK();
   return KB_OK;
 }
