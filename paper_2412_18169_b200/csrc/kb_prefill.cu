@@ -103,7 +103,7 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
 }
 // pairs i with i % kEmuEvery == kEmuEvery - 1 use exp2_fma2
 #ifndef KB_PF_EMU_EVERY
-#define KB_PF_EMU_EVERY 5
+#define KB_PF_EMU_EVERY 4
 #endif
 constexpr int kEmuEvery = KB_PF_EMU_EVERY;
 // P key pairs published with p_lo (the rest with p_hi): 32 = halves; 48 =
