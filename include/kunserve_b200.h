@@ -20,8 +20,13 @@
  *
  * Device layout
  *   weight VA : num_layers x slab_bytes, layer l at l*slab_bytes; one
- *               physical VMM handle (cuMemCreate) mapped per held layer.
- *   KV VA     : [slack pages | residual | dropped slab 0 | dropped slab 1 ...]
+ *               physical VMM handle (cuMemCreate) per layer slab, mapped at
+ *               pool creation under the weight VA AND under its alias in
+ *               the KV VA (drop / restore flip page availability; no
+ *               cuMemMap / cuMemUnmap on the hot path).
+ *   KV VA     : [slack pages | residual | alias of slab 0 | ... slab L-1]
+ *               (a slab's alias pages are free for KV only while its layer
+ *               is dropped; reserved otherwise)
  *               page p at kv_base + p*page_bytes; a page holds one layer of
  *               `block_tokens` tokens of one request:
  *               [K|V][n_kv_heads][block_tokens][head_dim], K bf16, V fp16
