@@ -371,7 +371,7 @@ def decode_measure(cyc, iters: int, hbm_peak: float):
     # merges the KV splits itself at this batch size) or attention + combine
     # (kb_paged_decode fuses from half a (sequence, kv head) pair per SM up:
     # KB_DEC_FUSE_MIN_PAIRS_PER_SM_X4 = 2, kb_decode.cu)
-    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     launches = sum(1 + (hi - lo) * (1 if 4 * q.shape[0] * pool.shape.n_kv_heads >= 2 * sms else 2)
                    for pool, lo, hi, q, *_ in work)
     gbs = algo_bytes / (ms / 1e3) / 1e9
