@@ -264,9 +264,13 @@ int kb_kv_append(kb_pool* pool, int32_t layer, uint64_t k, uint64_t v,
  * bound relative to it), and still store the fp16 rounding.
  * kb_pool_kv_status returns the flags of every append that has completed
  * (synchronize the appending stream first for an exact answer) and clears
- * them when `clear` != 0; the host shims raise ValueError on any flag. */
+ * them when `clear` != 0; the host shims raise ValueError on any flag.
+ * KB_KV_NO_PAGE: a row whose slot or position lies outside the block table,
+ * or whose page was never grown (kb_pages_grow), was skipped -- nothing is
+ * written outside the pool. */
 #define KB_KV_V_OVERFLOW 1u
 #define KB_KV_V_UNDERFLOW 2u
+#define KB_KV_NO_PAGE 4u
 int kb_pool_kv_status(kb_pool* pool, uint32_t* flags, int32_t clear);
 /* Decode: q [nseq][n_q_heads][head_dim] bf16, one query token per sequence
  * attending to ctx_lens[i] cached tokens of slot slots[i] (including its

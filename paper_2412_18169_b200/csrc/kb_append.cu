@@ -55,8 +55,8 @@ __device__ __forceinline__ uint32_t max_mag8(int4 v) {
 __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __restrict__ bt,
                                  const int4* __restrict__ k, const int4* __restrict__ v,
                                  const int32_t* __restrict__ slots, const int32_t* __restrict__ pos,
-                                 int ntok, int Hkv, int B, int L, int maxp, int layer,
-                                 int64_t page_bytes, int64_t row_vec,
+                                 int ntok, int Hkv, int B, int L, int maxp, int max_slots,
+                                 int layer, int64_t page_bytes, int64_t row_vec,
                                  uint32_t* __restrict__ status) {
   // the attention launch that follows (programmatic dependent launch) may
   // run its prologue now; it waits for this grid's writes before reading
@@ -66,7 +66,15 @@ __global__ void kv_append_kernel(uint8_t* __restrict__ kv, const int32_t* __rest
   if (warp >= ntok * Hkv) return;
   const int t = warp / Hkv, h = warp % Hkv;
   const int slot = slots[t], p = pos[t];
-  const int32_t page = bt[((int64_t)slot * L + layer) * maxp + p / B];
+  // a slot or position the block table does not cover, or a position whose
+  // page was never grown, would write outside the pool: skip the row and
+  // raise the sticky KB_KV_NO_PAGE word (warp-uniform: t and h are)
+  const bool in_table = slot >= 0 && slot < max_slots && p >= 0 && p / B < maxp;
+  const int32_t page = in_table ? bt[((int64_t)slot * L + layer) * maxp + p / B] : -1;
+  if (page < 0) {
+    if (lane == 0) *(volatile uint32_t*)(status + 2) = 1u;
+    return;
+  }
   const int row = p % B;
   const int which = lane >> 4;  // 0 = K, 1 = V
   const int4* src = (which ? v : k) + (int64_t)t * row_vec + h * 16 + (lane & 15);
@@ -114,7 +122,7 @@ extern "C" int kb_kv_append(kb_pool* p, int32_t layer, uint64_t k, uint64_t v, u
       reinterpret_cast<uint8_t*>(p->kva), p->d_bt, reinterpret_cast<const int4*>(k),
       reinterpret_cast<const int4*>(v), reinterpret_cast<const int32_t*>(slots),
       reinterpret_cast<const int32_t*>(pos), ntok, p->m.n_kv_heads, p->m.block_tokens,
-      p->m.num_layers, p->maxp, layer, p->m.page_bytes, stride / 8, p->d_status);
+      p->m.num_layers, p->maxp, p->max_slots, layer, p->m.page_bytes, stride / 8, p->d_status);
   KB_LAUNCH_CHECK();
   return pool_leave(p, (cudaStream_t)stream);
 }
@@ -123,10 +131,12 @@ extern "C" int kb_pool_kv_status(kb_pool* p, uint32_t* flags, int32_t clear) {
   if (!p || !flags) return fail(KB_EINVAL, "null argument");
   if (p->view) return refuse_view();
   volatile uint32_t* h = p->h_status;
-  *flags = (h[0] ? KB_KV_V_OVERFLOW : 0u) | (h[1] ? KB_KV_V_UNDERFLOW : 0u);
+  *flags = (h[0] ? KB_KV_V_OVERFLOW : 0u) | (h[1] ? KB_KV_V_UNDERFLOW : 0u) |
+           (h[2] ? KB_KV_NO_PAGE : 0u);
   if (clear) {
     h[0] = 0;
     h[1] = 0;
+    h[2] = 0;
   }
   return KB_OK;
 }

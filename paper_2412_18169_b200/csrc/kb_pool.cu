@@ -619,6 +619,7 @@ extern "C" int kb_pool_create(int32_t device, const kb_model_desc* model, int64_
     return bail(fail(KB_ECUDA, "cudaHostAlloc(status) failed"));
   p->h_status[0] = 0;  // KB_KV_V_OVERFLOW seen
   p->h_status[1] = 0;  // KB_KV_V_UNDERFLOW seen
+  p->h_status[2] = 0;  // KB_KV_NO_PAGE seen
   if (cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(KB_ECUDA, "cudaStreamCreate failed"));
   if (cudaEventCreateWithFlags(&p->counts_ev, cudaEventDisableTiming) != cudaSuccess ||

@@ -31,7 +31,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 KB_OK, KB_REFUSED = 0, 1
-KB_KV_V_OVERFLOW, KB_KV_V_UNDERFLOW = 1, 2
+KB_KV_V_OVERFLOW, KB_KV_V_UNDERFLOW, KB_KV_NO_PAGE = 1, 2, 4
 
 
 class ModelDesc(C.Structure):
@@ -313,11 +313,15 @@ class DevicePool:
 
     def check_kv_range(self, synchronize: bool = True) -> None:
         """Raise ValueError if any appended V value fell outside the fp16
-        cache's exact range (|v| in [2^-14, 65504] or 0); clears the flags."""
+        cache's exact range (|v| in [2^-14, 65504] or 0), or an append hit a
+        position with no page; clears the flags."""
         if synchronize:
             import torch
             torch.cuda.synchronize(self.rt.device)
         f = self.kv_status(clear=True)
+        if f & KB_KV_NO_PAGE:
+            raise ValueError(f"pool {self.iid}: kv_append to a slot / position without a "
+                             "page (outside the block table or never grown); the row was skipped")
         if f:
             what = []
             if f & KB_KV_V_OVERFLOW:

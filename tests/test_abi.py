@@ -32,6 +32,20 @@ def test_python_binding_covers_header():
     assert set(declared_symbols()) == set(runtime.EXPORTED)
 
 
+def test_header_flag_values_match_the_binding():
+    """Every flag #define the header declares has the same value in the
+    Python binding (the binding passes / decodes them as plain ints)."""
+    from paper_2412_18169_b200 import runtime
+    defs = dict(re.findall(r"#define (KB_(?:KV|DECODE)_[A-Z_0-9]+) (\d+)u?", open(HEADER).read()))
+    assert {"KB_KV_V_OVERFLOW", "KB_KV_V_UNDERFLOW", "KB_KV_NO_PAGE",
+            "KB_DECODE_REUSE_PLAN", "KB_DECODE_COMBINE", "KB_DECODE_FUSE"} <= set(defs)
+    for name, val in defs.items():
+        py = getattr(runtime, name, None)
+        if py is None:
+            py = getattr(runtime, name[len("KB_"):])
+        assert py == int(val), name
+
+
 def test_runtime_refuses_without_library(tmp_path, monkeypatch):
     # the product path must fail loudly, never fall back to the CPU
     import importlib

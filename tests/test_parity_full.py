@@ -196,6 +196,47 @@ def test_fp16_v_cache_range_guard(runtime, case):
     pool.close()
 
 
+def test_kv_append_without_page_is_skipped(runtime):
+    """Rows whose position has no grown page, or whose slot / position lies
+    outside the block table, are skipped (nothing written outside the pool)
+    and flagged KB_KV_NO_PAGE; the rows that do have pages land as usual."""
+    shape = SHAPES["tiny"]
+    model = shape.spec()
+    rt = runtime.Runtime(0, max_slots=4, max_pages_per_seq=4, slack_pages=16)
+    pool = rt.create_pool(0, model, model.param_bytes + MIB, shape)
+    assert pool.grow([(0, 0, 1, 2), (1, 0, 1, 4)])    # slot 0: tokens 0-127
+    g = torch.Generator().manual_seed(2)
+    k = torch.randn((256, 1, 128), generator=g).to(torch.bfloat16)
+    v = torch.randn((256, 1, 128), generator=g).to(torch.bfloat16)
+    _append(runtime, pool, 0, k, v, 1, 0)              # slot 1 filled, the bystander
+    torch.cuda.synchronize()
+    info = pool.info()
+
+    def page_hashes():
+        rows = {s: pool.block_table(s, 0) for s in (0, 1)}
+        idx = torch.tensor(rows[0] + rows[1], dtype=torch.int64, device="cuda")
+        return runtime.hash_segments(info.kv_base, pool.page_bytes, idx.numel(), index=idx).cpu()
+    before = page_hashes()
+    assert pool.kv_status() == 0
+    _append(runtime, pool, 0, k[:10], v[:10], 0, 120)   # 120-127 have a page, 128-129 not
+    torch.cuda.synchronize()
+    assert pool.kv_status() == runtime.KB_KV_NO_PAGE
+    with pytest.raises(ValueError, match="without a page"):
+        pool.check_kv_range()
+    assert pool.kv_status() == 0
+    after = page_hashes()
+    assert torch.equal(after[2:], before[2:])          # slot 1 untouched
+    assert not torch.equal(after[:2], before[:2])      # slot 0's rows 120-127 landed
+    for slot, p in ((9, 0), (-1, 0), (0, -1), (0, 4 * 64)):   # outside the table
+        runtime.kv_append(pool, 0, k[:1].cuda(), v[:1].cuda(),
+                          torch.tensor([slot], dtype=torch.int32, device="cuda"),
+                          torch.tensor([p], dtype=torch.int32, device="cuda"))
+        torch.cuda.synchronize()
+        assert pool.kv_status(clear=True) == runtime.KB_KV_NO_PAGE
+    assert torch.equal(page_hashes(), after)
+    pool.close()
+
+
 def test_decode_workspace_too_small_is_refused(runtime):
     shape = SHAPES["tiny"]
     model = shape.spec()
