@@ -329,7 +329,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
       const int b = item_bucket(len, s, splits_first);
       for (int h = 0; h < Hkv; ++h) {
         const int pos = atomicAdd(&cursor[b], 1);
-        items[pos] = DecodeItem{i, h, k, beg, len, slots[i], ctx[i], 0};
+        items[pos] = DecodeItem{i, h, k, beg, len, slots[i], ctx[i], s};
       }
     }
   }

@@ -57,10 +57,10 @@ constexpr uint32_t kDecTmemCols = 64;    // S0 S1 O0 O1, 16 columns each
 constexpr int kRing = 16;                // work items published ahead per CTA
 
 // one KV split of a (sequence, kv head) pair: tiles [t_beg, t_beg + nt);
-// the slot and context length ride along (one dependent load less before
-// the item's first TMA)
+// the slot, context length and the pair's split count ride along (no
+// dependent global load before the item's first TMA or in its epilogue)
 struct DecodeItem {
-  int32_t seq, h, split, t_beg, nt, slot, ctx, _pad;
+  int32_t seq, h, split, t_beg, nt, slot, ctx, ns;
 };
 
 struct DecodeMisc {
@@ -551,7 +551,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         if (lane == 0) misc->lred[warp][g] = v;
       }
       named_bar_sync(1, 128);
-      const int ns = nsplit_of[pit.seq];
+      const int ns = pit.ns;  // (a global load here sat on the softmax's path)
       for (int g = 0; g < G; ++g) {
         const float l = misc->lred[0][g] + misc->lred[1][g] + misc->lred[2][g] + misc->lred[3][g];
         const int64_t hrow = (int64_t)pit.seq * Hq + pit.h * G + g;
