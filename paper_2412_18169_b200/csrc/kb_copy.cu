@@ -188,7 +188,8 @@ extern "C" int kb_copy_pages(kb_pool* dst, kb_pool* src, const kb_move* moves, i
     const kb_move& mv = moves[i];
     if (mv.layer_lo < 0 || mv.layer_hi > L || mv.layer_hi <= mv.layer_lo || mv.npages < 0 ||
         mv.flat_lo < 0 || mv.flat_hi < mv.flat_lo ||
-        mv.flat_hi > (mv.layer_hi - mv.layer_lo) * mv.npages)
+        mv.flat_hi > (mv.layer_hi - mv.layer_lo) * mv.npages || mv.src_slot < 0 ||
+        mv.src_slot >= src->max_slots || mv.dst_slot < 0 || mv.dst_slot >= dst->max_slots)
       return fail(KB_EINVAL, "bad move " + std::to_string(i));
     for (int l = mv.layer_lo; l < mv.layer_hi; ++l) {
       if (src->h_np[(int64_t)mv.src_slot * L + l] < mv.npages ||

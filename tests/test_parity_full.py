@@ -234,6 +234,11 @@ def test_kv_append_without_page_is_skipped(runtime):
         torch.cuda.synchronize()
         assert pool.kv_status(clear=True) == runtime.KB_KV_NO_PAGE
     assert torch.equal(page_hashes(), after)
+    # page moves naming a slot outside either pool's table are refused on
+    # the host before anything is read
+    for src_slot, dst_slot in ((4, 1), (-1, 1), (1, 4), (1, -1)):
+        with pytest.raises(runtime.DeviceError, match="bad move"):
+            runtime.copy_pages(pool, pool, [(src_slot, dst_slot, 0, 1, 1, 0, 1)])
     pool.close()
 
 
