@@ -21,7 +21,7 @@ constexpr int kLenBuckets = 1024;
 #define KB_DEC_ITEMS_PER_CTA 2  // swept 1-8 on B200 with dynamic fetching: 1-2 best
 #endif
 constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per persistent CTA
-// ...except when the batch has 1.5-2.4 (sequence, kv head) pairs per CTA:
+// ...except when the batch has 1.25-2.4 (sequence, kv head) pairs per CTA:
 // two rounds then leave the pairs nearly unsplit and their lognormal lengths
 // unbalanced; three items per CTA split the long ones (B200 sweep over four
 // context draws, r3p: 32 sequences +1 to +9 pt of HBM, 40 about even; two
@@ -33,6 +33,14 @@ constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per per
 // the items are then whole pairs of similar length, and a second round only
 // adds a merge; r3r: +2 to +6 pt at 4-8 sequences, 2 items stay better at
 // 12-24).  Twice the items-per-CTA target there, an A/B knob:
+// lower bound of that range in eighths of a pair per CTA: 10 = 1.25 (r5
+// A/B over seven context draws: at 24 Llama sequences (1.30 pairs per CTA)
+// 3 items per CTA take 3.3% less time in sum (-0.6 to +10% per draw), at
+// 26 (1.41) 1-16% less over four draws; at 20-23 sequences (1.08-1.24) the
+// draws split both ways; was 12 = 1.5)
+#ifndef KB_DEC_IPC3_LO_X8
+#define KB_DEC_IPC3_LO_X8 10
+#endif
 #ifndef KB_DEC_TINY_IPC_X2
 #define KB_DEC_TINY_IPC_X2 2
 #endif
@@ -160,7 +168,8 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
   const bool splits_first = KB_DEC_SPLITS_FIRST && pairs < 2LL * grid_ctas;
   // items per CTA, doubled (the small-batch knob allows halves)
   const int ipc2 = !KB_DEC_ADAPT_IPC ? 2 * kItemsPerCta
-                   : (2 * pairs >= 3LL * grid_ctas && 5 * pairs <= 12LL * grid_ctas) ? 6
+                   : (8 * pairs >= (long long)KB_DEC_IPC3_LO_X8 * grid_ctas &&
+                      5 * pairs <= 12LL * grid_ctas) ? 6
                    : (2 * pairs < (long long)grid_ctas) ? KB_DEC_TINY_IPC_X2
                    : 2 * kItemsPerCta;
   if (tid == 0) total_tiles = 0;
