@@ -44,6 +44,10 @@ constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per per
 #ifndef KB_DEC_TINY_IPC_X2
 #define KB_DEC_TINY_IPC_X2 2
 #endif
+// ...and between half a pair and one pair per CTA (A/B knob, doubled)
+#ifndef KB_DEC_SUB1_IPC_X2
+#define KB_DEC_SUB1_IPC_X2 (2 * KB_DEC_ITEMS_PER_CTA)
+#endif
 #ifndef KB_DEC_MIN_TILES
 #define KB_DEC_MIN_TILES 2
 #endif
@@ -171,6 +175,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
                    : (8 * pairs >= (long long)KB_DEC_IPC3_LO_X8 * grid_ctas &&
                       5 * pairs <= 12LL * grid_ctas) ? 6
                    : (2 * pairs < (long long)grid_ctas) ? KB_DEC_TINY_IPC_X2
+                   : (pairs < (long long)grid_ctas) ? KB_DEC_SUB1_IPC_X2
                    : 2 * kItemsPerCta;
   if (tid == 0) total_tiles = 0;
   for (int i = tid; i < kMaxLayers; i += blockDim.x) item_counter[i] = 0;
