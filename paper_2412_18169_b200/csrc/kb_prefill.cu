@@ -834,16 +834,25 @@ prefill_combine_kernel(const uint8_t* __restrict__ part, const int32_t* __restri
   }
   __syncthreads();
   const int rows = min(kCombRows, qlen - row0);
-  // 16 threads per row, 8 fp16 (16 B) each
+  // 16 threads per row, 8 fp16 (16 B) each; every split's 16 bytes of a
+  // (row, chunk) are loaded before the first is used (up to 8 loads in
+  // flight per thread instead of one per split in turn)
+  const uint8_t* base = part + ((int64_t)unit * splits * kRows + rbase) * 256;
+  const int64_t split_stride = (int64_t)kRows * 256;
   for (int i = threadIdx.x; i < rows * 16; i += blockDim.x) {
     const int r = i >> 4, c8 = i & 15;
+    int4 v[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if (s < splits)
+        v[s] = __ldcs(reinterpret_cast<const int4*>(base + s * split_stride + (int64_t)r * 256) + c8);
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int s = 0; s < splits; ++s) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      if (s >= splits) break;
       const float w = s_w[r][s];
-      if (w == 0.f) continue;
-      const int4 v = reinterpret_cast<const int4*>(
-          part + (((int64_t)unit * splits + s) * kRows + rbase + r) * 256)[c8];
-      const __half2* h = reinterpret_cast<const __half2*>(&v);
+      if (w == 0.f) continue;  // a split with no keys for this row: never written
+      const __half2* h = reinterpret_cast<const __half2*>(&v[s]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 f = __half22float2(h[e]);
