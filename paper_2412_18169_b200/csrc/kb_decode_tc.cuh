@@ -17,8 +17,9 @@
 // every work item has at most T tiles -- T balancing the work over two items
 // per persistent CTA -- and orders items longest first.  CTA b starts with
 // item b, then fetches the next index from a per-layer counter (greedy
-// longest-processing-time); the producer copies each item into a
-// shared-memory ring for the MMA and softmax warps.  The TMA -> MMA ->
+// longest-processing-time) three tiles before its current item's last
+// load, so the CTAs that finish first take the next items; the producer
+// copies each item into a shared-memory ring for the MMA and softmax warps.  The TMA -> MMA ->
 // softmax pipeline runs continuously across items (the next item's Q is
 // staged one tile into the current one, and an item's epilogue runs after
 // the next item's first P is out), so HBM streaming never drains between
@@ -55,6 +56,19 @@ constexpr int kDecMiscBytes = 2048;
 constexpr int kDecSmem = kDecStages * kStageBytes + 2 * kQBytes + 2 * kPBytes + kDecMiscBytes + 1024;
 constexpr uint32_t kDecTmemCols = 64;    // S0 S1 O0 O1, 16 columns each
 constexpr int kRing = 16;                // work items published ahead per CTA
+// KB_DEC_LAZY_D > 0: claim item r+1 at item r's tile nt - D (producer) and
+// read it / load its Q at tile nt - DS (softmax); 0: the round-4 scheme
+// (item 1 claimed at the start, then two items ahead).  r5 A/B, us per
+// Llama layer at 4 / 16 / 32 / 64 / 147 sequences: 0: 10.59 / 25.09 /
+// 34.61 / 72.47 / 178.78; D = DS = 3: 10.54 / 24.33 / 33.96 / 70.99 /
+// 178.00 (kept); 4: 10.53 / 24.37 / 34.16 / 70.85 / 177.22; 5: 10.52 /
+// 24.98 / 34.10 / 71.19 / 177.64; 1: 10.39 / 24.62 / 35.05 / 72.95 / 180.63
+#ifndef KB_DEC_LAZY_D
+#define KB_DEC_LAZY_D 3
+#endif
+#ifndef KB_DEC_LAZY_DS
+#define KB_DEC_LAZY_DS KB_DEC_LAZY_D
+#endif
 
 // one KV split of a (sequence, kv head) pair: tiles [t_beg, t_beg + nt);
 // the slot, context length and the pair's split count ride along (no
@@ -267,7 +281,30 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
 
   if (warp == 4) {
     // ------------------------------------------------ TMA producer
-    if (lane == 0) {
+    if (lane == 0 && KB_DEC_LAZY_D > 0) {
+      // Lazy claims: item r+1 is claimed and published while item r's tile
+      // nt - KB_DEC_LAZY_D is issued -- one item ahead, late in the current
+      // one -- so the CTAs that finish first take the next items (a
+      // longest-processing-time queue), instead of every CTA holding two
+      // items claimed at its start.
+      if (published == 0) publish();  // item 0
+      int j = 0;
+      for (int r = 0;; ++r) {
+        DecodeItem it;
+        if (!get_item(r, it)) break;
+        if (r == 0) DEC_TRACE(2);
+        const int pub_t = max(it.nt - KB_DEC_LAZY_D, 0);
+        for (int t = 0; t < it.nt; ++t, ++j) {
+          if (!(r == 0 && t < npre)) {  // else issued before griddepcontrol.wait
+            const int stage = j % kDecStages;
+            if (j >= kDecStages) mbar_wait(&misc->empty[stage], ((j / kDecStages) - 1) & 1);
+            issue_tile(it, t, j);
+            if (j == 0) DEC_TRACE(3);
+          }
+          if (t == pub_t) publish();  // item r + 1
+        }
+      }
+    } else if (lane == 0) {
       if (published == 0) publish();  // item 0; item 1 once item 0's first loads are out
       bool second = npre > 0;
       if (second) publish();
@@ -695,7 +732,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
           store_q(r + 1);
           q_state = 2;
         }
-        if (q_state == 0) {
+        if (q_state == 0 && t >= (KB_DEC_LAZY_D > 0 ? max(it.nt - KB_DEC_LAZY_DS, 0) : 0)) {
           nhave = get_item(r + 1, nxt);
           q_state = 2;
           if (nhave) {
