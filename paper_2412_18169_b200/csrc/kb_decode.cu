@@ -21,7 +21,7 @@ constexpr int kLenBuckets = 1024;
 #define KB_DEC_ITEMS_PER_CTA 2  // swept 1-8 on B200 with dynamic fetching: 1-2 best
 #endif
 constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per persistent CTA
-// ...except when the batch has 1.25-2.4 (sequence, kv head) pairs per CTA:
+// ...except when the batch has 1.5-2.8 (sequence, kv head) pairs per CTA:
 // two rounds then leave the pairs nearly unsplit and their lognormal lengths
 // unbalanced; three items per CTA split the long ones (B200 sweep over four
 // context draws, r3p: 32 sequences +1 to +9 pt of HBM, 40 about even; two
@@ -29,18 +29,22 @@ constexpr int kItemsPerCta = KB_DEC_ITEMS_PER_CTA;  // target work items per per
 #ifndef KB_DEC_ADAPT_IPC
 #define KB_DEC_ADAPT_IPC 1
 #endif
+// lower bound of that range in eighths of a pair per CTA: 12 = 1.5 (r5:
+// before the lazy claims 1.25 measured 3.3% faster at 24 Llama sequences
+// over seven context draws; with them 1.5 is 2-10% faster there again)
+#ifndef KB_DEC_IPC3_LO_X8
+#define KB_DEC_IPC3_LO_X8 12
+#endif
+// upper bound in fifths of a pair per CTA: 14 = 2.8 (r5, with lazy claims:
+// 48 Llama sequences (2.6 pairs per CTA) 0.6-5% faster with 3 items, 56
+// (3.0) 2-3% slower; was 12 = 2.4)
+#ifndef KB_DEC_IPC3_HI_X5
+#define KB_DEC_IPC3_HI_X5 14
+#endif
 // ...and one item per CTA below half a pair per CTA (<= 9 Llama sequences:
 // the items are then whole pairs of similar length, and a second round only
 // adds a merge; r3r: +2 to +6 pt at 4-8 sequences, 2 items stay better at
 // 12-24).  Twice the items-per-CTA target there, an A/B knob:
-// lower bound of that range in eighths of a pair per CTA: 10 = 1.25 (r5
-// A/B over seven context draws: at 24 Llama sequences (1.30 pairs per CTA)
-// 3 items per CTA take 3.3% less time in sum (-0.6 to +10% per draw), at
-// 26 (1.41) 1-16% less over four draws; at 20-23 sequences (1.08-1.24) the
-// draws split both ways; was 12 = 1.5)
-#ifndef KB_DEC_IPC3_LO_X8
-#define KB_DEC_IPC3_LO_X8 10
-#endif
 #ifndef KB_DEC_TINY_IPC_X2
 #define KB_DEC_TINY_IPC_X2 2
 #endif
@@ -173,7 +177,7 @@ decode_plan_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ 
   // items per CTA, doubled (the small-batch knob allows halves)
   const int ipc2 = !KB_DEC_ADAPT_IPC ? 2 * kItemsPerCta
                    : (8 * pairs >= (long long)KB_DEC_IPC3_LO_X8 * grid_ctas &&
-                      5 * pairs <= 12LL * grid_ctas) ? 6
+                      5 * pairs <= (long long)KB_DEC_IPC3_HI_X5 * grid_ctas) ? 6
                    : (2 * pairs < (long long)grid_ctas) ? KB_DEC_TINY_IPC_X2
                    : (pairs < (long long)grid_ctas) ? KB_DEC_SUB1_IPC_X2
                    : 2 * kItemsPerCta;
