@@ -63,6 +63,12 @@ constexpr int kRing = 16;                // work items published ahead per CTA
 // 34.61 / 72.47 / 178.78; D = DS = 3: 10.54 / 24.33 / 33.96 / 70.99 /
 // 178.00 (kept); 4: 10.53 / 24.37 / 34.16 / 70.85 / 177.22; 5: 10.52 /
 // 24.98 / 34.10 / 71.19 / 177.64; 1: 10.39 / 24.62 / 35.05 / 72.95 / 180.63
+// KB_DEC_BT_PREFETCH: prefetch a published item's first block-table line
+// into L1 (r5 A/B: within +-0.2% at 4-147 sequences -- the border's page
+// lookup is not what an extra item costs; off)
+#ifndef KB_DEC_BT_PREFETCH
+#define KB_DEC_BT_PREFETCH 0
+#endif
 #ifndef KB_DEC_LAZY_D
 #define KB_DEC_LAZY_D 3
 #endif
@@ -244,6 +250,15 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
     if (idx >= 0) v = pre ? *pre : items[idx];
     misc->ring_it[slot] = v;
     mbar_arrive(&misc->ring_full[slot]);
+#if KB_DEC_BT_PREFETCH
+    // the item's first block-table entries into L1 now: its first tile's
+    // page lookup at the item border is then an L1 hit, not an L2 round
+    // trip behind a saturated memory system
+    if (idx >= 0 && r > 0) {
+      const int32_t* row = bt + ((int64_t)v.slot * L + layer) * maxp + v.t_beg * (kTileTok / kB);
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(row));
+    }
+#endif
   };
   // Launched with programmatic stream serialization: the prologue above
   // overlapped the previous kernel's tail.  With a reused plan
