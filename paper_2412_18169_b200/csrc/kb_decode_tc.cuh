@@ -27,7 +27,8 @@
 // griddepcontrol.wait.
 //
 // Warp roles (192 threads): 0-3 softmax / epilogue, 4 TMA producer,
-// 5 MMA issuer + TMEM owner.
+// 5 MMA issuer + TMEM owner; the merge-warp build adds 6 split merger and
+// 7 work-item claims (256 threads).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -45,7 +46,15 @@ constexpr int kDecStages = 3;
 // combine launch is cheaper than merges in the kernel's tail) the CTA keeps
 // its six warps and register budget (r4: the 224-thread build was 2-6%
 // slower at 4-16 sequences in combine mode).
-constexpr int dec_threads(bool mw) { return mw ? 224 : 192; }
+// KB_DEC_CLAIM_WARP (merge-warp builds): an eighth warp takes the lazy
+// claims (counter atomic + item load) off the TMA producer, which only
+// signals a request -- the producer never blocks on a claim's round trips
+// (r5 A/B, us per Llama layer at 16 / 32 / 64 / 147 sequences: 24.25 /
+// 33.80 / 70.62 / 177.04 without, 24.05 / 33.65 / 70.41 / 177.17 with)
+#ifndef KB_DEC_CLAIM_WARP
+#define KB_DEC_CLAIM_WARP 1
+#endif
+constexpr int dec_threads(bool mw) { return mw ? (KB_DEC_CLAIM_WARP ? 256 : 224) : 192; }
 constexpr int kMRing = 8;  // merge jobs in flight per CTA
 constexpr int kTileTok = 128;
 constexpr int kStageBytes = 65536;       // K (32 KiB) + V (32 KiB) for 128 tokens
@@ -96,6 +105,7 @@ struct DecodeMisc {
   uint64_t m_full[kMRing];   // merge job published by the softmax warps
   uint64_t m_empty[kMRing];  // merge warp has read the job
   int4 m_job[kMRing];        // {seq, h, ns, 1}; {.., 0}: no more jobs
+  uint64_t creq;             // claim requests, producer -> claim warp
   uint32_t tmem_base;
   int32_t last;  // this CTA finished the last split of its (sequence, kv head)
   float red[2][4][8];
@@ -172,6 +182,7 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
         mbar_init(&misc->m_full[r], 1);
         mbar_init(&misc->m_empty[r], 1);
       }
+      mbar_init(&misc->creq, 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -316,7 +327,12 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
             issue_tile(it, t, j);
             if (j == 0) DEC_TRACE(3);
           }
-          if (t == pub_t) publish();  // item r + 1
+          if (t == pub_t) {  // item r + 1
+            if (kMW && KB_DEC_CLAIM_WARP)
+              mbar_arrive(&misc->creq);
+            else
+              publish();
+          }
         }
       }
     } else if (lane == 0) {
@@ -400,6 +416,20 @@ decode_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __nv_bfloat16* 
       }
       if (lane == 0) mbar_arrive(&misc->ring_empty[r % kRing]);  // done with item r
       __syncwarp();
+    }
+  } else if (kMW && KB_DEC_CLAIM_WARP && warp == 7) {
+    // ------------------------------------------------ claims (items >= 1)
+    if (lane == 0 && KB_DEC_LAZY_D > 0) {
+      n_items = *n_items_ptr;
+      published = 1;  // item 0 is the producer's
+      mbar_wait(&misc->ring_full[0], 0);
+      if (misc->ring_it[0].nt > 0) {
+        for (int k = 0;; ++k) {
+          mbar_wait(&misc->creq, k & 1);
+          publish();
+          if (exhausted) break;
+        }
+      }
     }
   } else if (kMW && warp == 6) {
     // ------------------------------------------------ split merger
